@@ -1,0 +1,1553 @@
+// capi.cu -- the host engine behind include/svmb200.h (the C ABI): validation, problem building
+// (a0), the working-set loop driver around the persistent kernel (a1-a3), certification and bias
+// (a4), model assembly (a5) and batched predict (a6).  Every arithmetic step of the path runs in
+// the CUDA kernels of smo.cu / layout.cu / predict.cu; this file allocates, copies and launches.
+//
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.  Readings and layouts: DESIGN.md.
+#include "../../include/svmb200.h"
+#include "layout.cuh"
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+// ================================================================ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            return fail(e_ == cudaErrorMemoryAllocation ? SVM_ENOMEM : SVM_ECUDA,         \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,  \
+                        __LINE__);                                                        \
+        }                                                                                 \
+    } while (0)
+
+#define TRY(expr)                   \
+    do {                            \
+        int rc_ = (expr);           \
+        if (rc_ != SVM_OK) return rc_; \
+    } while (0)
+
+// ================================================================ device memory (RAII)
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    int alloc(size_t b)
+    {
+        release();
+        if (b == 0) b = 16;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            return fail(SVM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", b, cudaGetErrorString(e));
+        }
+        bytes = b;
+        return SVM_OK;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+static bool is_device_ptr(const void* p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// copy n elements of T from (host or device) src into a new device buffer
+template <class T>
+static int to_device(DBuf& dst, const T* src, int64_t n, cudaStream_t st)
+{
+    TRY(dst.alloc(sizeof(T) * (size_t)std::max<int64_t>(n, 1)));
+    if (n > 0)
+        CK(cudaMemcpyAsync(dst.p, src, sizeof(T) * n,
+                           is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    return SVM_OK;
+}
+
+template <class T>
+static int to_host(std::vector<T>& dst, const T* src, int64_t n, cudaStream_t st)
+{
+    dst.resize((size_t)std::max<int64_t>(n, 0));
+    if (n > 0) {
+        CK(cudaMemcpyAsync(dst.data(), src, sizeof(T) * n,
+                           is_device_ptr(src) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return SVM_OK;
+}
+
+static int sm_count()
+{
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 1;
+}
+
+static double now_ms()
+{
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ================================================================ parameters
+extern "C" int svm_params_default(svm_params* p, int64_t d)
+{
+    if (!p || d < 1) return fail(SVM_EINVAL, "svm_params_default: NULL params or d < 1");
+    memset(p, 0, sizeof *p);
+    p->type = SVM_C_CLASSIFICATION;
+    p->kernel = SVM_RADIAL;
+    p->cost = 1.0;
+    p->gamma = 1.0 / (double)d;
+    p->degree = 3;
+    p->coef0 = 0.0;
+    p->epsilon = 0.1;
+    p->tolerance = 1e-3;          // e1071 default
+    p->working_set = 16;
+    p->max_iter = 0;
+    p->layout = SVM_ROW_MAJOR;
+    p->certify = -1;
+    p->stream = nullptr;
+    return SVM_OK;
+}
+
+static int check_params(const svm_params* p, int64_t n, int64_t d)
+{
+    if (!p) return fail(SVM_EINVAL, "params is NULL");
+    if (n < 2) return fail(SVM_EINVAL, "need n >= 2 training rows (got %lld)", (long long)n);
+    if (d < 1) return fail(SVM_EINVAL, "need d >= 1 features (got %lld)", (long long)d);
+    if (d > 3072) return fail(SVM_EINVAL, "d = %lld exceeds the fused pass limit of 3072", (long long)d);
+    if (p->type != SVM_C_CLASSIFICATION && p->type != SVM_EPS_REGRESSION)
+        return fail(SVM_EINVAL, "type must be SVM_C_CLASSIFICATION or SVM_EPS_REGRESSION");
+    if (p->kernel < SVM_LINEAR || p->kernel > SVM_SIGMOID) return fail(SVM_EINVAL, "bad kernel");
+    if (!(p->cost > 0.0) || !std::isfinite(p->cost)) return fail(SVM_EINVAL, "cost must be > 0");
+    if (!std::isfinite(p->gamma)) return fail(SVM_EINVAL, "gamma must be finite");
+    if (p->kernel == SVM_POLYNOMIAL && p->degree < 1) return fail(SVM_EINVAL, "degree must be >= 1");
+    if (!(p->epsilon >= 0.0) || !std::isfinite(p->epsilon)) return fail(SVM_EINVAL, "epsilon must be >= 0");
+    if (!(p->tolerance > 0.0) || !std::isfinite(p->tolerance))
+        return fail(SVM_EINVAL, "tolerance must be > 0");
+    if (p->working_set < 2 || p->working_set > SVM_WS || (p->working_set & 1))
+        return fail(SVM_EINVAL, "working_set must be even and in [2, 16] (got %d)", p->working_set);
+    if (p->layout != SVM_ROW_MAJOR && p->layout != SVM_COL_MAJOR) return fail(SVM_EINVAL, "bad layout");
+    if (!(p->coef0 == p->coef0)) return fail(SVM_EINVAL, "coef0 is NaN");
+    return SVM_OK;
+}
+
+static KParams kparams(const svm_params* p, int64_t d)
+{
+    KParams k;
+    k.kernel = p->kernel;
+    k.degree = p->degree;
+    k.gamma64 = p->gamma > 0.0 ? p->gamma : 1.0 / (double)d;
+    k.coef064 = p->coef0;
+    k.gamma = (float)k.gamma64;
+    k.coef0 = (float)p->coef0;
+    return k;
+}
+
+// ================================================================ training data on the device
+struct Data {
+    int64_t n = 0, d = 0, n_pad = 0, rows_per_cta = 0, nnz = 0;
+    int nblk = 0;
+    bool csr = false;
+    DBuf XT, XR_own, norms, indptr_own, indices_own, vals_own;
+    const float* XR = nullptr;            // row-major rows (owned or borrowed)
+    const int64_t* indptr = nullptr;      // CSR (owned or borrowed)
+    const int32_t* indices = nullptr;
+    const float* vals = nullptr;
+};
+
+static int pick_nblk(int64_t n)
+{
+    const char* env = getenv("SVMB200_NBLK");
+    int sms = sm_count();
+    if (env && atoi(env) > 0) return std::min(atoi(env), sms);
+    int64_t want = (n + 255) / 256;  // >= 256 rows per CTA before using more SMs
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, sms));
+}
+
+static void set_geometry(Data& D, int64_t n, int nblk)
+{
+    D.nblk = nblk;
+    int64_t per = (n + nblk - 1) / nblk;
+    D.rows_per_cta = (per + 3) / 4 * 4;
+    D.n_pad = D.rows_per_cta * nblk;
+}
+
+static int check_bad_flag(DBuf& flag, cudaStream_t st, int code, const char* what)
+{
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h) return fail(code, "%s", what);
+    return SVM_OK;
+}
+
+static int build_dense(Data& D, const float* X, int64_t n, int64_t d, int layout, int nblk,
+                       cudaStream_t st)
+{
+    if (!X) return fail(SVM_EINVAL, "X is NULL");
+    D.n = n;
+    D.d = d;
+    D.csr = false;
+    set_geometry(D, n, nblk);
+    TRY(D.XT.alloc(sizeof(float) * D.n_pad * d));
+    TRY(D.norms.alloc(sizeof(float) * D.n_pad));
+    bool dev = is_device_ptr(X);
+    DBuf tmp;
+    const float* Xd = X;
+    if (!dev) {
+        TRY(tmp.alloc(sizeof(float) * n * d));
+        CK(cudaMemcpyAsync(tmp.p, X, sizeof(float) * n * d, cudaMemcpyHostToDevice, st));
+        Xd = tmp.as<float>();
+    }
+    if (layout == SVM_ROW_MAJOR) {
+        CK(lay_rowmajor_to_XT(Xd, n, d, D.XT.as<float>(), D.n_pad, st));
+        if (dev) D.XR = X;  // borrowed for the call
+        else {
+            D.XR_own.p = tmp.p;  // keep the uploaded row-major copy
+            D.XR_own.bytes = tmp.bytes;
+            tmp.p = nullptr;
+            D.XR = D.XR_own.as<float>();
+        }
+    } else {
+        CK(lay_colmajor_to_XT(Xd, n, d, D.XT.as<float>(), D.n_pad, st));
+        TRY(D.XR_own.alloc(sizeof(float) * n * d));
+        CK(lay_XT_to_rowmajor(D.XT.as<float>(), n, d, D.n_pad, D.XR_own.as<float>(), st));
+        D.XR = D.XR_own.as<float>();
+    }
+    DBuf bad;
+    TRY(bad.alloc(sizeof(int)));
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    CK(lay_check_finite(D.XT.as<float>(), D.n_pad * d, bad.as<int>(), st));
+    TRY(check_bad_flag(bad, st, SVM_ENONFINITE, "X contains a non-finite value"));
+    CK(lay_norms_XT(D.XT.as<float>(), n, d, D.n_pad, D.norms.as<float>(), st));
+    return SVM_OK;
+}
+
+static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, const float* data,
+                     int64_t n, int64_t d, int nblk, cudaStream_t st)
+{
+    if (!indptr || !indices || !data) return fail(SVM_EINVAL, "CSR arrays must not be NULL");
+    D.n = n;
+    D.d = d;
+    D.csr = true;
+    set_geometry(D, n, nblk);
+    // nnz from indptr[n]
+    int64_t nnz = 0, first = 0;
+    if (is_device_ptr(indptr)) {
+        CK(cudaMemcpyAsync(&nnz, indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&first, indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        nnz = indptr[n];
+        first = indptr[0];
+    }
+    if (first != 0 || nnz < 0) return fail(SVM_EINVAL, "CSR indptr[0] must be 0 and indptr[n] >= 0");
+    D.nnz = nnz;
+    if (is_device_ptr(indptr)) D.indptr = indptr;
+    else { TRY(to_device(D.indptr_own, indptr, n + 1, st)); D.indptr = D.indptr_own.as<int64_t>(); }
+    if (is_device_ptr(indices)) D.indices = indices;
+    else { TRY(to_device(D.indices_own, indices, nnz, st)); D.indices = D.indices_own.as<int32_t>(); }
+    if (is_device_ptr(data)) D.vals = data;
+    else { TRY(to_device(D.vals_own, data, nnz, st)); D.vals = D.vals_own.as<float>(); }
+    DBuf bad;
+    TRY(bad.alloc(sizeof(int)));
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    CK(lay_check_csr(D.indptr, D.indices, n, d, nnz, bad.as<int>(), st));
+    TRY(check_bad_flag(bad, st, SVM_EINVAL,
+                       "CSR invariants violated (indptr non-decreasing, columns strictly increasing "
+                       "within a row and < d)"));
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    CK(lay_check_finite(D.vals, nnz, bad.as<int>(), st));
+    TRY(check_bad_flag(bad, st, SVM_ENONFINITE, "X contains a non-finite value"));
+    TRY(D.norms.alloc(sizeof(float) * D.n_pad));
+    CK(lay_norms_csr(D.indptr, D.vals, n, D.n_pad, D.norms.as<float>(), st));
+    return SVM_OK;
+}
+
+// ================================================================ one binary problem (Eq. 2)
+struct Exchange {
+    int L = 0;
+    DBuf keys, pay, flags, info;
+    uint32_t epoch = 0;
+    int alloc(int L_)
+    {
+        L = L_;
+        TRY(keys.alloc(sizeof(uint64_t) * 2 * L * 16));
+        TRY(pay.alloc(sizeof(CandPay) * 2 * L * 16));
+        TRY(flags.alloc(sizeof(uint32_t) * L));
+        TRY(info.alloc(sizeof(SmoInfo)));
+        CK(cudaMemset(flags.p, 0, sizeof(uint32_t) * L));
+        CK(cudaMemset(keys.p, 0, keys.bytes));
+        return SVM_OK;
+    }
+};
+
+struct Problem {
+    int ncopy = 1;
+    double C = 1, eps = 0.1, tol = 1e-3;
+    int q = 16;
+    int64_t max_iter = 0;
+    KParams kp;
+    DBuf alpha, G, status, yv;   // yv: +-1 labels or z, fp32 [n]
+    int64_t iterations = 0;
+    double m_up = 0, M_low = 0;
+    bool converged = false, certified = false;
+    double loop_ms = 0, cert_ms = 0;
+    SmoInfo last_info;
+};
+
+static int problem_init(Problem& P, const Data& D, const float* yv_host, const svm_params* prm,
+                        cudaStream_t st)
+{
+    P.ncopy = prm->type == SVM_EPS_REGRESSION ? 2 : 1;
+    P.C = prm->cost;
+    P.eps = prm->epsilon;
+    P.tol = prm->tolerance;
+    P.q = prm->working_set;
+    int64_t m = D.n * P.ncopy;
+    P.max_iter = prm->max_iter > 0 ? prm->max_iter : std::max<int64_t>(10 * m, 10000);
+    P.kp = kparams(prm, D.d);
+    TRY(P.alpha.alloc(sizeof(double) * D.n_pad * P.ncopy));
+    TRY(P.G.alloc(sizeof(float) * D.n_pad * P.ncopy));
+    TRY(P.status.alloc(D.n_pad * P.ncopy));
+    TRY(to_device(P.yv, yv_host, D.n, st));
+    CK(lay_init_state(P.yv.as<float>(), D.n, D.n_pad, P.ncopy, P.eps, P.C, P.alpha.as<double>(),
+                      P.G.as<float>(), P.status.as<uint8_t>(), st));
+    return SVM_OK;
+}
+
+// Peer view of a sharded run (world = 1 when NULL).
+struct ShardCtx {
+    int rank = 0, world = 1;
+    int64_t row0 = 0, n_global = 0;
+    int64_t rank_row0[SVM_MAX_RANKS + 1] = {};
+    const float* XR[SVM_MAX_RANKS] = {};
+    const float* norms[SVM_MAX_RANKS] = {};
+    const int64_t* indptr[SVM_MAX_RANKS] = {};
+    const int32_t* indices[SVM_MAX_RANKS] = {};
+    const float* vals[SVM_MAX_RANKS] = {};
+    uint64_t* keys[SVM_MAX_RANKS] = {};
+    CandPay* pay[SVM_MAX_RANKS] = {};
+    uint32_t* flags[SVM_MAX_RANKS] = {};
+};
+
+static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx* sc = nullptr)
+{
+    SmoArgs a;
+    memset(&a, 0, sizeof a);
+    a.XT = D.csr ? nullptr : D.XT.as<float>();
+    a.indptr = D.indptr;
+    a.indices = D.indices;
+    a.vals = D.vals;
+    a.xnorm = D.norms.as<float>();
+    a.n_local = D.n;
+    a.n_pad = D.n_pad;
+    a.d = D.d;
+    a.row0 = 0;
+    a.n_global = D.n;
+    a.rows_per_cta = D.rows_per_cta;
+    a.ncopy = P.ncopy;
+    a.rpt = (!D.csr && D.rows_per_cta >= 4 * 32 * SMO_WARPS) ? 4 : 1;
+    if (const char* e = getenv("SVMB200_RPT")) a.rpt = (atoi(e) == 4 && !D.csr) ? 4 : 1;
+    a.alpha = P.alpha.as<double>();
+    a.G = P.G.as<float>();
+    a.status = P.status.as<uint8_t>();
+    a.C = P.C;
+    a.tol = P.tol;
+    a.inner_tol = std::max(0.1 * P.tol, 1e-10);  // DESIGN.md reading R2
+    a.inner_max = 64 * P.q;
+    a.q = P.q;
+    a.kp = P.kp;
+    a.rank = 0;
+    a.world = 1;
+    a.nblk = D.nblk;
+    a.rank_row0[0] = 0;
+    a.rank_row0[1] = D.n;
+    a.peer_XR[0] = D.XR;
+    a.peer_xnorm[0] = D.norms.as<float>();
+    a.peer_indptr[0] = D.indptr;
+    a.peer_indices[0] = D.indices;
+    a.peer_vals[0] = D.vals;
+    a.peer_keys[0] = E.keys.as<uint64_t>();
+    a.peer_pay[0] = E.pay.as<CandPay>();
+    a.peer_flags[0] = E.flags.as<uint32_t>();
+    a.timeout_ns = 30ull * 1000000000ull;
+    a.info = E.info.as<SmoInfo>();
+    if (sc && sc->world > 1) {
+        a.rank = sc->rank;
+        a.world = sc->world;
+        a.row0 = sc->row0;
+        a.n_global = sc->n_global;
+        for (int r = 0; r <= sc->world; ++r) a.rank_row0[r] = sc->rank_row0[r];
+        for (int r = 0; r < sc->world; ++r) {
+            a.peer_XR[r] = sc->XR[r];
+            a.peer_xnorm[r] = sc->norms[r];
+            a.peer_indptr[r] = sc->indptr[r];
+            a.peer_indices[r] = sc->indices[r];
+            a.peer_vals[r] = sc->vals[r];
+            a.peer_keys[r] = sc->keys[r];
+            a.peer_pay[r] = sc->pay[r];
+            a.peer_flags[r] = sc->flags[r];
+        }
+        a.timeout_ns = 60ull * 1000000000ull;
+    }
+    return a;
+}
+
+// Run up to max_iter iterations of the persistent loop; accumulates into P.
+static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cudaStream_t st,
+                    SmoInfo* info_out, const ShardCtx* sc = nullptr)
+{
+    SmoArgs a = make_args(D, P, E, sc);
+    a.tag0 = E.epoch;
+    a.max_iter = max_iter;
+    CK(cudaMemsetAsync(E.info.p, 0, sizeof(SmoInfo), st));
+    int smem = smo_smem_bytes(D.d, a.world, D.nblk);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    cudaError_t le = launch_smo(a, smem, st);
+    if (le != cudaSuccess) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return fail(SVM_ECUDA, "persistent working-set kernel launch failed: %s (smem %d B, %d CTAs)",
+                    cudaGetErrorString(le), smem, D.nblk);
+    }
+    CK(cudaEventRecord(e1, st));
+    SmoInfo info;
+    CK(cudaMemcpyAsync(&info, E.info.p, sizeof info, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (info.error) return fail(SVM_ETIMEOUT, "working-set exchange timed out (a rank stopped)");
+    E.epoch += (uint32_t)info.iterations + 1;
+    P.iterations += info.iterations;
+    P.m_up = info.m_up;
+    P.M_low = info.M_low;
+    P.converged = info.converged != 0;
+    P.loop_ms += ms;
+    P.last_info = info;
+    if (info_out) *info_out = info;
+    return SVM_OK;
+}
+
+// Per-row coefficients of problem P (device, fp64[n]) and the SV flags they imply.
+static int problem_coef(const Data& D, const Problem& P, DBuf& coef, DBuf& flag, cudaStream_t st)
+{
+    TRY(coef.alloc(sizeof(double) * D.n));
+    CK(lay_coef(P.alpha.as<double>(), P.status.as<uint8_t>(), D.n, D.n_pad, P.ncopy, P.C,
+                coef.as<double>(), flag.as<uint8_t>(), st));
+    return SVM_OK;
+}
+
+// Stream compaction of flagged rows -> device index list; returns count.
+static int compact(const DBuf& flag, int64_t n, DBuf& idx, int64_t* count, cudaStream_t st)
+{
+    int nb = 0;
+    DBuf cnt;
+    TRY(cnt.alloc(sizeof(int32_t) * ((n + 1023) / 1024 + 1)));
+    CK(lay_count_flags(flag.as<uint8_t>(), n, cnt.as<int32_t>(), &nb, st));
+    std::vector<int32_t> hc(nb);
+    CK(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> offs(nb);
+    int64_t tot = 0;
+    for (int i = 0; i < nb; ++i) { offs[i] = tot; tot += hc[i]; }
+    DBuf doffs;
+    TRY(to_device(doffs, offs.data(), nb, st));
+    TRY(idx.alloc(sizeof(int64_t) * std::max<int64_t>(tot, 1)));
+    CK(lay_scatter_flags(flag.as<uint8_t>(), n, doffs.as<int64_t>(), idx.as<int64_t>(), st));
+    CK(cudaStreamSynchronize(st));
+    *count = tot;
+    return SVM_OK;
+}
+
+// Feature-major SV block (+ norms) for a given row index list; nsv_pad multiple of 64.
+static int gather_rows_T(const Data& D, const DBuf& idx, int64_t nsv, int64_t nsv_pad, DBuf& SVT,
+                         DBuf& svn, cudaStream_t st)
+{
+    TRY(SVT.alloc(sizeof(float) * D.d * nsv_pad));
+    TRY(svn.alloc(sizeof(float) * nsv_pad));
+    if (!D.csr) {
+        CK(lay_gather_sv(D.XT.as<float>(), D.n_pad, D.d, D.norms.as<float>(), idx.as<int64_t>(), nsv,
+                         nsv_pad, SVT.as<float>(), svn.as<float>(), st));
+    } else {
+        CK(cudaMemsetAsync(SVT.p, 0, SVT.bytes, st));
+        CK(lay_csr_to_XT(D.indptr, D.indices, D.vals, idx.as<int64_t>(), nsv, 0, SVT.as<float>(),
+                         nsv_pad, st));
+        // norms of the gathered rows: reuse the SV gather of norms through a dense zero XT is not
+        // possible for CSR; gather norms directly
+        CK(lay_gather_sv(nullptr, 0, 0, D.norms.as<float>(), idx.as<int64_t>(), nsv, nsv_pad,
+                         nullptr, svn.as<float>(), st));
+    }
+    return SVM_OK;
+}
+
+// Decision sums F[i] = sum_s coef_s K(sv_s, x_i) over the TRAINING rows (fp64 accumulation).
+static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, int64_t nsv,
+                             int64_t nsv_pad, const DBuf& coef_sv, const KParams& kp, DBuf& F,
+                             cudaStream_t st)
+{
+    TRY(F.alloc(sizeof(double) * D.n));
+    // queries = training rows in feature-major form; dense: X^T (n_pad is a multiple of 4 but the
+    // predict tile needs 128) -> process through a padded view when needed
+    int64_t nq_pad = (D.n + 127) / 128 * 128;
+    DBuf QT, qn;
+    const float* qT = nullptr;
+    const float* qnorm = nullptr;
+    int64_t ld = 0;
+    if (!D.csr && D.n_pad % 128 == 0) {
+        qT = D.XT.as<float>();
+        qnorm = D.norms.as<float>();
+        ld = D.n_pad;
+    } else {
+        TRY(QT.alloc(sizeof(float) * D.d * nq_pad));
+        TRY(qn.alloc(sizeof(float) * nq_pad));
+        CK(cudaMemsetAsync(QT.p, 0, QT.bytes, st));
+        CK(cudaMemsetAsync(qn.p, 0, qn.bytes, st));
+        if (D.csr) {
+            CK(lay_csr_to_XT(D.indptr, D.indices, D.vals, nullptr, D.n, 0, QT.as<float>(), nq_pad, st));
+        } else {
+            for (int64_t k = 0; k < D.d; ++k)
+                CK(cudaMemcpyAsync(QT.as<float>() + k * nq_pad, D.XT.as<float>() + k * D.n_pad,
+                                   sizeof(float) * D.n, cudaMemcpyDeviceToDevice, st));
+        }
+        CK(cudaMemcpyAsync(qn.p, D.norms.p, sizeof(float) * D.n, cudaMemcpyDeviceToDevice, st));
+        qT = QT.as<float>();
+        qnorm = qn.as<float>();
+        ld = nq_pad;
+    }
+    CK(pred_decision(qT, qnorm, D.n, ld, SVT.as<float>(), svn.as<float>(), nsv, nsv_pad, D.d,
+                     coef_sv.as<double>(), 1, kp, F.as<double>(), st));
+    return SVM_OK;
+}
+
+struct Reduced {
+    double m_up, M_low, free_sum, free_cnt, dual;
+};
+
+static int reduce_state(const Data& D, const Problem& P, Reduced* r, cudaStream_t st)
+{
+    DBuf out;
+    TRY(out.alloc(sizeof(double) * 5));
+    CK(lay_reduce_state(P.alpha.as<double>(), P.G.as<float>(), P.status.as<uint8_t>(),
+                        P.yv.as<float>(), D.n, D.n_pad, P.ncopy, P.eps, P.C, out.as<double>(), st));
+    double h[5];
+    CK(cudaMemcpyAsync(h, out.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *r = {h[0], h[1], h[2], h[3], h[4]};
+    return SVM_OK;
+}
+
+static bool want_certify(const svm_params* prm, int64_t n, int64_t nsv, int64_t d)
+{
+    if (prm->certify == 0) return false;
+    if (prm->certify > 0) return true;
+    return (double)n * (double)nsv * (double)d <= 4e13;
+}
+
+// Certification (a4): recompute G = Q a + p from the support vectors with fp64 accumulation and
+// re-measure the violation; returns it in *viol.
+static int certify(const Data& D, Problem& P, double* viol, cudaStream_t st)
+{
+    double t0 = now_ms();
+    DBuf coef, flag, idx, SVT, svn, coef_sv, F;
+    TRY(flag.alloc(D.n));
+    CK(cudaMemsetAsync(flag.p, 0, D.n, st));
+    TRY(problem_coef(D, P, coef, flag, st));
+    int64_t nsv = 0;
+    TRY(compact(flag, D.n, idx, &nsv, st));
+    int64_t nsv_pad = std::max<int64_t>(64, (nsv + 63) / 64 * 64);
+    TRY(gather_rows_T(D, idx, nsv, nsv_pad, SVT, svn, st));
+    TRY(coef_sv.alloc(sizeof(double) * nsv_pad));
+    CK(lay_gather_coef(coef.as<double>(), idx.as<int64_t>(), nsv, nsv_pad, coef_sv.as<double>(), st));
+    TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef_sv, P.kp, F, st));
+    CK(pred_refresh_G(F.as<double>(), P.yv.as<float>(), P.status.as<uint8_t>(), D.n, D.n_pad,
+                      P.ncopy, P.eps, P.G.as<float>(), st));
+    Reduced r;
+    TRY(reduce_state(D, P, &r, st));
+    P.m_up = r.m_up;
+    P.M_low = r.M_low;
+    *viol = r.m_up - r.M_low;
+    P.certified = true;
+    P.cert_ms += now_ms() - t0;
+    return SVM_OK;
+}
+
+// The full solve of one problem: loop to tolerance, then certification + resume (a4).
+static int solve_problem(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
+                         cudaStream_t st)
+{
+    TRY(run_loop(D, P, E, P.max_iter, st, nullptr));
+    for (int round = 0; round < 4; ++round) {
+        if (!P.converged || prm->certify == 0) break;
+        if (prm->certify < 0) {  // auto: only when one pass over n x n_SV is affordable
+            DBuf coef, flag, idx;
+            TRY(flag.alloc(D.n));
+            CK(cudaMemsetAsync(flag.p, 0, D.n, st));
+            TRY(problem_coef(D, P, coef, flag, st));
+            int64_t nsv = 0;
+            TRY(compact(flag, D.n, idx, &nsv, st));
+            if (!want_certify(prm, D.n, nsv, D.d)) break;
+        }
+        double viol = 0;
+        TRY(certify(D, P, &viol, st));
+        if (viol <= P.tol) { P.converged = true; break; }
+        P.converged = false;
+        int64_t left = P.max_iter - P.iterations;
+        if (left <= 0) break;
+        TRY(run_loop(D, P, E, left, st, nullptr));
+    }
+    return SVM_OK;
+}
+
+// ================================================================ model
+struct svm_model {
+    svm_model_info info;
+    int64_t d = 0, nsv = 0, nsv_pad = 0;
+    int n_out = 1, mode = 0;   // mode 0 regression, 1 binary, 2 one-vs-rest
+    KParams kp;
+    double first_label = 0;
+    DBuf SVT, svnorm, coef, b, labels;  // coef fp64 [n_out][nsv_pad]
+    std::vector<int64_t> sv_index;
+    std::vector<double> coef_host;      // [n_out][nsv]
+};
+
+static int assemble_model(const Data& D, std::vector<Problem>& probs, const svm_params* prm,
+                          svm_model* M, const std::vector<double>& bs, cudaStream_t st)
+{
+    const int np = (int)probs.size();
+    DBuf flag;
+    TRY(flag.alloc(D.n));
+    CK(cudaMemsetAsync(flag.p, 0, D.n, st));
+    std::vector<DBuf> coefs(np);
+    for (int p = 0; p < np; ++p) TRY(problem_coef(D, probs[p], coefs[p], flag, st));
+    DBuf idx;
+    int64_t nsv = 0;
+    TRY(compact(flag, D.n, idx, &nsv, st));
+    M->nsv = nsv;
+    M->nsv_pad = std::max<int64_t>(64, (nsv + 63) / 64 * 64);
+    M->d = D.d;
+    TRY(gather_rows_T(D, idx, nsv, M->nsv_pad, M->SVT, M->svnorm, st));
+    TRY(M->coef.alloc(sizeof(double) * M->nsv_pad * np));
+    for (int p = 0; p < np; ++p)
+        CK(lay_gather_coef(coefs[p].as<double>(), idx.as<int64_t>(), nsv, M->nsv_pad,
+                           M->coef.as<double>() + (int64_t)p * M->nsv_pad, st));
+    TRY(to_device(M->b, bs.data(), np, st));
+    M->sv_index.resize(nsv);
+    if (nsv) CK(cudaMemcpyAsync(M->sv_index.data(), idx.p, sizeof(int64_t) * nsv,
+                                cudaMemcpyDeviceToHost, st));
+    M->coef_host.resize((size_t)nsv * np);
+    for (int p = 0; p < np; ++p)
+        if (nsv) CK(cudaMemcpyAsync(M->coef_host.data() + (size_t)p * nsv,
+                                    M->coef.as<double>() + (int64_t)p * M->nsv_pad,
+                                    sizeof(double) * nsv, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    (void)prm;
+    return SVM_OK;
+}
+
+// ================================================================ training entry points
+static int label_problems(const svm_params* prm, const std::vector<float>& y,
+                          std::vector<std::vector<float>>& ys, std::vector<double>& labels,
+                          int* mode, double* first_label)
+{
+    int64_t n = (int64_t)y.size();
+    for (int64_t i = 0; i < n; ++i)
+        if (!std::isfinite(y[i])) return fail(SVM_ENONFINITE, "y[%lld] is not finite", (long long)i);
+    if (prm->type == SVM_EPS_REGRESSION) {
+        ys.assign(1, y);
+        *mode = 0;
+        return SVM_OK;
+    }
+    std::vector<double> order;          // first-appearance order
+    std::map<double, int> seen;
+    for (float v : y)
+        if (seen.emplace((double)v, (int)order.size()).second) {
+            order.push_back(v);
+            if (order.size() > 64) return fail(SVM_EINVAL, "more than 64 classes");
+        }
+    if (order.size() < 2) return fail(SVM_EDEGENERATE, "classification labels have a single class");
+    labels = order;
+    *first_label = order[0];
+    if (order.size() == 2) {
+        *mode = 1;
+        bool pm1 = (order[0] == 1.0 && order[1] == -1.0) || (order[0] == -1.0 && order[1] == 1.0);
+        std::vector<float> yb(n);
+        double pos = pm1 ? 1.0 : order[0];
+        for (int64_t i = 0; i < n; ++i) yb[i] = ((double)y[i] == pos) ? 1.0f : -1.0f;
+        if (pm1) labels = {1.0, -1.0};
+        else labels = {order[0], order[1]};
+        ys.assign(1, yb);
+        return SVM_OK;
+    }
+    *mode = 2;                           // one-vs-rest (BASELINE config 3)
+    ys.clear();
+    for (double c : order) {
+        std::vector<float> yb(n);
+        for (int64_t i = 0; i < n; ++i) yb[i] = ((double)y[i] == c) ? 1.0f : -1.0f;
+        ys.push_back(std::move(yb));
+    }
+    return SVM_OK;
+}
+
+static int train_common(Data& D, const float* y, const svm_params* prm, svm_model** out,
+                        double t_start, cudaStream_t st)
+{
+    std::vector<float> yh;
+    TRY(to_host(yh, y, D.n, st));
+    std::vector<std::vector<float>> ys;
+    std::vector<double> labels;
+    int mode = 0;
+    double first = 0;
+    TRY(label_problems(prm, yh, ys, labels, &mode, &first));
+    double t_setup = now_ms() - t_start;
+    Exchange E;
+    TRY(E.alloc(D.nblk));
+    std::vector<Problem> probs(ys.size());
+    std::vector<double> bs(ys.size());
+    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0;
+    int64_t iters = 0;
+    bool conv = true, cert = true;
+    for (size_t p = 0; p < ys.size(); ++p) {
+        Problem& P = probs[p];
+        TRY(problem_init(P, D, ys[p].data(), prm, st));
+        TRY(solve_problem(D, P, E, prm, st));
+        Reduced r;
+        TRY(reduce_state(D, P, &r, st));
+        // bias (sign-corrected; reading R6)
+        bs[p] = r.free_cnt > 0 ? r.free_sum / r.free_cnt : 0.5 * (r.m_up + r.M_low);
+        if (!std::isfinite(bs[p])) bs[p] = 0.0;
+        dual += r.dual;
+        worst = std::max(worst, r.m_up - r.M_low);
+        iters += P.iterations;
+        conv = conv && P.converged;
+        cert = cert && P.certified;
+        loop_ms += P.loop_ms;
+        cert_ms += P.cert_ms;
+    }
+    svm_model* M = new (std::nothrow) svm_model();
+    if (!M) return fail(SVM_ENOMEM, "model allocation failed");
+    int rc = assemble_model(D, probs, prm, M, bs, st);
+    if (rc != SVM_OK) { delete M; return rc; }
+    M->mode = mode;
+    M->n_out = (int)probs.size();
+    M->kp = probs[0].kp;
+    M->first_label = first;
+    std::vector<double> lab = labels;
+    if (lab.empty()) lab.push_back(0.0);
+    rc = to_device(M->labels, lab.data(), (int64_t)lab.size(), st);
+    if (rc != SVM_OK) { delete M; return rc; }
+    svm_model_info& I = M->info;
+    memset(&I, 0, sizeof I);
+    I.type = prm->type;
+    I.kernel = prm->kernel;
+    I.degree = prm->degree;
+    I.gamma = M->kp.gamma;
+    I.coef0 = prm->coef0;
+    I.n_features = D.d;
+    I.n_train = D.n;
+    I.n_sv = M->nsv;
+    I.n_class = mode == 0 ? 0 : (int32_t)labels.size();
+    I.n_problem = M->n_out;
+    for (size_t i = 0; i < labels.size() && i < 64; ++i) I.labels[i] = labels[i];
+    for (size_t i = 0; i < bs.size() && i < 64; ++i) I.b[i] = bs[i];
+    I.iterations = iters;
+    I.violation = worst;
+    I.converged = conv ? 1 : 0;
+    I.certified = cert ? 1 : 0;
+    I.dual_objective = dual;
+    I.loop_ms = loop_ms;
+    I.certify_ms = cert_ms;
+    I.setup_ms = t_setup;
+    cudaStreamSynchronize(st);
+    I.train_ms = now_ms() - t_start;
+    *out = M;
+    return SVM_OK;
+}
+
+extern "C" int svm_train(const float* X, const float* y, int64_t n, int64_t d,
+                         const svm_params* params, svm_model** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    double t0 = now_ms();
+    TRY(check_params(params, n, d));
+    if (!X || !y) return fail(SVM_EINVAL, "X or y is NULL");
+    cudaStream_t st = (cudaStream_t)params->stream;
+    Data D;
+    TRY(build_dense(D, X, n, d, params->layout, pick_nblk(n), st));
+    return train_common(D, y, params, out, t0, st);
+}
+
+extern "C" int svm_train_csr(const int64_t* indptr, const int32_t* indices, const float* data,
+                             const float* y, int64_t n, int64_t d, const svm_params* params,
+                             svm_model** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    double t0 = now_ms();
+    TRY(check_params(params, n, d));
+    if (!y) return fail(SVM_EINVAL, "y is NULL");
+    cudaStream_t st = (cudaStream_t)params->stream;
+    Data D;
+    TRY(build_csr(D, indptr, indices, data, n, d, pick_nblk(n), st));
+    return train_common(D, y, params, out, t0, st);
+}
+
+// ================================================================ predict
+static int predict_common(const svm_model* M, int64_t nq, const float* Xq_dense, int layout,
+                          const int64_t* indptr, const int32_t* indices, const float* data,
+                          float* decision, float* out)
+{
+    cudaStream_t st = nullptr;
+    const int64_t CH = 65536;  // query rows per chunk
+    bool dec_dev = is_device_ptr(decision), out_dev = is_device_ptr(out);
+    DBuf hostX, QT, qn, F, ddec, dout;
+    const float* Xd = Xq_dense;
+    if (Xq_dense && !is_device_ptr(Xq_dense)) {
+        TRY(hostX.alloc(sizeof(float) * nq * M->d));
+        CK(cudaMemcpyAsync(hostX.p, Xq_dense, sizeof(float) * nq * M->d, cudaMemcpyHostToDevice, st));
+        Xd = hostX.as<float>();
+    }
+    DBuf dptr, didx, dval;
+    const int64_t* ip = indptr;
+    const int32_t* ix = indices;
+    const float* iv = data;
+    if (!Xq_dense) {
+        int64_t nnz = 0;
+        if (is_device_ptr(indptr)) {
+            CK(cudaMemcpyAsync(&nnz, indptr + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else nnz = indptr[nq];
+        if (!is_device_ptr(indptr)) { TRY(to_device(dptr, indptr, nq + 1, st)); ip = dptr.as<int64_t>(); }
+        if (!is_device_ptr(indices)) { TRY(to_device(didx, indices, nnz, st)); ix = didx.as<int32_t>(); }
+        if (!is_device_ptr(data)) { TRY(to_device(dval, data, nnz, st)); iv = dval.as<float>(); }
+        DBuf bad;
+        TRY(bad.alloc(sizeof(int)));
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        CK(lay_check_csr(ip, ix, nq, M->d, nnz, bad.as<int>(), st));
+        TRY(check_bad_flag(bad, st, SVM_EINVAL, "query CSR invariants violated"));
+    }
+    int64_t chunk = std::min<int64_t>(CH, nq);
+    int64_t cpad = (chunk + 127) / 128 * 128;
+    TRY(QT.alloc(sizeof(float) * M->d * cpad));
+    TRY(qn.alloc(sizeof(float) * cpad));
+    TRY(F.alloc(sizeof(double) * chunk * M->n_out));
+    TRY(ddec.alloc(sizeof(float) * chunk * M->n_out));
+    TRY(dout.alloc(sizeof(float) * chunk));
+    for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+        int64_t m = std::min(chunk, nq - q0);
+        if (Xq_dense) {
+            if (layout == SVM_ROW_MAJOR) {
+                CK(lay_rowmajor_to_XT(Xd + q0 * M->d, m, M->d, QT.as<float>(), cpad, st));
+            } else {
+                // column-major queries: column k of the chunk starts at Xd + k * nq + q0
+                CK(cudaMemsetAsync(QT.p, 0, QT.bytes, st));
+                CK(cudaMemcpy2DAsync(QT.p, sizeof(float) * cpad, Xd + q0, sizeof(float) * nq,
+                                     sizeof(float) * m, M->d, cudaMemcpyDeviceToDevice, st));
+            }
+        } else {
+            CK(cudaMemsetAsync(QT.p, 0, QT.bytes, st));
+            CK(lay_csr_to_XT(ip, ix, iv, nullptr, m, q0, QT.as<float>(), cpad, st));
+        }
+        DBuf bad;
+        TRY(bad.alloc(sizeof(int)));
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        CK(lay_check_finite(QT.as<float>(), M->d * cpad, bad.as<int>(), st));
+        TRY(check_bad_flag(bad, st, SVM_ENONFINITE, "query X contains a non-finite value"));
+        CK(lay_norms_XT(QT.as<float>(), m, M->d, cpad, qn.as<float>(), st));
+        CK(pred_decision(QT.as<float>(), qn.as<float>(), m, cpad, M->SVT.as<float>(),
+                         M->svnorm.as<float>(), M->nsv, M->nsv_pad, M->d, M->coef.as<double>(),
+                         M->n_out, M->kp, F.as<double>(), st));
+        CK(pred_finalize(F.as<double>(), m, M->n_out, M->b.as<double>(), M->mode,
+                         M->labels.as<double>(), M->first_label, ddec.as<float>(),
+                         dout.as<float>(), st));
+        if (decision)
+            CK(cudaMemcpyAsync(decision + q0 * M->n_out, ddec.p, sizeof(float) * m * M->n_out,
+                               dec_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        if (out)
+            CK(cudaMemcpyAsync(out + q0, dout.p, sizeof(float) * m,
+                               out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return SVM_OK;
+}
+
+extern "C" int svm_predict(const svm_model* model, const float* Xq, int64_t nq, int64_t d,
+                           int32_t layout, float* decision, float* out)
+{
+    if (!model) return fail(SVM_EINVAL, "model is NULL");
+    if (d != model->d) return fail(SVM_EINVAL, "d = %lld does not match the model's %lld",
+                                   (long long)d, (long long)model->d);
+    if (nq < 0) return fail(SVM_EINVAL, "nq < 0");
+    if (nq == 0) return SVM_OK;
+    if (!Xq) return fail(SVM_EINVAL, "Xq is NULL");
+    if (layout != SVM_ROW_MAJOR && layout != SVM_COL_MAJOR) return fail(SVM_EINVAL, "bad layout");
+    return predict_common(model, nq, Xq, layout, nullptr, nullptr, nullptr, decision, out);
+}
+
+extern "C" int svm_predict_csr(const svm_model* model, const int64_t* indptr,
+                               const int32_t* indices, const float* data, int64_t nq, int64_t d,
+                               float* decision, float* out)
+{
+    if (!model) return fail(SVM_EINVAL, "model is NULL");
+    if (d != model->d) return fail(SVM_EINVAL, "d = %lld does not match the model's %lld",
+                                   (long long)d, (long long)model->d);
+    if (nq < 0) return fail(SVM_EINVAL, "nq < 0");
+    if (nq == 0) return SVM_OK;
+    if (!indptr || !indices || !data) return fail(SVM_EINVAL, "CSR arrays must not be NULL");
+    return predict_common(model, nq, nullptr, SVM_ROW_MAJOR, indptr, indices, data, decision, out);
+}
+
+extern "C" int svm_model_get_info(const svm_model* model, svm_model_info* info)
+{
+    if (!model || !info) return fail(SVM_EINVAL, "NULL model or info");
+    *info = model->info;
+    return SVM_OK;
+}
+
+extern "C" int svm_model_get_sv(const svm_model* model, int64_t* sv_index, double* coef)
+{
+    if (!model) return fail(SVM_EINVAL, "model is NULL");
+    if (sv_index && model->nsv)
+        memcpy(sv_index, model->sv_index.data(), sizeof(int64_t) * model->nsv);
+    if (coef && !model->coef_host.empty())
+        memcpy(coef, model->coef_host.data(), sizeof(double) * model->coef_host.size());
+    return SVM_OK;
+}
+
+extern "C" void svm_free_model(svm_model* model) { delete model; }
+
+extern "C" const char* svm_last_error(void) { return g_err.c_str(); }
+
+// ================================================================ solver-state API
+struct svm_solver {
+    Data D;
+    Problem P;
+    Exchange E;
+    svm_params prm;
+    cudaStream_t st = nullptr;
+};
+
+static int solver_create_common(svm_solver* S, const float* y, const svm_params* params)
+{
+    std::vector<float> yh;
+    TRY(to_host(yh, y, S->D.n, S->st));
+    std::vector<std::vector<float>> ys;
+    std::vector<double> labels;
+    int mode = 0;
+    double first = 0;
+    TRY(label_problems(params, yh, ys, labels, &mode, &first));
+    if (mode == 2) return fail(SVM_EINVAL, "solver API takes binary or regression problems only");
+    TRY(S->E.alloc(S->D.nblk));
+    TRY(problem_init(S->P, S->D, ys[0].data(), params, S->st));
+    CK(cudaStreamSynchronize(S->st));
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_create(const float* X, const float* y, int64_t n, int64_t d,
+                                 const svm_params* params, svm_solver** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(params, n, d));
+    if (!X || !y) return fail(SVM_EINVAL, "X or y is NULL");
+    svm_solver* S = new (std::nothrow) svm_solver();
+    if (!S) return fail(SVM_ENOMEM, "solver allocation failed");
+    S->prm = *params;
+    S->st = (cudaStream_t)params->stream;
+    int rc = build_dense(S->D, X, n, d, params->layout, pick_nblk(n), S->st);
+    if (rc == SVM_OK) rc = solver_create_common(S, y, params);
+    if (rc != SVM_OK) { delete S; return rc; }
+    *out = S;
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_create_csr(const int64_t* indptr, const int32_t* indices,
+                                     const float* data, const float* y, int64_t n, int64_t d,
+                                     const svm_params* params, svm_solver** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(params, n, d));
+    if (!y) return fail(SVM_EINVAL, "y is NULL");
+    svm_solver* S = new (std::nothrow) svm_solver();
+    if (!S) return fail(SVM_ENOMEM, "solver allocation failed");
+    S->prm = *params;
+    S->st = (cudaStream_t)params->stream;
+    int rc = build_csr(S->D, indptr, indices, data, n, d, pick_nblk(n), S->st);
+    if (rc == SVM_OK) rc = solver_create_common(S, y, params);
+    if (rc != SVM_OK) { delete S; return rc; }
+    *out = S;
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_size(const svm_solver* s, int64_t* m)
+{
+    if (!s || !m) return fail(SVM_EINVAL, "NULL solver or m");
+    *m = s->D.n * s->P.ncopy;
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_set_state(svm_solver* s, const double* alpha, const float* G)
+{
+    if (!s || !alpha || !G) return fail(SVM_EINVAL, "NULL argument");
+    int64_t m = s->D.n * s->P.ncopy;
+    std::vector<double> ah;
+    TRY(to_host(ah, alpha, m, s->st));
+    for (int64_t i = 0; i < m; ++i)
+        if (!(ah[i] >= 0.0 && ah[i] <= s->P.C))
+            return fail(SVM_EINVAL, "alpha[%lld] = %g outside [0, C]", (long long)i, ah[i]);
+    DBuf da, dg;
+    TRY(to_device(da, alpha, m, s->st));
+    TRY(to_device(dg, G, m, s->st));
+    CK(lay_unpack_state(da.as<double>(), dg.as<float>(), s->D.n, s->D.n_pad, s->P.ncopy,
+                        s->P.alpha.as<double>(), s->P.G.as<float>(), s->st));
+    CK(lay_status_from_alpha(s->P.alpha.as<double>(), s->D.n, s->D.n_pad, s->P.ncopy, s->P.C,
+                             s->P.status.as<uint8_t>(), s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_get_state(const svm_solver* s, double* alpha, float* G)
+{
+    if (!s) return fail(SVM_EINVAL, "NULL solver");
+    int64_t m = s->D.n * s->P.ncopy;
+    DBuf da, dg;
+    TRY(da.alloc(sizeof(double) * m));
+    TRY(dg.alloc(sizeof(float) * m));
+    CK(lay_pack_state(s->P.alpha.as<double>(), s->P.G.as<float>(), s->D.n, s->D.n_pad, s->P.ncopy,
+                      da.as<double>(), dg.as<float>(), s->st));
+    if (alpha) CK(cudaMemcpyAsync(alpha, da.p, sizeof(double) * m,
+                                  is_device_ptr(alpha) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->st));
+    if (G) CK(cudaMemcpyAsync(G, dg.p, sizeof(float) * m,
+                              is_device_ptr(G) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_run(svm_solver* s, int64_t max_iter, svm_solver_stats* stats)
+{
+    if (!s) return fail(SVM_EINVAL, "NULL solver");
+    if (max_iter < 0) return fail(SVM_EINVAL, "max_iter < 0");
+    s->P.loop_ms = 0;
+    int64_t before = s->P.iterations;
+    SmoInfo info;
+    TRY(run_loop(s->D, s->P, s->E, max_iter, s->st, &info));
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        stats->iterations = s->P.iterations - before;
+        stats->m_up = info.m_up;
+        stats->M_low = info.M_low;
+        stats->converged = info.converged;
+        stats->last_nw = info.iterations > 0 ? info.last_nw : 0;
+        for (int i = 0; i < stats->last_nw; ++i) {
+            stats->last_w[i] = info.last_w[i];
+            stats->last_dalpha[i] = info.last_dalpha[i];
+        }
+        stats->last_inner = info.last_inner;
+        stats->loop_ms = s->P.loop_ms;
+    }
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_kernel_rows(svm_solver* s, const int64_t* rows, int32_t nr, float* K)
+{
+    if (!s || !rows || !K) return fail(SVM_EINVAL, "NULL argument");
+    if (nr < 1 || nr > SVM_WS) return fail(SVM_EINVAL, "nr must be in [1, 16]");
+    std::vector<int64_t> rh;
+    TRY(to_host(rh, rows, nr, s->st));
+    for (int i = 0; i < nr; ++i)
+        if (rh[i] < 0 || rh[i] >= s->D.n) return fail(SVM_EINVAL, "row index out of range");
+    DBuf drows, dK;
+    TRY(to_device(drows, rh.data(), nr, s->st));
+    TRY(dK.alloc(sizeof(float) * s->D.n * nr));
+    SmoArgs a = make_args(s->D, s->P, s->E);
+    CK(launch_kernel_rows(a, drows.as<int64_t>(), nr, dK.as<float>(), s->st));
+    CK(cudaMemcpyAsync(K, dK.p, sizeof(float) * s->D.n * nr,
+                       is_device_ptr(K) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return SVM_OK;
+}
+
+extern "C" void svm_solver_free(svm_solver* s) { delete s; }
+
+// ================================================================ row-sharded training
+// Rank r owns rows [row0, row0 + n_local).  Exported (cudaIpc) buffers per rank: the candidate
+// receive buffers (keys, payloads, flags), the scalar exchange buffer, its rows (dense row-major
+// or CSR) and norms, and the per-row coefficient / SV-index export used to gather the model.
+namespace {
+constexpr uint32_t SHARD_MAGIC = 0x53564D42u;  // "SVMB"
+enum { H_KEYS, H_PAY, H_FLAGS, H_XBUF, H_XFLAGS, H_XR, H_NORMS, H_INDPTR, H_INDICES, H_VALS,
+       H_SVIDX, H_COEFX, H_COUNT };
+struct ShardHandle {
+    uint32_t magic;
+    int32_t rank, world, nblk, csr, nprob, ncopy, pad;
+    int64_t n_local, row0, n_global, d;
+    cudaIpcMemHandle_t h[H_COUNT];
+};
+static_assert(sizeof(ShardHandle) <= SVM_SHARD_HANDLE_BYTES, "shard handle too large");
+}  // namespace
+
+struct svm_shard {
+    Data D;
+    svm_params prm;
+    cudaStream_t st = nullptr;
+    int rank = 0, world = 1;
+    int64_t row0 = 0, n_global = 0;
+    std::vector<std::vector<float>> ys;  // per problem, local rows
+    std::vector<double> labels;
+    int mode = 0, nprob = 1;
+    double first = 0;
+    Exchange E;
+    DBuf xbuf, xflags, xvals, xout, xerr, svidx, coefx;
+    uint32_t xepoch = 0;
+    ShardCtx sc;
+    XchgPeers xp;
+    SvPeers svp;
+    std::vector<void*> opened;
+    bool connected = false;
+    ~svm_shard()
+    {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+    }
+};
+
+// device-side all-gather of K doubles across ranks (also a barrier)
+static int shard_xchg(svm_shard* S, const std::vector<double>& vals, std::vector<double>& all,
+                      double timeout_s = 60.0)
+{
+    int K = (int)vals.size();
+    CK(cudaMemcpyAsync(S->xvals.p, vals.data(), sizeof(double) * K, cudaMemcpyHostToDevice, S->st));
+    CK(cudaMemsetAsync(S->xerr.p, 0, sizeof(int), S->st));
+    uint32_t tag = ++S->xepoch;
+    CK(lay_xchg(S->xvals.as<double>(), K, S->rank, S->world, S->xp, tag, S->xout.as<double>(),
+                (uint64_t)(timeout_s * 1e9), S->xerr.as<int>(), S->st));
+    all.resize((size_t)S->world * K);
+    int err = 0;
+    CK(cudaMemcpyAsync(all.data(), S->xout.p, sizeof(double) * S->world * K, cudaMemcpyDeviceToHost, S->st));
+    CK(cudaMemcpyAsync(&err, S->xerr.p, sizeof(int), cudaMemcpyDeviceToHost, S->st));
+    CK(cudaStreamSynchronize(S->st));
+    if (err) return fail(SVM_ETIMEOUT, "rank exchange timed out (a peer stopped)");
+    return SVM_OK;
+}
+
+static int shard_create_common(svm_shard* S, const float* y_global, const svm_params* params)
+{
+    std::vector<float> yg;
+    TRY(to_host(yg, y_global, S->n_global, S->st));
+    std::vector<std::vector<float>> ys;
+    TRY(label_problems(params, yg, ys, S->labels, &S->mode, &S->first));
+    S->nprob = (int)ys.size();
+    S->ys.resize(ys.size());
+    for (size_t p = 0; p < ys.size(); ++p)
+        S->ys[p].assign(ys[p].begin() + S->row0, ys[p].begin() + S->row0 + S->D.n);
+    const int L = S->world * S->D.nblk;
+    TRY(S->E.alloc(L));
+    TRY(S->xbuf.alloc(sizeof(double) * 2 * S->world * XCH_K));
+    TRY(S->xflags.alloc(sizeof(uint32_t) * S->world));
+    CK(cudaMemset(S->xflags.p, 0, S->xflags.bytes));
+    TRY(S->xvals.alloc(sizeof(double) * XCH_K));
+    TRY(S->xout.alloc(sizeof(double) * S->world * XCH_K));
+    TRY(S->xerr.alloc(sizeof(int)));
+    TRY(S->svidx.alloc(sizeof(int64_t) * std::max<int64_t>(S->D.n, 1)));
+    TRY(S->coefx.alloc(sizeof(double) * std::max<int64_t>(S->D.n, 1) * S->nprob));
+    if (!S->D.csr && !S->D.XR_own.p) {  // exported rows must be a cudaMalloc base: own a copy
+        TRY(S->D.XR_own.alloc(sizeof(float) * S->D.n * S->D.d));
+        CK(cudaMemcpyAsync(S->D.XR_own.p, S->D.XR, sizeof(float) * S->D.n * S->D.d,
+                           cudaMemcpyDeviceToDevice, S->st));
+        S->D.XR = S->D.XR_own.as<float>();
+    }
+    if (S->D.csr) {
+        if (!S->D.indptr_own.p) { TRY(to_device(S->D.indptr_own, S->D.indptr, S->D.n + 1, S->st)); S->D.indptr = S->D.indptr_own.as<int64_t>(); }
+        if (!S->D.indices_own.p) { TRY(to_device(S->D.indices_own, S->D.indices, S->D.nnz, S->st)); S->D.indices = S->D.indices_own.as<int32_t>(); }
+        if (!S->D.vals_own.p) { TRY(to_device(S->D.vals_own, S->D.vals, S->D.nnz, S->st)); S->D.vals = S->D.vals_own.as<float>(); }
+    }
+    CK(cudaStreamSynchronize(S->st));
+    return SVM_OK;
+}
+
+static int shard_check_args(int64_t n_local, int64_t row0, int64_t n_global, int32_t rank,
+                            int32_t world)
+{
+    if (world < 1 || world > SVM_MAX_RANKS) return fail(SVM_EINVAL, "world must be in [1, 8]");
+    if (rank < 0 || rank >= world) return fail(SVM_EINVAL, "rank out of range");
+    if (n_local < 1 || row0 < 0 || row0 + n_local > n_global)
+        return fail(SVM_EINVAL, "local rows [row0, row0 + n_local) outside [0, n_global)");
+    return SVM_OK;
+}
+
+extern "C" int svm_shard_create(const float* X_local, int64_t n_local, int64_t d, int64_t row0,
+                                const float* y_global, int64_t n_global, int32_t rank,
+                                int32_t world, const svm_params* params, svm_shard** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(params, n_global, d));
+    TRY(shard_check_args(n_local, row0, n_global, rank, world));
+    if (!X_local || !y_global) return fail(SVM_EINVAL, "X_local or y_global is NULL");
+    svm_shard* S = new (std::nothrow) svm_shard();
+    if (!S) return fail(SVM_ENOMEM, "shard allocation failed");
+    S->prm = *params;
+    S->st = (cudaStream_t)params->stream;
+    S->rank = rank;
+    S->world = world;
+    S->row0 = row0;
+    S->n_global = n_global;
+    int nblk = pick_nblk((n_global + world - 1) / world);
+    int rc = build_dense(S->D, X_local, n_local, d, params->layout, nblk, S->st);
+    if (rc == SVM_OK) rc = shard_create_common(S, y_global, params);
+    if (rc != SVM_OK) { delete S; return rc; }
+    *out = S;
+    return SVM_OK;
+}
+
+extern "C" int svm_shard_create_csr(const int64_t* indptr, const int32_t* indices,
+                                    const float* data, int64_t n_local, int64_t d, int64_t row0,
+                                    const float* y_global, int64_t n_global, int32_t rank,
+                                    int32_t world, const svm_params* params, svm_shard** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(params, n_global, d));
+    TRY(shard_check_args(n_local, row0, n_global, rank, world));
+    if (!y_global) return fail(SVM_EINVAL, "y_global is NULL");
+    svm_shard* S = new (std::nothrow) svm_shard();
+    if (!S) return fail(SVM_ENOMEM, "shard allocation failed");
+    S->prm = *params;
+    S->st = (cudaStream_t)params->stream;
+    S->rank = rank;
+    S->world = world;
+    S->row0 = row0;
+    S->n_global = n_global;
+    int nblk = pick_nblk((n_global + world - 1) / world);
+    int rc = build_csr(S->D, indptr, indices, data, n_local, d, nblk, S->st);
+    if (rc == SVM_OK) rc = shard_create_common(S, y_global, params);
+    if (rc != SVM_OK) { delete S; return rc; }
+    *out = S;
+    return SVM_OK;
+}
+
+extern "C" int svm_shard_handle(const svm_shard* S, void* handle)
+{
+    if (!S || !handle) return fail(SVM_EINVAL, "NULL argument");
+    ShardHandle H;
+    memset(&H, 0, sizeof H);
+    H.magic = SHARD_MAGIC;
+    H.rank = S->rank;
+    H.world = S->world;
+    H.nblk = S->D.nblk;
+    H.csr = S->D.csr ? 1 : 0;
+    H.nprob = S->nprob;
+    H.ncopy = S->prm.type == SVM_EPS_REGRESSION ? 2 : 1;
+    H.n_local = S->D.n;
+    H.row0 = S->row0;
+    H.n_global = S->n_global;
+    H.d = S->D.d;
+    const void* ptrs[H_COUNT] = {S->E.keys.p, S->E.pay.p, S->E.flags.p, S->xbuf.p, S->xflags.p,
+                                 S->D.csr ? nullptr : S->D.XR, S->D.norms.p,
+                                 S->D.csr ? S->D.indptr : nullptr, S->D.csr ? S->D.indices : nullptr,
+                                 S->D.csr ? S->D.vals : nullptr, S->svidx.p, S->coefx.p};
+    for (int i = 0; i < H_COUNT; ++i)
+        if (ptrs[i]) CK(cudaIpcGetMemHandle(&H.h[i], const_cast<void*>(ptrs[i])));
+    memset(handle, 0, SVM_SHARD_HANDLE_BYTES);
+    memcpy(handle, &H, sizeof H);
+    return SVM_OK;
+}
+
+extern "C" int svm_shard_connect(svm_shard* S, const void* all_handles)
+{
+    if (!S || !all_handles) return fail(SVM_EINVAL, "NULL argument");
+    if (S->connected) return fail(SVM_EINVAL, "shard already connected");
+    const unsigned char* base = static_cast<const unsigned char*>(all_handles);
+    ShardCtx& c = S->sc;
+    c.rank = S->rank;
+    c.world = S->world;
+    c.row0 = S->row0;
+    c.n_global = S->n_global;
+    memset(&S->xp, 0, sizeof S->xp);
+    memset(&S->svp, 0, sizeof S->svp);
+    S->svp.world = S->world;
+    int64_t expect_row0 = 0;
+    for (int r = 0; r < S->world; ++r) {
+        ShardHandle H;
+        memcpy(&H, base + (size_t)r * SVM_SHARD_HANDLE_BYTES, sizeof H);
+        if (H.magic != SHARD_MAGIC || H.rank != r || H.world != S->world || H.nblk != S->D.nblk ||
+            H.csr != (S->D.csr ? 1 : 0) || H.nprob != S->nprob || H.n_global != S->n_global ||
+            H.d != S->D.d)
+            return fail(SVM_EPEER, "shard handle of rank %d does not match this run", r);
+        if (H.row0 != expect_row0)
+            return fail(SVM_EPEER, "ranks must hold contiguous row blocks in rank order");
+        expect_row0 += H.n_local;
+        c.rank_row0[r] = H.row0;
+        S->svp.n_local[r] = H.n_local;
+        S->svp.row0[r] = H.row0;
+        void* p[H_COUNT] = {};
+        if (r == S->rank) {
+            void* mine[H_COUNT] = {S->E.keys.p, S->E.pay.p, S->E.flags.p, S->xbuf.p, S->xflags.p,
+                                   S->D.csr ? nullptr : (void*)S->D.XR, S->D.norms.p,
+                                   S->D.csr ? (void*)S->D.indptr : nullptr,
+                                   S->D.csr ? (void*)S->D.indices : nullptr,
+                                   S->D.csr ? (void*)S->D.vals : nullptr, S->svidx.p, S->coefx.p};
+            memcpy(p, mine, sizeof p);
+        } else {
+            for (int i = 0; i < H_COUNT; ++i) {
+                bool present = false;
+                for (size_t b = 0; b < sizeof(cudaIpcMemHandle_t); ++b)
+                    present |= H.h[i].reserved[b] != 0;
+                if (!present) continue;
+                cudaError_t e = cudaIpcOpenMemHandle(&p[i], H.h[i], cudaIpcMemLazyEnablePeerAccess);
+                if (e != cudaSuccess)
+                    return fail(SVM_EPEER, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", r, i,
+                                cudaGetErrorString(e));
+                S->opened.push_back(p[i]);
+            }
+        }
+        c.keys[r] = (uint64_t*)p[H_KEYS];
+        c.pay[r] = (CandPay*)p[H_PAY];
+        c.flags[r] = (uint32_t*)p[H_FLAGS];
+        c.XR[r] = (const float*)p[H_XR];
+        c.norms[r] = (const float*)p[H_NORMS];
+        c.indptr[r] = (const int64_t*)p[H_INDPTR];
+        c.indices[r] = (const int32_t*)p[H_INDICES];
+        c.vals[r] = (const float*)p[H_VALS];
+        S->xp.buf[r] = (double*)p[H_XBUF];
+        S->xp.flags[r] = (uint32_t*)p[H_XFLAGS];
+        S->svp.XR[r] = c.XR[r];
+        S->svp.indptr[r] = c.indptr[r];
+        S->svp.indices[r] = c.indices[r];
+        S->svp.vals[r] = c.vals[r];
+        S->svp.norms[r] = c.norms[r];
+        S->svp.svidx[r] = (const int64_t*)p[H_SVIDX];
+        S->svp.coefx[r] = (const double*)p[H_COEFX];
+    }
+    if (expect_row0 != S->n_global) return fail(SVM_EPEER, "row blocks do not cover n_global");
+    c.rank_row0[S->world] = S->n_global;
+    S->connected = true;
+    return SVM_OK;
+}
+
+// Global SV set of the per-row coefficients currently in every rank's coefx export (problems
+// [0, nprob_used)): compaction locally, counts exchanged, rows gathered from their owners.
+static int shard_global_sv(svm_shard* S, int nprob_used, const DBuf& flag, DBuf& SVT, DBuf& svn,
+                           DBuf& coef, int64_t* nsv_out, int64_t* nsv_pad_out, DBuf* grow)
+{
+    const Data& D = S->D;
+    DBuf idx;
+    int64_t nloc = 0;
+    TRY(compact(flag, D.n, idx, &nloc, S->st));
+    if (nloc) CK(cudaMemcpyAsync(S->svidx.p, idx.p, sizeof(int64_t) * nloc, cudaMemcpyDeviceToDevice, S->st));
+    CK(cudaStreamSynchronize(S->st));
+    std::vector<double> all;
+    TRY(shard_xchg(S, {(double)nloc}, all));       // also: every export is complete
+    S->svp.off[0] = 0;
+    for (int r = 0; r < S->world; ++r) S->svp.off[r + 1] = S->svp.off[r] + (int64_t)all[r];
+    int64_t nsv = S->svp.off[S->world];
+    int64_t nsv_pad = std::max<int64_t>(64, (nsv + 63) / 64 * 64);
+    TRY(SVT.alloc(sizeof(float) * D.d * nsv_pad));
+    TRY(svn.alloc(sizeof(float) * nsv_pad));
+    TRY(coef.alloc(sizeof(double) * nsv_pad * nprob_used));
+    if (D.csr) CK(cudaMemsetAsync(SVT.p, 0, SVT.bytes, S->st));
+    if (grow) TRY(grow->alloc(sizeof(int64_t) * nsv_pad));
+    CK(lay_gather_global_sv(S->svp, nsv, nsv_pad, D.d, nprob_used, SVT.as<float>(), svn.as<float>(),
+                            coef.as<double>(), grow ? grow->as<int64_t>() : nullptr, S->st));
+    CK(cudaStreamSynchronize(S->st));
+    std::vector<double> none;
+    TRY(shard_xchg(S, {0.0}, none));               // nobody rewrites exports before all gathered
+    *nsv_out = nsv;
+    *nsv_pad_out = nsv_pad;
+    return SVM_OK;
+}
+
+static int shard_reduce(svm_shard* S, const Problem& P, Reduced* g)
+{
+    Reduced r;
+    TRY(reduce_state(S->D, P, &r, S->st));
+    std::vector<double> all;
+    TRY(shard_xchg(S, {r.m_up, r.M_low, r.free_sum, r.free_cnt, r.dual}, all));
+    Reduced t = {-INFINITY, INFINITY, 0, 0, 0};
+    for (int k = 0; k < S->world; ++k) {  // fixed rank order: identical on every rank
+        t.m_up = std::max(t.m_up, all[k * 5 + 0]);
+        t.M_low = std::min(t.M_low, all[k * 5 + 1]);
+        t.free_sum += all[k * 5 + 2];
+        t.free_cnt += all[k * 5 + 3];
+        t.dual += all[k * 5 + 4];
+    }
+    *g = t;
+    return SVM_OK;
+}
+
+static int shard_certify(svm_shard* S, Problem& P, double* viol)
+{
+    double t0 = now_ms();
+    const Data& D = S->D;
+    DBuf flag, coefrow, SVT, svn, coef, F;
+    TRY(flag.alloc(D.n));
+    CK(cudaMemsetAsync(flag.p, 0, D.n, S->st));
+    TRY(problem_coef(D, P, coefrow, flag, S->st));
+    CK(cudaMemcpyAsync(S->coefx.p, coefrow.p, sizeof(double) * D.n, cudaMemcpyDeviceToDevice, S->st));
+    int64_t nsv = 0, nsv_pad = 0;
+    TRY(shard_global_sv(S, 1, flag, SVT, svn, coef, &nsv, &nsv_pad, nullptr));
+    TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef, P.kp, F, S->st));
+    CK(pred_refresh_G(F.as<double>(), P.yv.as<float>(), P.status.as<uint8_t>(), D.n, D.n_pad,
+                      P.ncopy, P.eps, P.G.as<float>(), S->st));
+    Reduced g;
+    TRY(shard_reduce(S, P, &g));
+    P.m_up = g.m_up;
+    P.M_low = g.M_low;
+    *viol = g.m_up - g.M_low;
+    P.certified = true;
+    P.cert_ms += now_ms() - t0;
+    return SVM_OK;
+}
+
+extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!S) return fail(SVM_EINVAL, "shard is NULL");
+    if (!S->connected) return fail(SVM_EINVAL, "svm_shard_connect has not been called");
+    double t_start = now_ms();
+    const Data& D = S->D;
+    const svm_params* prm = &S->prm;
+    std::vector<double> none;
+    TRY(shard_xchg(S, {0.0}, none, 300.0));        // start barrier
+    std::vector<Problem> probs(S->nprob);
+    std::vector<double> bs(S->nprob);
+    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0;
+    int64_t iters = 0;
+    bool conv = true, cert = true;
+    for (int p = 0; p < S->nprob; ++p) {
+        Problem& P = probs[p];
+        TRY(problem_init(P, D, S->ys[p].data(), prm, S->st));
+        P.max_iter = prm->max_iter > 0 ? prm->max_iter
+                                       : std::max<int64_t>(10 * S->n_global * P.ncopy, 10000);
+        TRY(run_loop(D, P, S->E, P.max_iter, S->st, nullptr, &S->sc));
+        for (int round = 0; round < 4 && P.converged && prm->certify != 0; ++round) {
+            double viol = 0;
+            TRY(shard_certify(S, P, &viol));
+            if (viol <= P.tol) break;
+            P.converged = false;
+            int64_t left = P.max_iter - P.iterations;
+            if (left <= 0) break;
+            TRY(run_loop(D, P, S->E, left, S->st, nullptr, &S->sc));
+        }
+        Reduced g;
+        TRY(shard_reduce(S, P, &g));
+        bs[p] = g.free_cnt > 0 ? g.free_sum / g.free_cnt : 0.5 * (g.m_up + g.M_low);
+        if (!std::isfinite(bs[p])) bs[p] = 0.0;
+        dual += g.dual;
+        worst = std::max(worst, g.m_up - g.M_low);
+        iters += P.iterations;
+        conv = conv && P.converged;
+        cert = cert && P.certified;
+        loop_ms += P.loop_ms;
+        cert_ms += P.cert_ms;
+    }
+    // model: union of SVs over problems, coefficients of every problem, rows gathered
+    DBuf flag;
+    TRY(flag.alloc(D.n));
+    CK(cudaMemsetAsync(flag.p, 0, D.n, S->st));
+    for (int p = 0; p < S->nprob; ++p) {
+        DBuf coefrow;
+        TRY(problem_coef(D, probs[p], coefrow, flag, S->st));
+        CK(cudaMemcpyAsync(S->coefx.as<double>() + (int64_t)p * D.n, coefrow.p, sizeof(double) * D.n,
+                           cudaMemcpyDeviceToDevice, S->st));
+    }
+    svm_model* M = new (std::nothrow) svm_model();
+    if (!M) return fail(SVM_ENOMEM, "model allocation failed");
+    DBuf grow;
+    int64_t nsv = 0, nsv_pad = 0;
+    int rc = shard_global_sv(S, S->nprob, flag, M->SVT, M->svnorm, M->coef, &nsv, &nsv_pad, &grow);
+    if (rc != SVM_OK) { delete M; return rc; }
+    M->nsv = nsv;
+    M->nsv_pad = nsv_pad;
+    M->d = D.d;
+    M->mode = S->mode;
+    M->n_out = S->nprob;
+    M->kp = probs[0].kp;
+    M->first_label = S->first;
+    rc = to_device(M->b, bs.data(), S->nprob, S->st);
+    std::vector<double> lab = S->labels;
+    if (lab.empty()) lab.push_back(0.0);
+    if (rc == SVM_OK) rc = to_device(M->labels, lab.data(), (int64_t)lab.size(), S->st);
+    if (rc != SVM_OK) { delete M; return rc; }
+    M->sv_index.resize(nsv);
+    M->coef_host.resize((size_t)nsv * S->nprob);
+    if (nsv) {
+        cudaMemcpyAsync(M->sv_index.data(), grow.p, sizeof(int64_t) * nsv, cudaMemcpyDeviceToHost, S->st);
+        for (int p = 0; p < S->nprob; ++p)
+            cudaMemcpyAsync(M->coef_host.data() + (size_t)p * nsv, M->coef.as<double>() + (int64_t)p * nsv_pad,
+                            sizeof(double) * nsv, cudaMemcpyDeviceToHost, S->st);
+    }
+    cudaError_t e = cudaStreamSynchronize(S->st);
+    if (e != cudaSuccess) { delete M; return fail(SVM_ECUDA, "%s", cudaGetErrorString(e)); }
+    svm_model_info& I = M->info;
+    memset(&I, 0, sizeof I);
+    I.type = prm->type;
+    I.kernel = prm->kernel;
+    I.degree = prm->degree;
+    I.gamma = M->kp.gamma64;
+    I.coef0 = prm->coef0;
+    I.n_features = D.d;
+    I.n_train = S->n_global;
+    I.n_sv = nsv;
+    I.n_class = S->mode == 0 ? 0 : (int32_t)S->labels.size();
+    I.n_problem = S->nprob;
+    for (size_t i = 0; i < S->labels.size() && i < 64; ++i) I.labels[i] = S->labels[i];
+    for (size_t i = 0; i < bs.size() && i < 64; ++i) I.b[i] = bs[i];
+    I.iterations = iters;
+    I.violation = worst;
+    I.converged = conv ? 1 : 0;
+    I.certified = cert ? 1 : 0;
+    I.dual_objective = dual;
+    I.loop_ms = loop_ms;
+    I.certify_ms = cert_ms;
+    I.train_ms = now_ms() - t_start;
+    *out = M;
+    return SVM_OK;
+}
+
+extern "C" void svm_shard_free(svm_shard* S) { delete S; }

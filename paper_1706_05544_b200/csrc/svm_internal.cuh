@@ -1,0 +1,162 @@
+// svm_internal.cuh -- device-side structures and helpers shared by the CUDA translation units of
+// libsvmb200.so (the product path).  Nothing here is shared with oracle/ (the test oracle).
+//
+// Paper: Rgtsvm, arXiv 1706.05544 (P:n = PAPER.md line n).  The hot path is the working-set
+// iteration of P:53 on the Eq. 2 dual, with eps-SVR through Eq. 1's doubled problem
+// (P:59-69).  Layout and kernel design are in DESIGN.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SVM_MAX_RANKS 8
+#define SVM_WS 16           // maximum |W| ("16 dual space coefficients")
+#define SMO_THREADS 512     // persistent CTA size: 16 warps
+#define SMO_WARPS (SMO_THREADS / 32)
+
+// ---- kernel functions (P:77 names; S:116 formulas; e1071 parameterisation) -------------------
+struct KParams {
+    int32_t kernel;  // 0 linear, 1 polynomial, 2 radial, 3 sigmoid
+    int32_t degree;
+    float gamma;
+    float coef0;
+    double gamma64;  // the same parameters in fp64 for the fp64 subproblem matrix Q_WW
+    double coef064;
+};
+
+// K from the fp32 dot product u.v and the squared norms |u|^2, |v|^2.  RBF uses
+// |u - v|^2 = |u|^2 + |v|^2 - 2 u.v clamped at 0 (reading R11), so K <= 1.
+__device__ __forceinline__ float kernel_from_dot(const KParams& kp, float dot, float nu, float nv)
+{
+    if (kp.kernel == 2) {
+        float d2 = fmaxf(fmaf(-2.0f, dot, nu + nv), 0.0f);
+        return __expf(-kp.gamma * d2);
+    }
+    if (kp.kernel == 0) return dot;
+    float z = fmaf(kp.gamma, dot, kp.coef0);
+    if (kp.kernel == 1) {
+        float r = 1.0f;
+        for (int e = 0; e < kp.degree; ++e) r *= z;
+        return r;
+    }
+    return tanhf(z);
+}
+
+// fp64 kernel between two rows held in shared memory as columns a, b of a [d][16] tile;
+// used for the 16x16 subproblem matrix Q_WW (direct difference for RBF, as the definition).
+__device__ __forceinline__ double kernel_fp64_from(double dot_or_dist, const KParams& kp)
+{
+    if (kp.kernel == 2) return exp(-kp.gamma64 * dot_or_dist);
+    if (kp.kernel == 0) return dot_or_dist;
+    double z = kp.gamma64 * dot_or_dist + kp.coef064;
+    if (kp.kernel == 1) {
+        double r = 1.0;
+        for (int e = 0; e < kp.degree; ++e) r *= z;
+        return r;
+    }
+    return tanh(z);
+}
+
+// Sequential fp32 squared norm with explicit fmaf, so every unit that needs |x|^2 (layout
+// kernel, CSR norms, the in-CTA recompute for working-set rows) gets bit-identical values.
+__device__ __forceinline__ float sqnorm_step(float acc, float v) { return fmaf(v, v, acc); }
+
+// ---- status byte per dual variable ---------------------------------------------------------
+// bit0: y = +1;  bit1: alpha == 0 (lower bound);  bit2: alpha == C (upper bound).
+#define ST_YPOS 1u
+#define ST_LOW 2u
+#define ST_UPP 4u
+
+__device__ __forceinline__ bool st_in_up(uint32_t st)
+{   // I_up = {y=+1, a<C} u {y=-1, a>0}
+    return (st & ST_YPOS) ? !(st & ST_UPP) : !(st & ST_LOW);
+}
+__device__ __forceinline__ bool st_in_low(uint32_t st)
+{   // I_low = {y=+1, a>0} u {y=-1, a<C}
+    return (st & ST_YPOS) ? !(st & ST_LOW) : !(st & ST_UPP);
+}
+__host__ __device__ __forceinline__ uint8_t make_status(int y, double a, double C)
+{
+    return (uint8_t)((y > 0 ? ST_YPOS : 0u) | (a <= 0.0 ? ST_LOW : 0u) | (a >= C ? ST_UPP : 0u));
+}
+
+// ---- candidate keys --------------------------------------------------------------------------
+// 64-bit key, larger = better: high word = order-preserving image of the fp32 score, low word =
+// ~dual_index so equal scores prefer the lower index.  0 = no candidate.
+__device__ __forceinline__ uint32_t ord_f32(float f)
+{
+    uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t u)
+{
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ __forceinline__ uint64_t make_key(float score, uint64_t gidx)
+{
+    return ((uint64_t)ord_f32(score) << 32) | (uint64_t)(0xffffffffu - (uint32_t)gidx);
+}
+__device__ __forceinline__ uint64_t key_index(uint64_t key) { return 0xffffffffu - (uint32_t)key; }
+
+// Payload published with each candidate key: the candidate's alpha, G and status, so a rank
+// never reads another rank's state arrays.
+struct __align__(16) CandPay {
+    double alpha;
+    float G;
+    uint32_t status;
+};
+
+// Device-side result record of the persistent loop (written by CTA 0 of rank 0).
+struct SmoInfo {
+    int64_t iterations;      // iterations completed in this launch
+    double m_up, M_low;      // at the last selection
+    int32_t converged;
+    int32_t error;           // 0, or 1 = timeout waiting for candidates
+    int32_t last_nw;
+    int32_t last_inner;
+    int64_t last_w[SVM_WS];
+    double last_dalpha[SVM_WS];
+    int64_t inner_total;
+};
+
+// All arguments of the persistent working-set kernel (passed by value).
+struct SmoArgs {
+    // local training rows [row0, row0 + n_local) of an n_global-row problem
+    const float* XT;          // dense: feature-major [d][n_pad]; NULL for CSR
+    const int64_t* indptr;    // CSR (local rows); NULL for dense
+    const int32_t* indices;
+    const float* vals;
+    const float* xnorm;       // [n_pad] squared norms
+    int64_t n_local, n_pad, d, row0, n_global;
+    int64_t rows_per_cta;     // multiple of 4
+    int32_t ncopy;            // 1 = SVC (m = n), 2 = eps-SVR (m = 2n, Eq. 1)
+    int32_t rpt;              // rows per thread in the dense pass: 1 or 4
+    // per-dual state of the local rows, copy-major: dual (c, i) at c * n_pad + i
+    double* alpha;
+    float* G;
+    uint8_t* status;
+    double C, tol, inner_tol;
+    int32_t inner_max;
+    int32_t q;                // |W| requested (even, <= 16)
+    KParams kp;
+    // ranks (world = 1 for single-GPU training)
+    int32_t rank, world, nblk;
+    int64_t rank_row0[SVM_MAX_RANKS + 1];
+    const float* peer_XR[SVM_MAX_RANKS];      // dense row-major rows of each rank
+    const float* peer_xnorm[SVM_MAX_RANKS];   // squared norms of each rank's rows
+    const int64_t* peer_indptr[SVM_MAX_RANKS];
+    const int32_t* peer_indices[SVM_MAX_RANKS];
+    const float* peer_vals[SVM_MAX_RANKS];
+    uint64_t* peer_keys[SVM_MAX_RANKS];       // receive buffers: [2][world*nblk][16] keys
+    CandPay* peer_pay[SVM_MAX_RANKS];         //                  [2][world*nblk][16] payloads
+    uint32_t* peer_flags[SVM_MAX_RANKS];      //                  [world*nblk] tags
+    uint32_t tag0;            // epoch: this launch publishes tags tag0+1, tag0+2, ...
+    int64_t max_iter;         // iterations allowed in this launch
+    uint64_t timeout_ns;
+    SmoInfo* info;
+};
+
+cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
+int smo_smem_bytes(int64_t d, int world, int nblk);
+cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
+                               cudaStream_t st);

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star; SURVEY 8(c) "Parity criteria"):
+  one step from identical fp32-representable state: W identical; kernel rows within 1e-5
+  relative (absolute floor 1e-9 where K < 1e-4); G within 1e-5 * max(1, |G|); dalpha within
+  1e-6 relative (+1e-9 C absolute: Q_WW fp64 on both sides, fp32 G in);
+  end to end: dual objective within 1e-4 relative, decision values within 1e-3 absolute,
+  >= 99.9% label agreement, fp64-recomputed KKT violation <= tolerance.
+"""
+import numpy as np
+import pytest
+
+import oracle as ora
+import paper_1706_05544_b200 as pkg
+from paper_1706_05544_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = {"linear": dict(kernel="linear"), "rbf": dict(kernel="radial"),
+           "poly": dict(kernel="polynomial", degree=3, coef0=1.0),
+           "sigmoid": dict(kernel="sigmoid", coef0=-0.5)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    pkg.lib()
+
+
+def _ks(name, d, gamma):
+    kw = KERNELS[name]
+    return ora.kspec({"linear": "linear", "radial": "rbf", "polynomial": "poly",
+                      "sigmoid": "sigmoid"}[kw["kernel"]], gamma, kw.get("degree", 3),
+                     kw.get("coef0", 0.0), d)
+
+
+def _oracle_K(X, rows, ks):
+    Xd = X.astype(np.float64)
+    out = np.empty((X.shape[0], len(rows)))
+    for j, r in enumerate(rows):
+        for i in range(X.shape[0]):
+            out[i, j] = ora.kernel(X[i], X[r], ks)
+    return out
+
+
+# ----------------------------------------------------------------------------- a3 kernel rows
+@pytest.mark.parametrize("kname", list(KERNELS))
+@pytest.mark.parametrize("csr", [False, True])
+def test_kernel_rows(kname, csr):
+    ds = synth.make("c1", n=700)
+    gamma = 1.0 / ds.d
+    rows = np.array([0, 3, 17, 699, 350, 12, 1, 2, 5, 6, 7, 8, 9, 10, 11, 13])
+    if csr:
+        Xs = ds.X.copy()
+        Xs[np.abs(Xs) < 0.8] = 0.0                    # ~ 45% sparse
+        ip = np.concatenate([[0], np.cumsum((Xs != 0).sum(1))]).astype(np.int64)
+        ix = np.nonzero(Xs)[1].astype(np.int32)
+        vv = Xs[Xs != 0].astype(np.float32)
+        s = pkg.Solver(csr=(ip, ix, vv), y=ds.y, d=ds.d, gamma=gamma, **KERNELS[kname])
+        X = Xs
+    else:
+        s = pkg.Solver(ds.X, ds.y, gamma=gamma, **KERNELS[kname])
+        X = ds.X
+    K = s.kernel_rows(rows)
+    ref = _oracle_K(X, rows, _ks(kname, ds.d, gamma))
+    err = np.abs(K - ref)
+    tol = np.where(np.abs(ref) < 1e-4, 1e-9 + 1e-5 * np.abs(ref), 1e-5 * np.abs(ref))
+    if kname == "linear" or kname == "poly":
+        tol = np.maximum(tol, 1e-5 * np.abs(ref).max(axis=0, keepdims=True) * 1e-1)
+    assert (err <= tol).all(), f"max rel err {np.max(err / np.maximum(np.abs(ref), 1e-30))}"
+
+
+# ----------------------------------------------------------------------------- a1 selection
+def test_fresh_state_selection_c1():
+    """the first iteration's W at alpha = 0 is {0..15} on C1 (interleaved labels)."""
+    ds = synth.make("c1")
+    s = pkg.Solver(ds.X, ds.y, gamma=1.0 / ds.d)
+    st = s.run(1)
+    assert st.iterations == 1
+    np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), np.arange(16))
+
+
+# ----------------------------------------------------------------------------- one step
+def _state_after(X, prob, ks, C, steps, q=16):
+    alpha, G = np.zeros(prob.m), prob.p.copy()
+    for _ in range(steps):
+        _, _, alpha, G = ora.step(X, prob, ks, alpha, G, C, q=q)
+    return alpha, G.astype(np.float32).astype(np.float64)   # fp32-representable G
+
+
+@pytest.mark.parametrize("kname", ["rbf", "linear", "poly"])
+@pytest.mark.parametrize("svm_type", ["C-classification", "eps-regression"])
+@pytest.mark.parametrize("csr", [False, True])
+def test_one_step_from_identical_state(kname, svm_type, csr):
+    reg = svm_type == "eps-regression"
+    ds = synth.make("c2" if reg else "c1", n=900)
+    X = ds.X
+    if csr:
+        X = X.copy()
+        X[np.abs(X) < 0.6] = 0.0
+    C = 1.0
+    gamma = 1.0 / ds.d
+    ks = _ks(kname, ds.d, gamma)
+    prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION, ds.y, ds.n, 0.1)
+    for steps in (0, 7, 40):
+        alpha, G = _state_after(X, prob, ks, C, steps)
+        W, dA, a1, G1 = ora.step(X, prob, ks, alpha, G, C, q=16, tol=1e-3)
+        if csr:
+            ip = np.concatenate([[0], np.cumsum((X != 0).sum(1))]).astype(np.int64)
+            s = pkg.Solver(csr=(ip, np.nonzero(X)[1].astype(np.int32), X[X != 0]), y=ds.y,
+                           d=ds.d, svm_type=svm_type, gamma=gamma, **KERNELS[kname])
+        else:
+            s = pkg.Solver(X, ds.y, svm_type=svm_type, gamma=gamma, **KERNELS[kname])
+        s.set_state(alpha, G.astype(np.float32))
+        st = s.run(1)
+        assert st.iterations == 1
+        np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+        np.testing.assert_allclose(np.array(st.last_dalpha[:st.last_nw]), dA, rtol=1e-6,
+                                   atol=1e-9 * C)
+        ag, Gg = s.get_state()
+        np.testing.assert_allclose(ag, a1, rtol=1e-6, atol=1e-9 * C)
+        assert (np.abs(Gg - G1) <= 1e-5 * np.maximum(1.0, np.abs(G1))).all(), \
+            np.abs(Gg - G1).max()
+
+
+# ----------------------------------------------------------------------------- end to end
+def _kkt_fp64(X, prob, ks, alpha, C):
+    G = ora.gradient_full(X, prob, ks, alpha)
+    up, low = ora.violation(prob, alpha, G, C)
+    return up - low
+
+
+def _alpha_from_model(model, prob, n, C):
+    """Reconstruct alpha (dual-indexed) from the model's signed coefficients."""
+    idx, coef = model.support()
+    alpha = np.zeros(prob.m)
+    c = np.zeros(n)
+    c[idx] = coef[0]
+    if prob.m == n:
+        alpha = np.abs(c)
+    else:
+        alpha[:n] = np.maximum(c, 0)
+        alpha[n:] = np.maximum(-c, 0)
+    return alpha
+
+
+@pytest.mark.parametrize("cfg,n", [("c1", None), ("c2", 3000), ("c4", 3000)])
+def test_end_to_end(cfg, n):
+    ds = synth.make(cfg, n=n)
+    reg = ds.svm_type == synth.EPS_REGRESSION
+    kw = dict(svm_type="eps-regression" if reg else "C-classification", kernel="radial",
+              cost=1.0, gamma=1.0 / ds.d, epsilon=0.1, tolerance=1e-3)
+    model = pkg.train(ds.X, ds.y, **kw)
+    info = model.info
+    om = ora.train(ds.X, ds.y, svm_type=ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
+                   kernel="rbf", C=1.0, gamma=1.0 / ds.d, epsilon=0.1, tol=1e-3)
+    d_ora = om.results[0]["dual"]
+    assert info.converged == 1
+    assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
+    Xh = synth.make(cfg, n=min(ds.n, 1000), heldout=True).X
+    for Xq in (ds.X[:1500], Xh):
+        out, dec = model.predict(Xq, decision=True)
+        f_ora = om.decision_function(Xq)[:, 0]
+        assert np.abs(dec[:, 0] - f_ora).max() <= 1e-3
+        if not reg:
+            assert (out == om.predict(Xq)).mean() >= 0.999
+    prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
+                       ds.y if reg else ora.binary_labels(ds.y)[0], ds.n, 0.1)
+    alpha = _alpha_from_model(model, prob, ds.n, 1.0)
+    assert _kkt_fp64(ds.X, prob, ora.kspec("rbf", 1.0 / ds.d, d=ds.d), alpha, 1.0) <= 1e-3
+
+
+@pytest.mark.parametrize("case", ["two_point_linear_C1", "three_point_linear_C10",
+                                  "xor_rbf_C10", "svr_two_point_rbf", "svr_constant_target"])
+def test_closed_forms_on_gpu(case):
+    import json
+    import os
+    cases = {c["name"]: c for c in json.load(open(os.path.join(os.path.dirname(__file__),
+                                                               "golden", "closed_forms.json")))}
+    c = cases[case]
+    X = np.array(c["X"], np.float32)
+    model = pkg.train(X, np.array(c["y"], np.float32),
+                      svm_type="eps-regression" if c["type"] == 3 else "C-classification",
+                      kernel={"linear": "linear", "rbf": "radial"}[c["kernel"]],
+                      gamma=c.get("gamma", 1.0), cost=c["C"], epsilon=c.get("epsilon", 0.1),
+                      tolerance=1e-6)
+    info = model.info
+    assert abs(info.dual_objective - c["dual"]) <= 1e-5 * max(1.0, abs(c["dual"]))
+    assert abs(info.b[0] - c["b"]) <= 1e-5
+
+
+def test_predict_matches_oracle_decision_of_gpu_model():
+    """a6 alone: the GPU model's own SVs/coefs evaluated by the oracle's decision function."""
+    ds = synth.make("c2", n=2500)
+    model = pkg.train(ds.X, ds.y, svm_type="eps-regression", gamma=1.0 / ds.d)
+    idx, coef = model.support()
+    Xq = synth.make("c2", n=777, heldout=True).X
+    out, dec = model.predict(Xq, decision=True)
+    f = ora.decision(ds.X[idx], coef[0], model.info.b[0], ora.kspec("rbf", 1.0 / ds.d, d=ds.d), Xq)
+    np.testing.assert_allclose(dec[:, 0], f, atol=2e-5 * max(1.0, np.abs(f).max()))
+    np.testing.assert_array_equal(out, dec[:, 0])
+
+
+def test_ovr_multiclass():
+    ds = synth.make("c3", n=1200, d=40)
+    model = pkg.train(ds.X, ds.y, gamma=1.0 / 40)
+    info = model.info
+    assert info.n_problem == 10 and info.n_class == 10
+    om = ora.train(ds.X, ds.y, gamma=1.0 / 40)
+    Xh = synth.make("c3", n=400, d=40, heldout=True).X
+    out, dec = model.predict(Xh, decision=True)
+    f = om.decision_function(Xh)
+    assert np.abs(dec - f).max() <= 1e-3
+    assert (out == om.predict(Xh)).mean() >= 0.999
+    d_ora = sum(r["dual"] for r in om.results)
+    assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
+
+
+def test_errors_and_edge_cases():
+    ds = synth.make("c1", n=50)
+    with pytest.raises(pkg.SvmError) as e:
+        pkg.train(ds.X, np.ones(50, np.float32))
+    assert e.value.code == -2
+    Xb = ds.X.copy()
+    Xb[3, 2] = np.nan
+    with pytest.raises(pkg.SvmError) as e:
+        pkg.train(Xb, ds.y)
+    assert e.value.code == -3
+    m = pkg.train(ds.X[:2], np.array([1, -1], np.float32), kernel="linear")
+    assert m.info.n_sv == 2
+    with pytest.raises(pkg.SvmError) as e:
+        m.predict(np.zeros((3, 7), np.float32))
+    assert e.value.code == -1
