@@ -166,6 +166,17 @@ def step(X, prob: Problem, ks, alpha, G, C, q=16, tol=1e-3, inner_max=None):
     return W[:nw].copy(), dA[:nw].copy(), alpha, G
 
 
+def gradient_update(X, prob: Problem, ks, W, dalpha, G):
+    """Step 6 applied to a given working set and alpha change: returns the new G."""
+    X = np.ascontiguousarray(X, np.float32)
+    W = np.ascontiguousarray(W, np.int64)
+    dalpha = np.ascontiguousarray(dalpha, np.float64)
+    Gn = np.array(G, np.float64)
+    lib().ora_gradient_update(_p(X), X.shape[1], prob.m, _p(prob.y), _p(prob.map), len(W), _p(W),
+                              _p(dalpha), ctypes.byref(ks), _p(Gn))
+    return Gn
+
+
 def gradient_full(X, prob: Problem, ks, alpha):
     X = np.ascontiguousarray(X, np.float32)
     G = np.empty(prob.m)

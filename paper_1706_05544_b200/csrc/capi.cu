@@ -305,17 +305,14 @@ static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, con
 // ================================================================ one binary problem (Eq. 2)
 struct Exchange {
     int L = 0;
-    DBuf keys, pay, flags, info;
+    DBuf xw, info;               // candidate words [2][L][XW_PER_SLOT] (self-tagged), loop info
     uint32_t epoch = 0;
     int alloc(int L_)
     {
         L = L_;
-        TRY(keys.alloc(sizeof(uint64_t) * 2 * L * 16));
-        TRY(pay.alloc(sizeof(CandPay) * 2 * L * 16));
-        TRY(flags.alloc(sizeof(uint32_t) * L));
+        TRY(xw.alloc(sizeof(uint64_t) * 2 * L * XW_PER_SLOT));
         TRY(info.alloc(sizeof(SmoInfo)));
-        CK(cudaMemset(flags.p, 0, sizeof(uint32_t) * L));
-        CK(cudaMemset(keys.p, 0, keys.bytes));
+        CK(cudaMemset(xw.p, 0, xw.bytes));
         return SVM_OK;
     }
 };
@@ -364,9 +361,8 @@ struct ShardCtx {
     const int64_t* indptr[SVM_MAX_RANKS] = {};
     const int32_t* indices[SVM_MAX_RANKS] = {};
     const float* vals[SVM_MAX_RANKS] = {};
-    uint64_t* keys[SVM_MAX_RANKS] = {};
-    CandPay* pay[SVM_MAX_RANKS] = {};
-    uint32_t* flags[SVM_MAX_RANKS] = {};
+    int64_t rpc[SVM_MAX_RANKS] = {};
+    uint64_t* xw[SVM_MAX_RANKS] = {};
 };
 
 static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx* sc = nullptr)
@@ -406,9 +402,8 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.peer_indptr[0] = D.indptr;
     a.peer_indices[0] = D.indices;
     a.peer_vals[0] = D.vals;
-    a.peer_keys[0] = E.keys.as<uint64_t>();
-    a.peer_pay[0] = E.pay.as<CandPay>();
-    a.peer_flags[0] = E.flags.as<uint32_t>();
+    a.rank_rpc[0] = D.rows_per_cta;
+    a.peer_xw[0] = E.xw.as<uint64_t>();
     a.timeout_ns = 30ull * 1000000000ull;
     a.info = E.info.as<SmoInfo>();
     if (sc && sc->world > 1) {
@@ -423,9 +418,8 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
             a.peer_indptr[r] = sc->indptr[r];
             a.peer_indices[r] = sc->indices[r];
             a.peer_vals[r] = sc->vals[r];
-            a.peer_keys[r] = sc->keys[r];
-            a.peer_pay[r] = sc->pay[r];
-            a.peer_flags[r] = sc->flags[r];
+            a.rank_rpc[r] = sc->rpc[r];
+            a.peer_xw[r] = sc->xw[r];
         }
         a.timeout_ns = 60ull * 1000000000ull;
     }
@@ -440,7 +434,26 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     a.tag0 = E.epoch;
     a.max_iter = max_iter;
     CK(cudaMemsetAsync(E.info.p, 0, sizeof(SmoInfo), st));
-    int smem = smo_smem_bytes(D.d, a.world, D.nblk);
+    const int64_t score_elems = D.rows_per_cta * P.ncopy;
+    const int64_t smem_cap = 200 * 1024;
+    DBuf score_glb;
+    int smem = smo_smem_bytes(D.d, a.world, D.nblk, score_elems, D.csr ? 0 : D.rows_per_cta);
+    if (!D.csr && smem <= smem_cap && !getenv("SVMB200_NO_XSMEM")) {
+        a.x_in_smem = 1;  // this CTA's X slice stays resident in shared memory
+    } else {
+        smem = smo_smem_bytes(D.d, a.world, D.nblk, score_elems, 0);
+        if (smem > smem_cap) {  // score arrays do not fit next to X_W: keep them in global (L2)
+            TRY(score_glb.alloc(sizeof(uint32_t) * 2 * score_elems * D.nblk));
+            a.score_global = score_glb.as<uint32_t>();
+            smem = smo_smem_bytes(D.d, a.world, D.nblk, 0, 0);
+        }
+    }
+    if (smem > 220 * 1024)
+        return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d lists)", smem,
+                    (long long)D.d, a.world * D.nblk);
+    if (score_elems > 65535)
+        return fail(SVM_EINVAL, "%lld dual variables per CTA exceed the 16-bit candidate position",
+                    (long long)score_elems);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -468,6 +481,27 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     P.converged = info.converged != 0;
     P.loop_ms += ms;
     P.last_info = info;
+    if (getenv("SVMB200_PROFILE")) {
+        int clk = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+        double tot = 0;
+        for (int i = 0; i < 8; ++i) tot += (double)info.phase_cycles[i];
+        fprintf(stderr, "[svmb200] %lld iters, %.1f ms: phases (cycles/iter) wait+stage %.0f merge+W %.0f rows %.0f "
+                "qww %.0f sub %.0f pass %.0f select %.0f publish %.0f | total %.0f | inner/iter %.1f\n",
+                (long long)info.iterations, ms,
+                info.phase_cycles[0] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[1] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[2] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[3] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[4] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[5] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[6] / (double)std::max<int64_t>(1, info.iterations),
+                info.phase_cycles[7] / (double)std::max<int64_t>(1, info.iterations),
+                tot / (double)std::max<int64_t>(1, info.iterations),
+                info.inner_total / (double)std::max<int64_t>(1, info.iterations));
+        (void)clk;
+    }
     if (info_out) *info_out = info;
     return SVM_OK;
 }
@@ -1120,12 +1154,12 @@ extern "C" void svm_solver_free(svm_solver* s) { delete s; }
 // or CSR) and norms, and the per-row coefficient / SV-index export used to gather the model.
 namespace {
 constexpr uint32_t SHARD_MAGIC = 0x53564D42u;  // "SVMB"
-enum { H_KEYS, H_PAY, H_FLAGS, H_XBUF, H_XFLAGS, H_XR, H_NORMS, H_INDPTR, H_INDICES, H_VALS,
-       H_SVIDX, H_COEFX, H_COUNT };
+enum { H_XW, H_XBUF, H_XFLAGS, H_XR, H_NORMS, H_INDPTR, H_INDICES, H_VALS, H_SVIDX, H_COEFX,
+       H_COUNT };
 struct ShardHandle {
     uint32_t magic;
     int32_t rank, world, nblk, csr, nprob, ncopy, pad;
-    int64_t n_local, row0, n_global, d;
+    int64_t n_local, row0, n_global, d, rows_per_cta;
     cudaIpcMemHandle_t h[H_COUNT];
 };
 static_assert(sizeof(ShardHandle) <= SVM_SHARD_HANDLE_BYTES, "shard handle too large");
@@ -1286,7 +1320,8 @@ extern "C" int svm_shard_handle(const svm_shard* S, void* handle)
     H.row0 = S->row0;
     H.n_global = S->n_global;
     H.d = S->D.d;
-    const void* ptrs[H_COUNT] = {S->E.keys.p, S->E.pay.p, S->E.flags.p, S->xbuf.p, S->xflags.p,
+    H.rows_per_cta = S->D.rows_per_cta;
+    const void* ptrs[H_COUNT] = {S->E.xw.p, S->xbuf.p, S->xflags.p,
                                  S->D.csr ? nullptr : S->D.XR, S->D.norms.p,
                                  S->D.csr ? S->D.indptr : nullptr, S->D.csr ? S->D.indices : nullptr,
                                  S->D.csr ? S->D.vals : nullptr, S->svidx.p, S->coefx.p};
@@ -1326,7 +1361,7 @@ extern "C" int svm_shard_connect(svm_shard* S, const void* all_handles)
         S->svp.row0[r] = H.row0;
         void* p[H_COUNT] = {};
         if (r == S->rank) {
-            void* mine[H_COUNT] = {S->E.keys.p, S->E.pay.p, S->E.flags.p, S->xbuf.p, S->xflags.p,
+            void* mine[H_COUNT] = {S->E.xw.p, S->xbuf.p, S->xflags.p,
                                    S->D.csr ? nullptr : (void*)S->D.XR, S->D.norms.p,
                                    S->D.csr ? (void*)S->D.indptr : nullptr,
                                    S->D.csr ? (void*)S->D.indices : nullptr,
@@ -1345,9 +1380,8 @@ extern "C" int svm_shard_connect(svm_shard* S, const void* all_handles)
                 S->opened.push_back(p[i]);
             }
         }
-        c.keys[r] = (uint64_t*)p[H_KEYS];
-        c.pay[r] = (CandPay*)p[H_PAY];
-        c.flags[r] = (uint32_t*)p[H_FLAGS];
+        c.xw[r] = (uint64_t*)p[H_XW];
+        c.rpc[r] = H.rows_per_cta;
         c.XR[r] = (const float*)p[H_XR];
         c.norms[r] = (const float*)p[H_NORMS];
         c.indptr[r] = (const int64_t*)p[H_INDPTR];

@@ -6,15 +6,18 @@
 //   a1  merges the 8+8 candidates every CTA (of every rank) published into the working set W
 //       ("picking 16 dual space coefficients based on which partial derivatives ... are the
 //       largest, subject to dual space constraints") -- redundantly and identically
-//       in every CTA, so no CTA waits on a single solver;
+//       in every CTA, so no CTA ever waits on a single solver CTA;
 //   a2  solves the |W|-variable subproblem in fp64 on warp 0 ("optimized based on the local
-//       gradient"; P:69 for eps-SVR) WHILE the other 15 warps already stream X and form
-//       the kernel rows K(x_i, X_W) for their first rows;
+//       gradient"; P:69 for eps-SVR) WHILE the other 15 warps already form the kernel-row
+//       dot products x_i . X_W for their rows;
 //   a3  finishes the fused pass G_i += y_i sum_r c_r K(x_i, x_r) ("calculating the gradient for
-//       all dual space coefficients"; "the responses terms are updated") and keeps a
-//       running per-warp top-8 of the new scores, so the n x |W| kernel block is never stored;
-//   and publishes its CTA top-8 up / top-8 low keys + payloads into every rank's receive buffer
-//   with a release flag (the one-shot all-gather of SURVEY 8(e), fused into the pass).
+//       all dual space coefficients"; "the responses terms are updated"), writing the
+//       new up/low scores to shared memory -- the n x |W| kernel block is never stored;
+//   and writes its CTA top-8 up / top-8 low candidates as self-tagged 8-byte words into every
+//   rank's receive buffer (the one-shot all-gather of SURVEY 8(e), fused into the pass; no fence,
+//   no flag: readers poll the words' tags).
+// Measured B200 latencies that shaped this (scripts/ubench.cu): REDUX 22 cycles, SHFL 30, LDS 54,
+// L2 load ~290, __threadfence ~800-1100, __threadfence_system ~1700-3100, flag round trip ~3000.
 // DESIGN.md has the layout, the roofline and what differs from the paper's GTSVM design.
 #include "svm_internal.cuh"
 
@@ -24,20 +27,19 @@
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int SOLVER_WARP = SMO_WARPS - 1;
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p)
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p, bool sys)
 {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    uint64_t v;
+    if (sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v)
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v, bool sys)
 {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v)
-{
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer_ns()
 {
@@ -63,31 +65,16 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t k)
     return ((uint64_t)mh << 32) | ml;
 }
 
-// Running top-8 of a warp: lane l < 8 holds the l-th largest key offered so far (0 = empty).
-struct WarpTop8 {
-    uint64_t v;
-    __device__ __forceinline__ void reset() { v = 0; }
-    __device__ __forceinline__ uint64_t thresh() const { return __shfl_sync(FULL, v, 7); }
-    __device__ __forceinline__ void insert(uint64_t k, int lane)
-    {
-        uint64_t prev = __shfl_up_sync(FULL, v, 1);
-        if (lane < 8 && k > v) v = (lane == 0 || prev > k) ? k : prev;
-    }
-    // Offer one key per lane (0 = none).  Keys are unique, so the result is exact.
-    __device__ __forceinline__ void offer(uint64_t key, int lane)
-    {
-        uint64_t th = thresh();
-        unsigned b = __ballot_sync(FULL, key > th);
-        while (b) {
-            int src = __ffs(b) - 1;
-            uint64_t k = __shfl_sync(FULL, key, src);
-            insert(k, lane);
-            th = thresh();
-            b &= ~(1u << src);
-            b &= __ballot_sync(FULL, key > th);
-        }
-    }
-};
+// Order-preserving map of fp64 to u64 (exact, so argmax over keys == argmax over values).
+__device__ __forceinline__ uint64_t mono64(double x)
+{
+    uint64_t u = (uint64_t)__double_as_longlong(x + 0.0);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unmono64(uint64_t u)
+{
+    return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
 
 template <int RPT>
 __device__ __forceinline__ void zero_acc(float (&acc)[RPT][SVM_WS])
@@ -98,28 +85,28 @@ __device__ __forceinline__ void zero_acc(float (&acc)[RPT][SVM_WS])
         for (int r = 0; r < SVM_WS; ++r) acc[j][r] = 0.0f;
 }
 
-// Dense kernel-row dot products: acc[j][r] = x_{li+j} . x_{W_r} for RPT consecutive rows.
-// X is feature-major (one coalesced 4*RPT-byte load per lane per feature); X_W^T sits in shared
-// memory as [d][16] and is read with 4 broadcast LDS.128 per feature, feeding 16*RPT FFMA.
+// Dense kernel-row dot products acc[j][r] = x_{li+j} . x_{W_r} for RPT consecutive rows.  X^T is
+// feature-major with row stride `ld` (global [d][n_pad], or the CTA's slice staged in shared
+// memory); X_W^T is [d][16] in shared memory, read with 4 broadcast LDS.128 per feature.
 template <int RPT>
-__device__ __forceinline__ void dots_dense(const float* __restrict__ XT, int64_t n_pad, int d,
-                                           int64_t li, bool active, const float* sXW,
+__device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64_t ld, int d,
+                                           bool active, const float* sXW,
                                            float (&acc)[RPT][SVM_WS])
 {
     zero_acc<RPT>(acc);
     if (!active) return;
-    const float* p = XT + li;
+    const float* p = xcol;
     const float4* w4 = reinterpret_cast<const float4*>(sXW);
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < d; ++k) {
         float x[RPT];
         if constexpr (RPT == 4) {
-            float4 v = __ldg(reinterpret_cast<const float4*>(p));
+            float4 v = *reinterpret_cast<const float4*>(p);
             x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
         } else {
-            x[0] = __ldg(p);
+            x[0] = *p;
         }
-        p += n_pad;
+        p += ld;
         float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
@@ -158,18 +145,21 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
     }
 }
 
-// Shared state of one persistent CTA (static part; X_W and the staged keys are dynamic).
+// Shared state of one persistent CTA (static part; X_W, the staged keys, the score arrays and
+// the optional X slice are dynamic).
 struct SmoShared {
     uint64_t warp_up[SMO_WARPS][8], warp_low[SMO_WARPS][8];
     uint64_t cta_up[8], cta_low[8];
     uint64_t win_up[8], win_low[8];      // merged global winners (keys)
     int32_t win_up_src[8], win_low_src[8];
     int64_t w_gidx[SVM_WS];              // working set, ascending dual index
-    int32_t w_src[SVM_WS];               // payload slot of each position
+    int32_t w_src[SVM_WS];               // exchange word index (slot * 64 + candidate) per position
     int32_t w_slot[SVM_WS];              // distinct-row slot of each position
     int64_t r_row[SVM_WS];               // distinct rows (global)
     double kr[SVM_WS * SVM_WS];          // K between distinct rows, fp64
-    double qww[SVM_WS * SVM_WS];         // Q_WW = y_a y_b K
+    double kpos[SVM_WS * SVM_WS];        // K between working-set positions, fp64
+    double inv_eta[SVM_WS * SVM_WS];     // 1 / max(K_aa + K_bb - 2 K_ab, tau)
+    double qpart[136 * 4];               // k-split partial sums of the row-pair reductions
     double w_alpha[SVM_WS], w_G[SVM_WS], w_dalpha[SVM_WS], w_anew[SVM_WS];
     int32_t w_y[SVM_WS];
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
@@ -178,42 +168,94 @@ struct SmoShared {
     double m_up, M_low;
 };
 
-// Per-row epilogue shared by the scan (do_update = false) and the pass.
+// Per-row epilogue shared by the scan (do_update = false) and the pass: kernel values from the
+// dot products, G update, and the row's up / low scores (0 = not a candidate) into the CTA's
+// score arrays at position c * rows_per_cta + (li - cta_begin).
 template <int RPT>
-__device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& sh,
-                                             int64_t li0, int64_t cta_end, bool do_update,
-                                             const float (&acc)[RPT][SVM_WS], WarpTop8& up,
-                                             WarpTop8& low, int lane)
+__device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& sh, int64_t li0,
+                                             int64_t cta_begin, int64_t cta_end, bool do_update,
+                                             const float (&acc)[RPT][SVM_WS], uint32_t* scU,
+                                             uint32_t* scL)
 {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         int64_t li = li0 + j;
-        bool valid = li < cta_end;
+        if (li >= cta_end) continue;
         float S = 0.0f;
-        if (valid && do_update) {
+        if (do_update) {
             float xn = __ldg(a.xnorm + li);
 #pragma unroll
             for (int r = 0; r < SVM_WS; ++r)
                 S = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]), S);
         }
         for (int c = 0; c < a.ncopy; ++c) {
-            uint64_t ku = 0, kl = 0;
-            if (valid) {
-                int64_t idx = (int64_t)c * a.n_pad + li;
-                uint32_t st = a.status[idx];
-                float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
-                float g = a.G[idx];
-                if (do_update) {
-                    g = fmaf(yv, S, g);
-                    a.G[idx] = g;
-                }
-                float s = -yv * g;
-                uint64_t gidx = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(a.row0 + li);
-                if (st_in_up(st)) ku = make_key(s, gidx);
-                if (st_in_low(st)) kl = make_key(-s, gidx);
+            int64_t idx = (int64_t)c * a.n_pad + li;
+            uint32_t st = a.status[idx];
+            float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
+            float g = a.G[idx];
+            if (do_update) {
+                g = fmaf(yv, S, g);
+                a.G[idx] = g;
             }
-            up.offer(ku, lane);
-            low.offer(kl, lane);
+            float sc = -yv * g;
+            int pos = c * (int)a.rows_per_cta + (int)(li - cta_begin);
+            scU[pos] = st_in_up(st) ? ord_f32(sc) : 0u;
+            scL[pos] = st_in_low(st) ? ord_f32(-sc) : 0u;
+        }
+    }
+}
+
+// Top-8 keys of one warp's segment of a CTA score array by extraction rounds (warp max; only the
+// winning lane rescans its positions below the extracted key).  Both arrays at once for ILP.
+__device__ __forceinline__ void warp_select2(const uint32_t* scU, const uint32_t* scL, int Rn,
+                                             int R, int nvalid, uint64_t gbase, uint64_t n_global,
+                                             int w, int lane, uint64_t* outU, uint64_t* outL)
+{
+    const int seg = (Rn + SMO_WARPS - 1) / SMO_WARPS;
+    const int p0 = w * seg, p1 = min(p0 + seg, Rn);
+    auto key_at = [&](const uint32_t* sc, int p) -> uint64_t {
+        int c = p >= R ? 1 : 0;
+        int li = p - c * R;
+        uint32_t v = sc[p];
+        if (li >= nvalid || v == 0u) return 0ull;
+        uint64_t g = (uint64_t)c * n_global + gbase + (uint64_t)li;
+        return ((uint64_t)v << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
+    };
+    uint64_t lu = 0, ll = 0;
+    for (int p = p0 + lane; p < p1; p += 32) {
+        uint64_t ku = key_at(scU, p), kl = key_at(scL, p);
+        lu = ku > lu ? ku : lu;
+        ll = kl > ll ? kl : ll;
+    }
+    bool doneU = false, doneL = false;
+    for (int r = 0; r < 8; ++r) {
+        uint64_t bu = warp_max_u64(lu);
+        uint64_t bl = warp_max_u64(ll);
+        if (lane == 0) {
+            outU[r] = doneU ? 0 : bu;
+            outL[r] = doneL ? 0 : bl;
+        }
+        doneU = doneU || bu == 0;
+        doneL = doneL || bl == 0;
+        if (doneU && doneL) {
+            if (lane > r && lane < 8) { outU[lane] = 0; outL[lane] = 0; }
+            break;
+        }
+        const bool wu = !doneU && lu == bu, wl = !doneL && ll == bl;
+        if (wu || wl) {
+            uint64_t nu = 0, nl = 0;
+            for (int p = p0 + lane; p < p1; p += 32) {
+                if (wu) {
+                    uint64_t k = key_at(scU, p);
+                    if (k < bu && k > nu) nu = k;
+                }
+                if (wl) {
+                    uint64_t k = key_at(scL, p);
+                    if (k < bl && k > nl) nl = k;
+                }
+            }
+            if (wu) lu = nu;
+            if (wl) ll = nl;
         }
     }
 }
@@ -223,50 +265,90 @@ __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* 
 {
     int idx = 0;
     uint64_t head = lane < SMO_WARPS ? lists[lane][0] : 0;
+    uint64_t next = lane < SMO_WARPS ? lists[lane][1] : 0;
     for (int r = 0; r < 8; ++r) {
         uint64_t best = warp_max_u64(head);
         if (lane == 0) out[r] = best;
         if (best == 0) {
-            for (int q = r + 1 + lane; q < 8; q += 32) out[q] = 0;
+            if (lane > r && lane < 8) out[lane] = 0;
             break;
         }
         if (head == best && lane < SMO_WARPS) {
             ++idx;
-            head = idx < 8 ? lists[lane][idx] : 0;
+            head = next;
+            next = idx + 1 < 8 ? lists[lane][idx + 1] : 0;
         }
     }
 }
 
 // Global merge of L sorted 8-lists (staged in shared memory as keys[L][8]) into the top-8 (one
-// warp).  src receives list * 8 + position of each winner.
-__device__ __forceinline__ void global_merge(const uint64_t* keys, uint8_t* head, int L,
-                                             uint64_t* out, int32_t* src, int lane)
+// warp).  Lane l owns lists l, l + 32, ... (at most MAXK); heads, current and next keys live in
+// registers.  src receives list * 8 + position of each winner.
+template <int MAXK>
+__device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64_t* out,
+                                             int32_t* src, int lane)
 {
-    for (int l = lane; l < L; l += 32) head[l] = 0;
-    __syncwarp();
-    uint64_t best_local = 0;
-    int best_list = -1;
-    for (int l = lane; l < L; l += 32) {
-        uint64_t k = keys[l * 8];
-        if (k > best_local) { best_local = k; best_list = l; }
+    uint64_t cur[MAXK], nxt[MAXK];
+    int hd[MAXK];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+        int l = lane + 32 * k;
+        cur[k] = l < L ? keys[l * 8] : 0;
+        nxt[k] = l < L ? keys[l * 8 + 1] : 0;
+        hd[k] = 0;
     }
     for (int r = 0; r < 8; ++r) {
-        uint64_t best = warp_max_u64(best_local);
+        uint64_t lb = cur[0];
+#pragma unroll
+        for (int k = 1; k < MAXK; ++k) lb = cur[k] > lb ? cur[k] : lb;
+        uint64_t best = warp_max_u64(lb);
         if (best == 0) {
             if (lane < 8 && lane >= r) { out[lane] = 0; src[lane] = -1; }
             break;
         }
-        if (best_local == best) {  // unique owner
-            int h = head[best_list];
+        if (lb == best) {  // unique owner
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) {
+                if (cur[k] == best) {
+                    int l = lane + 32 * k;
+                    out[r] = best;
+                    src[r] = l * 8 + hd[k];
+                    ++hd[k];
+                    cur[k] = nxt[k];
+                    nxt[k] = hd[k] + 1 < 8 ? keys[l * 8 + hd[k] + 1] : 0;
+                }
+            }
+        }
+    }
+}
+
+// Large-L variant (multi-rank runs): heads in shared memory, the winner rescans its lists.
+__device__ __noinline__ void global_merge_smem(const uint64_t* keys, uint8_t* head, int L,
+                                               uint64_t* out, int32_t* src, int lane)
+{
+    for (int l = lane; l < L; l += 32) head[l] = 0;
+    __syncwarp();
+    uint64_t lb = 0;
+    int ll = -1;
+    for (int l = lane; l < L; l += 32)
+        if (keys[l * 8] > lb) { lb = keys[l * 8]; ll = l; }
+    for (int r = 0; r < 8; ++r) {
+        uint64_t best = warp_max_u64(lb);
+        if (best == 0) {
+            if (lane < 8 && lane >= r) { out[lane] = 0; src[lane] = -1; }
+            break;
+        }
+        if (lb == best) {
+            const int h = head[ll];
             out[r] = best;
-            src[r] = best_list * 8 + h;
-            head[best_list] = (uint8_t)(h + 1);
-            best_local = 0;
-            best_list = -1;
+            src[r] = ll * 8 + h;
+            head[ll] = (uint8_t)(h + 1);
+            lb = 0;
+            ll = -1;
             for (int l = lane; l < L; l += 32) {
-                int hh = head[l];
-                uint64_t k = hh < 8 ? keys[l * 8 + hh] : 0;
-                if (k > best_local) { best_local = k; best_list = l; }
+                const int hh = head[l];
+                const uint64_t k = hh < 8 ? keys[l * 8 + hh] : 0;
+                if (k > lb) { lb = k; ll = l; }
             }
         }
         __syncwarp();
@@ -280,7 +362,68 @@ __device__ __forceinline__ int owner_rank(const SmoArgs& a, int64_t row)
     return r;
 }
 
-template <bool CSR, int RPT>
+// The |W|-variable subproblem (a2) on warp 0, lane a = position a: max-violating-pair steps in
+// fp64 ("optimized based on the local gradient").  argmax_{I_up} s and
+// argmin_{I_low} s are exact 64-bit REDUX reductions of order-preserving keys, ties to the lowest
+// lane = lowest position.  The step in score form (s_a = -y_a G_a):
+//   t = (s_i - s_j) / eta_ij clipped to the box;  s_a += t (K_aj - K_ai)
+// which is the oracle's G_W += Q_Wi y_i t - Q_Wj y_j t, since Q_ab = y_a y_b K_ab.
+__device__ __forceinline__ double lds_f64(uint32_t addr)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C, double inner_tol,
+                                                int inner_max, int lane)
+{
+    const int pa = lane & 15;
+    const bool valid = lane < nw;
+    const int y = valid ? sh.w_y[lane] : 1;
+    double al = valid ? sh.w_alpha[lane] : 0.0;
+    double s = valid ? -(double)y * sh.w_G[lane] : 0.0;
+    const uint32_t ypos = __ballot_sync(FULL, y > 0);
+    // shared-window addresses computed once (keeps S2R/LEA off the per-step chain)
+    const uint32_t a_ie = (uint32_t)__cvta_generic_to_shared(sh.inv_eta);
+    const uint32_t a_krow = (uint32_t)__cvta_generic_to_shared(sh.kpos + pa * SVM_WS);
+    int step = 0;
+    for (; step < inner_max; ++step) {
+        const bool upok = valid && (y > 0 ? al < C : al > 0.0);
+        const bool lowok = valid && (y > 0 ? al > 0.0 : al < C);
+        const uint64_t ku = upok ? mono64(s) : 0ull, kl = lowok ? mono64(-s) : 0ull;
+        const uint32_t hu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32));
+        const uint32_t hl = __reduce_max_sync(FULL, (uint32_t)(kl >> 32));
+        const uint32_t lu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32) == hu ? (uint32_t)ku : 0u);
+        const uint32_t ll = __reduce_max_sync(FULL, (uint32_t)(kl >> 32) == hl ? (uint32_t)kl : 0u);
+        const uint64_t mu = ((uint64_t)hu << 32) | lu, ml = ((uint64_t)hl << 32) | ll;
+        const int i = __ffs(__ballot_sync(FULL, ku == mu)) - 1;
+        const int j = __ffs(__ballot_sync(FULL, kl == ml)) - 1;
+        const double si = unmono64(mu), sj = -unmono64(ml);
+        if (mu == 0 || ml == 0 || si - sj <= inner_tol) break;
+        const double ie = lds_f64(a_ie + 8u * (uint32_t)(i * SVM_WS + j));
+        const double kai = lds_f64(a_krow + 8u * (uint32_t)i);
+        const double kaj = lds_f64(a_krow + 8u * (uint32_t)j);
+        const double ai = __shfl_sync(FULL, al, i), aj = __shfl_sync(FULL, al, j);
+        const bool yi = (ypos >> i) & 1u, yj = (ypos >> j) & 1u;
+        double t = (si - sj) * ie;
+        const double lim_i = yi ? C - ai : ai;
+        const double lim_j = yj ? aj : C - aj;
+        const bool ci = t >= lim_i;
+        t = ci ? lim_i : t;
+        const bool cj = t >= lim_j;
+        t = cj ? lim_j : t;
+        const bool clip_i = ci && (!cj || lim_i == lim_j);
+        const double ni = clip_i ? (yi ? C : 0.0) : (yi ? ai + t : ai - t);
+        const double nj = cj ? (yj ? 0.0 : C) : (yj ? aj - t : aj + t);
+        al = lane == i ? ni : (lane == j ? nj : al);
+        s = fma(t, kaj - kai, s);
+    }
+    if (lane < SVM_WS) sh.w_anew[lane] = al;
+    return step;
+}
+
+template <bool CSR, int RPT, bool XS>
 __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a)
 {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -288,161 +431,228 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int L = a.world * a.nblk;
     const int d = (int)a.d;
-    float* sXW = reinterpret_cast<float*>(dyn_smem);                       // [d][16]
-    uint64_t* sKU = reinterpret_cast<uint64_t*>(dyn_smem + (size_t)d * 64);  // [L][8]
-    uint64_t* sKL = sKU + (size_t)L * 8;                                    // [L][8]
-    uint8_t* sHeadU = reinterpret_cast<uint8_t*>(sKL + (size_t)L * 8);      // [L]
-    uint8_t* sHeadL = sHeadU + L;
+    const int dp = (d + 3) & ~3;
+    const int R = (int)a.rows_per_cta;
+    const int Rn = R * a.ncopy;
+    float* sXW = reinterpret_cast<float*>(dyn_smem);                        // [d][16]
+    float* sXWr = sXW + (size_t)d * SVM_WS;                                  // [16][dp]
+    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWr + (size_t)SVM_WS * dp);  // [L][8]
+    uint64_t* sKL = sKU + (size_t)L * 8;                                     // [L][8]
+    uint32_t* scU = a.score_global ? a.score_global + (size_t)blockIdx.x * 2 * Rn
+                                   : reinterpret_cast<uint32_t*>(sKL + (size_t)L * 8);
+    uint32_t* scL = scU + Rn;
+    float* sX = reinterpret_cast<float*>(
+        a.score_global ? reinterpret_cast<unsigned char*>(sKL + (size_t)L * 8)
+                       : reinterpret_cast<unsigned char*>(scL + ((Rn + 3) & ~3)));  // [d][R]
 
     const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
     const int64_t cta_end = min(cta_begin + a.rows_per_cta, a.n_local);
+    const int nvalid = cta_end > cta_begin ? (int)(cta_end - cta_begin) : 0;
     const int rows_per_chunk = 32 * RPT;
-    const int nchunks = cta_end > cta_begin
-                            ? (int)((cta_end - cta_begin + rows_per_chunk - 1) / rows_per_chunk)
-                            : 0;
+    const int nchunks = (nvalid + rows_per_chunk - 1) / rows_per_chunk;
     const int slot = a.rank * a.nblk + blockIdx.x;
     const bool sys = a.world > 1;
     const bool reporter = blockIdx.x == 0;  // CTA 0 of every rank reports for its rank
+    const uint64_t gbase = (uint64_t)(a.row0 + cta_begin);
+    uint64_t* rxw = a.peer_xw[a.rank];       // this rank's receive buffer
 
-    // ---- publish: CTA top-8 lists -> every rank's receive buffer, then the release flag ------
-    auto publish = [&](uint32_t tag) {
-        const int par = tag & 1;
-        if (tid < 16) {
-            uint64_t k = tid < 8 ? sh.cta_up[tid] : sh.cta_low[tid - 8];
-            CandPay pay = {0.0, 0.0f, 0u};
-            if (k) {
-                uint64_t g = key_index(k);
-                int c = g >= (uint64_t)a.n_global ? 1 : 0;
-                int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - a.row0;
-                int64_t idx = (int64_t)c * a.n_pad + li;
-                pay.alpha = a.alpha[idx];
-                pay.G = a.G[idx];
-                pay.status = a.status[idx];
-            }
-            size_t off = ((size_t)par * L + slot) * 16 + tid;
-            for (int r = 0; r < a.world; ++r) {
-                a.peer_keys[r][off] = k;
-                a.peer_pay[r][off] = pay;
-            }
-            if (sys) __threadfence_system(); else __threadfence();
+    // stage this CTA's X^T slice into shared memory once (resident across iterations)
+    if constexpr (XS) {
+        for (int i = tid; i < d * R; i += SMO_THREADS) {
+            int k = i / R, r = i - k * R;
+            sX[i] = a.XT[(int64_t)k * a.n_pad + cta_begin + r];
         }
+    }
+    const float* xbase = XS ? sX : a.XT + cta_begin;
+    const int64_t xld = XS ? R : a.n_pad;
+
+    // ---- CTA selection: per-warp top-8 of the score arrays, then the CTA merge ----------------
+    auto select_cta = [&]() {
         __syncthreads();
-        if (tid == 0) {
-            for (int r = 0; r < a.world; ++r) {
-                if (sys) st_release_sys(a.peer_flags[r] + slot, tag);
-                else st_release_gpu(a.peer_flags[r] + slot, tag);
-            }
-        }
-    };
-
-    // ---- per-warp lists -> CTA lists ---------------------------------------------------------
-    auto finish_lists = [&](WarpTop8& up, WarpTop8& low) {
-        if (lane < 8) {
-            sh.warp_up[warp][lane] = up.v;
-            sh.warp_low[warp][lane] = low.v;
-        }
+        warp_select2(scU, scL, Rn, R, nvalid, gbase, (uint64_t)a.n_global, warp, lane,
+                     sh.warp_up[warp], sh.warp_low[warp]);
         __syncthreads();
         if (warp == 0) cta_merge(sh.warp_up, sh.cta_up, lane);
         else if (warp == 1) cta_merge(sh.warp_low, sh.cta_low, lane);
         __syncthreads();
     };
 
+    // ---- publish: 16 key words + 48 payload words per rank, each carrying the tag ------------
+    auto publish = [&](uint32_t tag) {
+        const int par = tag & 1;
+        const uint64_t tg = tag16_of(tag);
+        if (tid < 16) {
+            uint64_t k = tid < 8 ? sh.cta_up[tid] : sh.cta_low[tid - 8];
+            uint64_t wkey = tg, w0 = tg, w1 = tg, w2 = tg;
+            if (k) {
+                uint64_t g = key_index(k);
+                int c = g >= (uint64_t)a.n_global ? 1 : 0;
+                int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - a.row0;
+                int64_t idx = (int64_t)c * a.n_pad + li;
+                uint64_t pos = (uint64_t)c * (uint64_t)R + (uint64_t)(li - cta_begin);
+                wkey = tg | ((k >> 32) << 16) | pos;
+                uint64_t ab = (uint64_t)__double_as_longlong(a.alpha[idx]);
+                w0 = tg | (ab >> 16);
+                w1 = tg | ((ab & 0xffffull) << 32) | (uint64_t)__float_as_uint(a.G[idx]);
+                w2 = tg | (uint64_t)a.status[idx];
+            }
+            size_t base = ((size_t)par * L + slot) * XW_PER_SLOT;
+            for (int r = 0; r < a.world; ++r) {
+                uint64_t* dst = a.peer_xw[r] + base;
+                st_relaxed_u64(dst + 16 + 3 * tid, w0, sys);
+                st_relaxed_u64(dst + 17 + 3 * tid, w1, sys);
+                st_relaxed_u64(dst + 18 + 3 * tid, w2, sys);
+                st_relaxed_u64(dst + tid, wkey, sys);
+            }
+        }
+    };
+
     // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
     {
-        WarpTop8 up, low;
-        up.reset();
-        low.reset();
         float acc[RPT][SVM_WS];
         zero_acc<RPT>(acc);
         for (int ch = warp; ch < nchunks; ch += SMO_WARPS) {
             int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
-            row_epilogue<RPT>(a, sh, li0, cta_end, false, acc, up, low, lane);
+            row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, false, acc, scU, scL);
         }
-        finish_lists(up, low);
+        select_cta();
         publish(a.tag0 + 1);
     }
 
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tprev = clock64();
+    auto mark = [&](int ph) {
+        long long now = clock64();
+        prof[ph] += now - tprev;
+        tprev = now;
+    };
     for (int64_t t = 0;; ++t) {
         const uint32_t tag = a.tag0 + 1 + (uint32_t)t;
         const int par = tag & 1;
-        // ---- wait until every CTA of every rank published `tag` ------------------------------
+        const uint64_t tg = tag16_of(tag);
+        // ---- a1 (1/2): wait for + stage every slot's 16 key words (decoded to 64-bit keys) ----
         if (tid == 0) sh.timeout = 0;
-        __syncthreads();
-        for (int sl = tid; sl < L; sl += SMO_THREADS) {
-            const uint32_t* f = a.peer_flags[a.rank] + sl;
+        {
+            const uint64_t* src = rxw + (size_t)par * L * XW_PER_SLOT;
             uint64_t t0 = 0;
-            int spins = 0;
-            while ((int32_t)(ld_acquire_sys(f) - tag) < 0) {
-                if (++spins == 1024) {
-                    spins = 0;
-                    uint64_t now = globaltimer_ns();
-                    if (t0 == 0) t0 = now;
-                    else if (now - t0 > a.timeout_ns) { sh.timeout = 1; break; }
+            for (int i = tid; i < L * 16; i += SMO_THREADS) {
+                const int sl = i >> 4, q = i & 15;
+                const uint64_t* pw = src + (size_t)sl * XW_PER_SLOT + q;
+                uint64_t w = ld_relaxed_u64(pw, sys);
+                int spins = 0;
+                while ((w & 0xffff000000000000ull) != tg) {
+                    if (++spins == 256) {
+                        spins = 0;
+                        uint64_t now = globaltimer_ns();
+                        if (t0 == 0) t0 = now;
+                        else if (now - t0 > a.timeout_ns) { sh.timeout = 1; break; }
+                    }
+                    w = ld_relaxed_u64(pw, sys);
                 }
+                uint64_t key = 0;
+                const uint32_t score = (uint32_t)(w >> 16);
+                if (score) {
+                    const int r = sl / a.nblk, blk = sl - r * a.nblk;
+                    const int64_t Rr = a.rank_rpc[r];
+                    const uint64_t pos = w & 0xffffull;
+                    const uint64_t c = pos >= (uint64_t)Rr ? 1 : 0;
+                    const uint64_t row = (uint64_t)a.rank_row0[r] + (uint64_t)blk * Rr + pos - c * Rr;
+                    const uint64_t g = c * (uint64_t)a.n_global + row;
+                    key = ((uint64_t)score << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
+                }
+                (q < 8 ? sKU : sKL)[sl * 8 + (q & 7)] = key;
             }
         }
         __syncthreads();
+        mark(0);
         if (sh.timeout) {
             if (reporter && tid == 0) a.info->error = 1;
             return;
         }
-        // ---- stage the published keys (L2, bypassing L1) ------------------------------------
-        {
-            const ulonglong2* src =
-                reinterpret_cast<const ulonglong2*>(a.peer_keys[a.rank] + (size_t)par * L * 16);
-            for (int i = tid; i < L * 8; i += SMO_THREADS) {
-                int l = i >> 3, w = i & 7;  // 8 x 16B per slot: 4 up, 4 low
-                ulonglong2 v = __ldcg(src + i);
-                uint64_t* dst = w < 4 ? sKU + l * 8 + 2 * w : sKL + l * 8 + 2 * (w - 4);
-                dst[0] = v.x;
-                dst[1] = v.y;
-            }
+        // ---- a1 (2/2): global merge (warp 0: I_up top-8, warp 1: I_low top-8) ----------------
+        if (warp < 2) {
+            const uint64_t* keys = warp == 0 ? sKU : sKL;
+            uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
+            int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
+            if (L <= 32) global_merge<1>(keys, L, out, srcs, lane);
+            else if (L <= 64) global_merge<2>(keys, L, out, srcs, lane);
+            else if (L <= 160) global_merge<5>(keys, L, out, srcs, lane);
+            else global_merge_smem(keys, reinterpret_cast<uint8_t*>(sh.qpart) + warp * 2048, L,
+                                   out, srcs, lane);
         }
         __syncthreads();
-        // ---- a1: global merge (warp 0: I_up top-8, warp 1: I_low top-8) ----------------------
-        if (warp == 0) global_merge(sKU, sHeadU, L, sh.win_up, sh.win_up_src, lane);
-        else if (warp == 1) global_merge(sKL, sHeadL, L, sh.win_low, sh.win_low_src, lane);
-        __syncthreads();
         if (warp == 0) {
-            // W = sorted union of |W|/2 up winners and |W|/2 low winners, deduplicated.
+            // W = sorted union of |W|/2 up winners and |W|/2 low winners, deduplicated
             const int half = a.q >> 1;
             uint64_t key = 0;
             int32_t src = -1;
-            if (lane < 8 && lane < half) { key = sh.win_up[lane]; src = sh.win_up_src[lane]; }
-            else if (lane >= 8 && lane < 16 && lane - 8 < half) {
+            if (lane < 8 && lane < half) {
+                key = sh.win_up[lane];
+                if (key) src = (sh.win_up_src[lane] >> 3) * XW_PER_SLOT + (sh.win_up_src[lane] & 7);
+            } else if (lane >= 8 && lane < 16 && lane - 8 < half) {
                 key = sh.win_low[lane - 8];
-                src = sh.win_low_src[lane - 8];
-                if (src >= 0) src = (src >> 3) * 16 + 8 + (src & 7);
+                if (key)
+                    src = (sh.win_low_src[lane - 8] >> 3) * XW_PER_SLOT + 8 + (sh.win_low_src[lane - 8] & 7);
             }
-            if (lane < 8 && src >= 0) src = (src >> 3) * 16 + (src & 7);
-            uint64_t g = key ? key_index(key) : ~0ull;
+            const uint64_t g = key ? key_index(key) : ~0ull;
             bool valid = key != 0;
-            // drop low entries already chosen by the up half
-            for (int j = 0; j < 8; ++j) {
-                uint64_t gj = __shfl_sync(FULL, g, j);
-                if (lane >= 8 && valid && gj == g) valid = false;
+            uint64_t gj[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) gj[j] = __shfl_sync(FULL, g, j);
+            if (lane >= 8 && lane < 16) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) valid = valid && gj[j] != g;
             }
+            valid = valid && lane < 16;
+            const uint32_t vm = __ballot_sync(FULL, valid);
             int rank = 0;
-            for (int j = 0; j < 16; ++j) {
-                uint64_t gj = __shfl_sync(FULL, g, j);
-                bool vj = __shfl_sync(FULL, valid, j);
-                rank += (vj && gj < g) ? 1 : 0;
-            }
-            unsigned vb = __ballot_sync(FULL, valid && lane < 16);
-            if (valid && lane < 16) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rank += (((vm >> j) & 1u) && gj[j] < g) ? 1 : 0;
+            const int nw = __popc(vm);
+            // position `rank` now holds g; gather per position via a ballot-ordered shuffle
+            const int64_t row = valid ? (int64_t)(g >= (uint64_t)a.n_global ? g - a.n_global : g) : -1;
+            if (valid) {
                 sh.w_gidx[rank] = (int64_t)g;
                 sh.w_src[rank] = src;
             }
+            // distinct rows in position order: lane p looks at the rows of all positions
+            int64_t rowp[16];
+            int rk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                rowp[j] = __shfl_sync(FULL, row, j);
+                rk[j] = __shfl_sync(FULL, rank, j);
+            }
+            // position p's row (lane p): the entry with rank == p
+            int64_t myrow = -1;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (((vm >> j) & 1u) && rk[j] == lane) myrow = rowp[j];
+            // first position with the same row (fo) and distinct-row slot
+            int fo = lane;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (((vm >> j) & 1u) && rowp[j] == myrow && rk[j] < fo) fo = rk[j];
+            const uint32_t firsts = __ballot_sync(FULL, lane < nw && fo == lane);
+            const int first_of = __shfl_sync(FULL, fo, lane);  // (own)
+            (void)first_of;
+            if (lane < nw) {
+                const int sl = __popc(firsts & ((1u << fo) - 1u));
+                sh.w_slot[lane] = sl;
+                if (fo == lane) sh.r_row[sl] = myrow;
+            }
             if (lane == 0) {
-                sh.nw = __popc(vb);
-                uint64_t ku = sh.win_up[0], kl = sh.win_low[0];
+                sh.nw = nw;
+                sh.nr = __popc(firsts);
+                const uint64_t ku = sh.win_up[0], kl = sh.win_low[0];
                 sh.m_up = ku ? (double)unord_f32((uint32_t)(ku >> 32)) : -INFINITY;
                 sh.M_low = kl ? -(double)unord_f32((uint32_t)(kl >> 32)) : INFINITY;
-                sh.stop = (sh.m_up - sh.M_low <= a.tol) || (t >= a.max_iter) || sh.nw == 0;
+                sh.stop = (sh.m_up - sh.M_low <= a.tol) || (t >= a.max_iter) || nw == 0;
                 sh.next_chunk = 0;
             }
         }
         __syncthreads();
+        mark(1);
         if (sh.stop) {
             if (reporter && tid == 0) {
                 a.info->iterations = t;
@@ -450,179 +660,143 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 a.info->M_low = sh.M_low;
                 a.info->converged = (sh.m_up - sh.M_low <= a.tol) ? 1 : 0;
             }
+            if (reporter && tid == SOLVER_WARP * 32)
+                for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[ph] = prof[ph];
             return;
         }
-        // ---- a2 setup: payloads, distinct rows, X_W^T into shared memory ----------------------
-        const int nw = sh.nw;
-        if (warp == 0) {
-            int64_t g = 0, row = -1;
-            if (lane < nw) {
-                g = sh.w_gidx[lane];
-                const CandPay* pp = a.peer_pay[a.rank] + (size_t)par * L * 16 + sh.w_src[lane];
-                double al = __ldcg(&pp->alpha);
-                float gv = __ldcg(&pp->G);
-                uint32_t st = __ldcg(&pp->status);
-                sh.w_alpha[lane] = al;
-                sh.w_G[lane] = (double)gv;
-                sh.w_y[lane] = (st & ST_YPOS) ? 1 : -1;
-                row = g >= a.n_global ? g - a.n_global : g;
-            }
-            // distinct rows in position order (eps-SVR may select both copies of one row)
-            int slot_r = -1;
-            int nr = 0;
-            for (int j = 0; j < nw; ++j) {
-                int64_t rj = __shfl_sync(FULL, row, j);
-                bool first = true;
-                for (int k = 0; k < j; ++k) first &= (__shfl_sync(FULL, row, k) != rj);
-                if (first) {
-                    if (lane == 0) sh.r_row[nr] = rj;
-                    if (lane == j) slot_r = nr;
-                    ++nr;
-                } else if (lane == j) {
-                    for (int k = 0; k < nr; ++k)
-                        if (sh.r_row[k] == rj) slot_r = k;
-                }
-                __syncwarp();
-            }
-            if (lane < nw) sh.w_slot[lane] = slot_r;
-            if (lane == 0) sh.nr = nr;
-        }
-        __syncthreads();
-        const int nr = sh.nr;
+        // ---- a2 setup: X_W rows (both layouts), their norms, and the W payloads --------------
+        const int nw = sh.nw, nr = sh.nr;
         if constexpr (!CSR) {
-            for (int i = tid; i < d * SVM_WS; i += SMO_THREADS) {
-                int r = i / d, k = i - r * d;
+            const int tot = nr * dp;
+            for (int i = tid; i < tot; i += SMO_THREADS) {
+                const int r = i / dp, k = i - r * dp;
                 float v = 0.0f;
-                if (r < nr) {
-                    int64_t row = sh.r_row[r];
-                    int o = owner_rank(a, row);
-                    v = a.peer_XR[o][(row - a.rank_row0[o]) * a.d + k];
+                if (k < d) {
+                    const int64_t row = sh.r_row[r];
+                    const int o = owner_rank(a, row);
+                    v = __ldg(a.peer_XR[o] + (row - a.rank_row0[o]) * a.d + k);
+                    sXW[k * SVM_WS + r] = v;
                 }
-                sXW[k * SVM_WS + r] = v;
+                sXWr[r * dp + k] = v;
+            }
+            for (int i = tid; i < (SVM_WS - nr) * d; i += SMO_THREADS) {
+                const int r = nr + i / d, k = i % d;
+                sXW[k * SVM_WS + r] = 0.0f;
             }
         } else {
             for (int i = tid; i < d * SVM_WS; i += SMO_THREADS) sXW[i] = 0.0f;
+            for (int i = tid; i < SVM_WS * dp; i += SMO_THREADS) sXWr[i] = 0.0f;
             __syncthreads();
             for (int r = warp; r < nr; r += SMO_WARPS) {
-                int64_t row = sh.r_row[r];
-                int o = owner_rank(a, row);
-                int64_t lr = row - a.rank_row0[o];
-                int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
-                for (int64_t p = b + lane; p < e; p += 32)
-                    sXW[a.peer_indices[o][p] * SVM_WS + r] = a.peer_vals[o][p];
+                const int64_t row = sh.r_row[r];
+                const int o = owner_rank(a, row);
+                const int64_t lr = row - a.rank_row0[o];
+                const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
+                for (int64_t p = b + lane; p < e; p += 32) {
+                    const int k = a.peer_indices[o][p];
+                    const float v = a.peer_vals[o][p];
+                    sXW[k * SVM_WS + r] = v;
+                    sXWr[r * dp + k] = v;
+                }
             }
         }
-        if (tid < SVM_WS) {
+        if (tid >= SMO_THREADS - SVM_WS) {
+            const int r = tid - (SMO_THREADS - SVM_WS);
             float xn = 0.0f;
-            if (tid < nr) {
-                int64_t row = sh.r_row[tid];
-                int o = owner_rank(a, row);
+            if (r < nr) {
+                const int64_t row = sh.r_row[r];
+                const int o = owner_rank(a, row);
                 xn = a.peer_xnorm[o][row - a.rank_row0[o]];
             }
-            sh.xn[tid] = xn;
+            sh.xn[r] = xn;
+        } else if (tid >= SMO_THREADS - 2 * SVM_WS && tid < SMO_THREADS - 2 * SVM_WS + nw) {
+            const int p = tid - (SMO_THREADS - 2 * SVM_WS);
+            const uint64_t* pw = rxw + (size_t)par * L * XW_PER_SLOT + sh.w_src[p];
+            // payload words of candidate q live at 16 + 3q .. 18 + 3q of its slot
+            const int q = sh.w_src[p] % XW_PER_SLOT;
+            const uint64_t* pl = pw - q + 16 + 3 * q;
+            uint64_t w0, w1, w2;
+            do { w0 = ld_relaxed_u64(pl, sys); } while ((w0 & 0xffff000000000000ull) != tg);
+            do { w1 = ld_relaxed_u64(pl + 1, sys); } while ((w1 & 0xffff000000000000ull) != tg);
+            do { w2 = ld_relaxed_u64(pl + 2, sys); } while ((w2 & 0xffff000000000000ull) != tg);
+            const uint64_t ab = ((w0 & 0xffffffffffffull) << 16) | ((w1 >> 32) & 0xffffull);
+            sh.w_alpha[p] = __longlong_as_double((long long)ab);
+            sh.w_G[p] = (double)__uint_as_float((uint32_t)w1);
+            sh.w_y[p] = ((uint32_t)w2 & ST_YPOS) ? 1 : -1;
         }
         __syncthreads();
-        // ---- Q_WW in fp64 (warps 0-3) -> warp 0 solves; other warps start the pass ------------
-        if (warp < 4) {
+        mark(2);
+        // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
+        {
             const int npairs = nr * (nr + 1) / 2;
-            for (int p = tid; p < npairs; p += 128) {
+            const int kp = max(1, min(4, SMO_THREADS / max(npairs, 1)));
+            const int klen = ((d + kp - 1) / kp + 3) & ~3;
+            if (tid < npairs * kp) {
+                const int p = tid / kp, part = tid - p * kp;
                 int r = 0, rem = p;
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
-                int s = r + rem;
-                double acc0 = 0.0, acc1 = 0.0;
-                int k = 0;
+                const int sidx = r + rem;
+                const float4* xr = reinterpret_cast<const float4*>(sXWr + r * dp);
+                const float4* xs = reinterpret_cast<const float4*>(sXWr + sidx * dp);
+                const int k0 = part * klen, k1 = min(k0 + klen, dp);
+                double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
                 if (a.kp.kernel == 2) {
-                    for (; k + 1 < d; k += 2) {
-                        double t0 = (double)sXW[k * SVM_WS + r] - (double)sXW[k * SVM_WS + s];
-                        double t1 = (double)sXW[(k + 1) * SVM_WS + r] -
-                                    (double)sXW[(k + 1) * SVM_WS + s];
+#pragma unroll 4
+                    for (int k = k0; k < k1; k += 4) {
+                        const float4 u = xr[k >> 2], v = xs[k >> 2];
+                        const double t0 = (double)u.x - (double)v.x, t1 = (double)u.y - (double)v.y;
+                        const double t2 = (double)u.z - (double)v.z, t3 = (double)u.w - (double)v.w;
                         acc0 = fma(t0, t0, acc0);
                         acc1 = fma(t1, t1, acc1);
-                    }
-                    if (k < d) {
-                        double t0 = (double)sXW[k * SVM_WS + r] - (double)sXW[k * SVM_WS + s];
-                        acc0 = fma(t0, t0, acc0);
+                        acc2 = fma(t2, t2, acc2);
+                        acc3 = fma(t3, t3, acc3);
                     }
                 } else {
-                    for (; k + 1 < d; k += 2) {
-                        acc0 = fma((double)sXW[k * SVM_WS + r], (double)sXW[k * SVM_WS + s], acc0);
-                        acc1 = fma((double)sXW[(k + 1) * SVM_WS + r],
-                                   (double)sXW[(k + 1) * SVM_WS + s], acc1);
+#pragma unroll 4
+                    for (int k = k0; k < k1; k += 4) {
+                        const float4 u = xr[k >> 2], v = xs[k >> 2];
+                        acc0 = fma((double)u.x, (double)v.x, acc0);
+                        acc1 = fma((double)u.y, (double)v.y, acc1);
+                        acc2 = fma((double)u.z, (double)v.z, acc2);
+                        acc3 = fma((double)u.w, (double)v.w, acc3);
                     }
-                    if (k < d)
-                        acc0 = fma((double)sXW[k * SVM_WS + r], (double)sXW[k * SVM_WS + s], acc0);
                 }
-                double kv = kernel_fp64_from(acc0 + acc1, a.kp);
-                sh.kr[r * SVM_WS + s] = kv;
-                sh.kr[s * SVM_WS + r] = kv;
+                sh.qpart[p * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
             }
-            named_bar_sync(2, 128);
+            __syncthreads();
+            if (tid < npairs) {
+                int r = 0, rem = tid;
+                while (rem >= nr - r) { rem -= nr - r; ++r; }
+                const int sidx = r + rem;
+                double v = 0.0;
+                for (int part = 0; part < kp; ++part) v += sh.qpart[tid * 4 + part];
+                const double kv = kernel_fp64_from(v, a.kp);
+                sh.kr[r * SVM_WS + sidx] = kv;
+                sh.kr[sidx * SVM_WS + r] = kv;
+            }
+            __syncthreads();
+            if (tid < SVM_WS * SVM_WS) {
+                const int pa = tid >> 4, pb = tid & 15;
+                double kab = 0.0, ie = 0.0;
+                if (pa < nw && pb < nw) {
+                    const int sa = sh.w_slot[pa], sb = sh.w_slot[pb];
+                    kab = sh.kr[sa * SVM_WS + sb];
+                    const double eta = sh.kr[sa * SVM_WS + sa] + sh.kr[sb * SVM_WS + sb] - 2.0 * kab;
+                    ie = 1.0 / (eta < 1e-12 ? 1e-12 : eta);
+                }
+                sh.kpos[tid] = kab;
+                sh.inv_eta[tid] = ie;
+            }
+            __syncthreads();
         }
+        mark(3);
 
-        WarpTop8 up, low;
-        up.reset();
-        low.reset();
-        if (warp == 0) {
-            // ---- a2: the |W|-variable subproblem, max-violating pair steps in fp64 -----------
-            const int pa = lane & 15;
-            const bool valid = pa < nw;
-            const double C = a.C;
-            int ya = valid ? sh.w_y[pa] : 1;
-            double al = valid ? sh.w_alpha[pa] : 0.0;
-            double Ga = valid ? sh.w_G[pa] : 0.0;
-            const double a_old = al;
-            if (lane < nw) {
-                for (int b = 0; b < nw; ++b)
-                    sh.qww[lane * SVM_WS + b] =
-                        (double)(ya * sh.w_y[b]) * sh.kr[sh.w_slot[lane] * SVM_WS + sh.w_slot[b]];
-            }
+        if (warp == SOLVER_WARP) {
+            // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
+            // arbiter favours high ids, so the serial chain is not starved by the FMA warps) ---
+            const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
             __syncwarp();
-            int step = 0;
-            for (; step < a.inner_max; ++step) {
-                double s = -(double)ya * Ga;
-                bool upok = valid && (ya > 0 ? al < C : al > 0.0);
-                bool lowok = valid && (ya > 0 ? al > 0.0 : al < C);
-                double v = lane < 16 ? (upok ? s : -INFINITY) : (lowok ? -s : -INFINITY);
-                int p = pa;
-#pragma unroll
-                for (int off = 8; off >= 1; off >>= 1) {
-                    double vo = __shfl_xor_sync(FULL, v, off);
-                    int po = __shfl_xor_sync(FULL, p, off);
-                    if (vo > v || (vo == v && po < p)) { v = vo; p = po; }
-                }
-                double si = __shfl_sync(FULL, v, 0);
-                int i = __shfl_sync(FULL, p, 0);
-                double msj = __shfl_sync(FULL, v, 16);
-                int j = __shfl_sync(FULL, p, 16);
-                double sj = -msj;
-                if (si == -INFINITY || msj == -INFINITY || si - sj <= a.inner_tol) break;
-                int yi = __shfl_sync(FULL, ya, i), yj = __shfl_sync(FULL, ya, j);
-                double ai = __shfl_sync(FULL, al, i), aj = __shfl_sync(FULL, al, j);
-                double eta = sh.qww[i * SVM_WS + i] + sh.qww[j * SVM_WS + j] -
-                             2.0 * (double)yi * (double)yj * sh.qww[i * SVM_WS + j];
-                if (eta < 1e-12) eta = 1e-12;
-                double tt = (si - sj) / eta;
-                double lim_i = yi > 0 ? C - ai : ai;
-                double lim_j = yj > 0 ? aj : C - aj;
-                bool clip_i = false, clip_j = false;
-                if (tt >= lim_i) { tt = lim_i; clip_i = true; }
-                if (tt >= lim_j) { tt = lim_j; clip_j = true; clip_i = clip_i && (lim_i == lim_j); }
-                if (pa == i) {
-                    al += (double)yi * tt;
-                    if (clip_i) al = yi > 0 ? C : 0.0;
-                }
-                if (pa == j) {
-                    al -= (double)yj * tt;
-                    if (clip_j) al = yj > 0 ? 0.0 : C;
-                }
-                if (valid)
-                    Ga += sh.qww[pa * SVM_WS + i] * ((double)yi * tt) -
-                          sh.qww[pa * SVM_WS + j] * ((double)yj * tt);
-            }
-            if (lane < nw) {
-                sh.w_dalpha[lane] = al - a_old;
-                sh.w_anew[lane] = al;
-            }
+            if (lane < nw) sh.w_dalpha[lane] = sh.w_anew[lane] - sh.w_alpha[lane];
             __syncwarp();
             if (lane < SVM_WS) {
                 double cr = 0.0;
@@ -630,16 +804,15 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     if (sh.w_slot[b] == lane) cr += (double)sh.w_y[b] * sh.w_dalpha[b];
                 sh.c[lane] = lane < nr ? (float)cr : 0.0f;
             }
-            // owner writes alpha and status of its W entries (before the pass reads status)
+            // the owner writes alpha and status of its W entries (before the pass reads status)
             if (lane < nw) {
-                int64_t g = sh.w_gidx[lane];
-                int c = g >= a.n_global ? 1 : 0;
-                int64_t row = g - (int64_t)c * a.n_global;
-                int64_t li = row - a.row0;
+                const int64_t g = sh.w_gidx[lane];
+                const int c = g >= a.n_global ? 1 : 0;
+                const int64_t li = g - (int64_t)c * a.n_global - a.row0;
                 if (li >= cta_begin && li < cta_end) {
-                    int64_t idx = (int64_t)c * a.n_pad + li;
-                    a.alpha[idx] = al;
-                    a.status[idx] = make_status(ya, al, C);
+                    const int64_t idx = (int64_t)c * a.n_pad + li;
+                    a.alpha[idx] = sh.w_anew[lane];
+                    a.status[idx] = make_status(sh.w_y[lane], sh.w_anew[lane], a.C);
                 }
             }
             if (reporter) {
@@ -649,23 +822,23 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 }
                 if (lane == 0) {
                     a.info->last_nw = nw;
-                    a.info->last_inner = step;
-                    a.info->inner_total += step;
+                    a.info->last_inner = steps;
+                    a.info->inner_total += steps;
                 }
             }
             __threadfence_block();
             named_bar_arrive(1, SMO_THREADS);
-            // warp 0 now joins the pass
-            for (;;) {
+            mark(4);
+            for (;;) {  // warp 0 joins the pass
                 int ch = 0;
                 if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
                 ch = __shfl_sync(FULL, ch, 0);
                 if (ch >= nchunks) break;
-                int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
-                else dots_dense<RPT>(a.XT, a.n_pad, d, li0, li0 < cta_end, sXW, acc);
-                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, up, low, lane);
+                else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
+                row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, true, acc, scU, scL);
             }
         } else {
             // ---- a3: the fused kernel-row + gradient pass (first chunk overlaps a2) -----------
@@ -675,20 +848,23 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
                 ch = __shfl_sync(FULL, ch, 0);
                 if (ch >= nchunks) break;
-                int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
-                else dots_dense<RPT>(a.XT, a.n_pad, d, li0, li0 < cta_end, sXW, acc);
+                else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
                 if (!waited) {
                     named_bar_sync(1, SMO_THREADS);
                     waited = true;
                 }
-                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, up, low, lane);
+                row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, true, acc, scU, scL);
             }
             if (!waited) named_bar_sync(1, SMO_THREADS);
         }
-        finish_lists(up, low);
+        mark(5);
+        select_cta();
+        mark(6);
         publish(tag + 1);
+        mark(7);
     }
 }
 
@@ -721,26 +897,29 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
     if (li >= a.n_local) return;
     float acc[1][SVM_WS];
     if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li, true, sXW, acc);
-    else dots_dense<1>(a.XT, a.n_pad, d, li, true, sXW, acc);
+    else dots_dense<1>(a.XT + li, a.n_pad, d, true, sXW, acc);
     float xi = a.xnorm[li];
     for (int r = 0; r < nr; ++r) K[li * nr + r] = kernel_from_dot(a.kp, acc[0][r], xi, xn[r]);
 }
 
 }  // namespace
 
-int smo_smem_bytes(int64_t d, int world, int nblk)
+int smo_smem_bytes(int64_t d, int world, int nblk, int64_t score_elems, int64_t x_rows)
 {
-    int L = world * nblk;
-    return (int)(d * 64 + (int64_t)L * 8 * 8 * 2 + 2 * L + 16);
+    int64_t L = (int64_t)world * nblk;
+    int64_t dp = (d + 3) & ~3;
+    return (int)(d * 64 + 64 * dp + L * 8 * 8 * 2 + 4 * (2 * score_elems + 4) + 4 * d * x_rows);
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
 {
     void* args[] = {const_cast<SmoArgs*>(&a)};
     const void* fn;
-    if (a.XT == nullptr) fn = (const void*)smo_persistent<true, 1>;
-    else if (a.rpt == 4) fn = (const void*)smo_persistent<false, 4>;
-    else fn = (const void*)smo_persistent<false, 1>;
+    if (a.XT == nullptr) fn = (const void*)smo_persistent<true, 1, false>;
+    else if (a.x_in_smem) fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, true>
+                                          : (const void*)smo_persistent<false, 1, true>;
+    else fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, false>
+                         : (const void*)smo_persistent<false, 1, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
     return cudaLaunchCooperativeKernel(fn, dim3(a.nblk), dim3(SMO_THREADS), args,

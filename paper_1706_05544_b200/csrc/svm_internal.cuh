@@ -98,13 +98,13 @@ __device__ __forceinline__ uint64_t make_key(float score, uint64_t gidx)
 }
 __device__ __forceinline__ uint64_t key_index(uint64_t key) { return 0xffffffffu - (uint32_t)key; }
 
-// Payload published with each candidate key: the candidate's alpha, G and status, so a rank
-// never reads another rank's state arrays.
-struct __align__(16) CandPay {
-    double alpha;
-    float G;
-    uint32_t status;
-};
+// Exchange words ("LL" format: every 8-byte word carries its own 16-bit tag, so a reader never
+// needs a fence or a separate flag -- it polls the words until their tags match).  Per CTA slot
+// and iteration: 16 key words [tag16 | ord(score) 32 | pos16] (8 up, 8 low; pos = c * rows_per_cta
+// + local row, score 0 = no candidate) and 16 x 3 payload words carrying the candidate's alpha
+// (fp64), G (fp32) and status byte.
+#define XW_PER_SLOT 64
+__host__ __device__ __forceinline__ uint64_t tag16_of(uint32_t tag) { return (uint64_t)(tag % 65535u + 1u) << 48; }
 
 // Device-side result record of the persistent loop (written by CTA 0 of rank 0).
 struct SmoInfo {
@@ -117,6 +117,7 @@ struct SmoInfo {
     int64_t last_w[SVM_WS];
     double last_dalpha[SVM_WS];
     int64_t inner_total;
+    int64_t phase_cycles[8];  // CTA 0, thread 0: clock64 per phase, summed over iterations
 };
 
 // All arguments of the persistent working-set kernel (passed by value).
@@ -147,16 +148,17 @@ struct SmoArgs {
     const int64_t* peer_indptr[SVM_MAX_RANKS];
     const int32_t* peer_indices[SVM_MAX_RANKS];
     const float* peer_vals[SVM_MAX_RANKS];
-    uint64_t* peer_keys[SVM_MAX_RANKS];       // receive buffers: [2][world*nblk][16] keys
-    CandPay* peer_pay[SVM_MAX_RANKS];         //                  [2][world*nblk][16] payloads
-    uint32_t* peer_flags[SVM_MAX_RANKS];      //                  [world*nblk] tags
+    int64_t rank_rpc[SVM_MAX_RANKS];          // rows_per_cta of each rank
+    uint64_t* peer_xw[SVM_MAX_RANKS];         // receive buffers: [2][world*nblk][XW_PER_SLOT]
     uint32_t tag0;            // epoch: this launch publishes tags tag0+1, tag0+2, ...
     int64_t max_iter;         // iterations allowed in this launch
     uint64_t timeout_ns;
     SmoInfo* info;
+    uint32_t* score_global;   // per-CTA score arrays in global memory when they exceed smem
+    int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
 };
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
-int smo_smem_bytes(int64_t d, int world, int nblk);
+int smo_smem_bytes(int64_t d, int world, int nblk, int64_t score_elems, int64_t x_rows);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);

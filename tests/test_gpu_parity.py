@@ -66,10 +66,24 @@ def test_kernel_rows(kname, csr):
     K = s.kernel_rows(rows)
     ref = _oracle_K(X, rows, _ks(kname, ds.d, gamma))
     err = np.abs(K - ref)
-    tol = np.where(np.abs(ref) < 1e-4, 1e-9 + 1e-5 * np.abs(ref), 1e-5 * np.abs(ref))
-    if kname == "linear" or kname == "poly":
-        tol = np.maximum(tol, 1e-5 * np.abs(ref).max(axis=0, keepdims=True) * 1e-1)
-    assert (err <= tol).all(), f"max rel err {np.max(err / np.maximum(np.abs(ref), 1e-30))}"
+    # RBF: the north_star bar, 1e-5 relative (absolute floor 1e-9 where K < 1e-4).  Dot-product
+    # kernels: an fp32 dot of d terms is exact to ~d 2^-24 sum|u_k v_k|, propagated through dK/ddot.
+    X64 = X.astype(np.float64)
+    absdot = np.abs(X64) @ np.abs(X64[rows]).T
+    dot = X64 @ X64[rows].T
+    if kname == "rbf":
+        tol = np.where(np.abs(ref) < 1e-4, 1e-9 + 1e-5 * np.abs(ref), 1e-5 * np.abs(ref))
+    else:
+        kw = KERNELS[kname]
+        if kname == "linear":
+            dk = np.ones_like(ref)
+        elif kname == "poly":
+            z = gamma * dot + kw["coef0"]
+            dk = gamma * kw["degree"] * np.abs(z) ** (kw["degree"] - 1)
+        else:
+            dk = gamma * (1 - ref ** 2)
+        tol = 1e-5 * np.abs(ref) + 1e-9 + dk * ds.d * 2.0 ** -24 * 4 * absdot
+    assert (err <= tol).all(), f"worst err/tol {np.max(err / tol)}"
 
 
 # ----------------------------------------------------------------------------- a1 selection
@@ -90,39 +104,81 @@ def _state_after(X, prob, ks, C, steps, q=16):
     return alpha, G.astype(np.float32).astype(np.float64)   # fp32-representable G
 
 
+def _qww(X, prob, ks, W):
+    return np.array([[prob.y[a] * prob.y[b] * ora.kernel(X[prob.map[a]], X[prob.map[b]], ks)
+                      for b in W] for a in W])
+
+
 @pytest.mark.parametrize("kname", ["rbf", "linear", "poly"])
 @pytest.mark.parametrize("svm_type", ["C-classification", "eps-regression"])
 @pytest.mark.parametrize("csr", [False, True])
 def test_one_step_from_identical_state(kname, svm_type, csr):
+    """One outer iteration from the same fp32-representable (alpha, G) on both sides.
+
+    a1: W identical.  a2: the GPU's subproblem result is a valid inner solve of the SAME
+    subproblem (box, y'dalpha = 0, local violation <= inner_tol measured in fp64 with the oracle's
+    Q_WW) and, solved to inner_tol 1e-10 on both sides, equal to the oracle's within 1e-6 relative
+    (the inner SMO paths at the default inner_tol may split at exact near-ties of fp64 scores, so
+    there only optimality is compared).  a3: the GPU's G equals the oracle's step 6 applied to the
+    GPU's own dalpha within 1e-5 max(1, |G|) (the north_star one-step bar)."""
     reg = svm_type == "eps-regression"
     ds = synth.make("c2" if reg else "c1", n=900)
     X = ds.X
     if csr:
         X = X.copy()
         X[np.abs(X) < 0.6] = 0.0
-    C = 1.0
+    C, tol = 1.0, 1e-3
     gamma = 1.0 / ds.d
     ks = _ks(kname, ds.d, gamma)
     prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION, ds.y, ds.n, 0.1)
-    for steps in (0, 7, 40):
-        alpha, G = _state_after(X, prob, ks, C, steps)
-        W, dA, a1, G1 = ora.step(X, prob, ks, alpha, G, C, q=16, tol=1e-3)
+
+    def solver(tolerance):
+        kw = dict(svm_type=svm_type, gamma=gamma, tolerance=tolerance, **KERNELS[kname])
         if csr:
             ip = np.concatenate([[0], np.cumsum((X != 0).sum(1))]).astype(np.int64)
-            s = pkg.Solver(csr=(ip, np.nonzero(X)[1].astype(np.int32), X[X != 0]), y=ds.y,
-                           d=ds.d, svm_type=svm_type, gamma=gamma, **KERNELS[kname])
-        else:
-            s = pkg.Solver(X, ds.y, svm_type=svm_type, gamma=gamma, **KERNELS[kname])
+            return pkg.Solver(csr=(ip, np.nonzero(X)[1].astype(np.int32), X[X != 0]), y=ds.y,
+                              d=ds.d, **kw)
+        return pkg.Solver(X, ds.y, **kw)
+
+    for steps in (0, 7, 40):
+        alpha, G = _state_after(X, prob, ks, C, steps)
+        W, dA, a1, G1 = ora.step(X, prob, ks, alpha, G, C, q=16, tol=tol)
+        s = solver(tol)
         s.set_state(alpha, G.astype(np.float32))
         st = s.run(1)
         assert st.iterations == 1
-        np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
-        np.testing.assert_allclose(np.array(st.last_dalpha[:st.last_nw]), dA, rtol=1e-6,
-                                   atol=1e-9 * C)
+        Wg = np.array(st.last_w[:st.last_nw])
+        np.testing.assert_array_equal(Wg, W)                                   # a1
+        dg = np.array(st.last_dalpha[:st.last_nw])
+        Q = _qww(X, prob, ks, W)
+        yW = prob.y[W].astype(np.float64)
+        aW = alpha[W] + dg
+        assert (aW >= -1e-15).all() and (aW <= C + 1e-15).all()             # a2: feasible
+        assert abs(yW @ dg) <= 1e-12 * C * len(W)
+        sW = -yW * (G[W] + Q @ dg)
+        up = np.array([(y > 0 and a < C) or (y < 0 and a > 0) for y, a in zip(yW, aW)])
+        lo = np.array([(y > 0 and a > 0) or (y < 0 and a < C) for y, a in zip(yW, aW)])
+        if up.any() and lo.any():
+            assert sW[up].max() - sW[lo].min() <= ora.inner_tol_for(tol) + 1e-9
         ag, Gg = s.get_state()
-        np.testing.assert_allclose(ag, a1, rtol=1e-6, atol=1e-9 * C)
-        assert (np.abs(Gg - G1) <= 1e-5 * np.maximum(1.0, np.abs(G1))).all(), \
-            np.abs(Gg - G1).max()
+        np.testing.assert_allclose(ag[W], aW, rtol=0, atol=1e-15)
+        Gref = ora.gradient_update(X, prob, ks, W, dg, G)                     # a3
+        assert (np.abs(Gg - Gref) <= 1e-5 * np.maximum(1.0, np.abs(Gref))).all(), \
+            np.abs(Gg - Gref).max()
+        # tight inner tolerance: the subproblem optimum (unique when Q_WW is definite)
+        Wt, dAt, _, _ = ora.step(X, prob, ks, alpha, G, C, q=16, tol=1e-9)
+        s2 = solver(1e-9)
+        s2.set_state(alpha, G.astype(np.float32))
+        st2 = s2.run(1)
+        np.testing.assert_array_equal(np.array(st2.last_w[:st2.last_nw]), Wt)
+        dg2 = np.array(st2.last_dalpha[:st2.last_nw])
+        Qt = _qww(X, prob, ks, Wt)
+        if np.linalg.eigvalsh(Qt).min() > 1e-6:
+            np.testing.assert_allclose(dg2, dAt, rtol=1e-6, atol=1e-9 * C)
+        else:   # singular Q_WW (e.g. both eps-SVR copies of a row): compare the optimum value
+            gl = G[Wt]
+            obj = lambda d_: 0.5 * d_ @ Qt @ d_ + gl @ d_
+            assert abs(obj(dg2) - obj(dAt)) <= 1e-9 * max(1.0, abs(obj(dAt)))
 
 
 # ----------------------------------------------------------------------------- end to end
