@@ -148,6 +148,10 @@ void svm_free_model(svm_model* model);
 /* Thread-local message of the last failing call on this thread ("" if none). */
 const char* svm_last_error(void);
 
+/* Number of CUDA kernels this library has launched since it was loaded (diagnostics: the bench
+ * reports the launches inside its timed region from the difference of two calls). */
+int64_t svm_launch_count(void);
+
 /* ---- solver-state API: one binary problem, stepwise (parity tests and drivers) -------------
  * A solver owns the device state of one Eq. 2 instance built from (X, y, params) exactly as
  * svm_train builds it (labels: binary only -- exactly two classes, mapped as svm_train maps them).

@@ -8,6 +8,7 @@
 
 The package holds no arithmetic of the method in Python; ``synth`` only draws seeded inputs.
 """
-from .binding import (Model, Solver, SvmError, lib, params, train, train_csr)  # noqa: F401
+from .binding import (Model, Solver, SvmError, launch_count, lib, params, train,  # noqa: F401
+                      train_csr)
 
-__all__ = ["Model", "Solver", "SvmError", "lib", "params", "train", "train_csr"]
+__all__ = ["Model", "Solver", "SvmError", "launch_count", "lib", "params", "train", "train_csr"]

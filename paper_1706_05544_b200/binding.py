@@ -78,6 +78,7 @@ SIGNATURES = {
     "svm_model_get_sv": (ctypes.c_int, [_P, _P, _P]),
     "svm_free_model": (None, [_P]),
     "svm_last_error": (ctypes.c_char_p, []),
+    "svm_launch_count": (ctypes.c_int64, []),
     "svm_solver_create": (ctypes.c_int, [_P, _P, _i64, _i64, ctypes.POINTER(svm_params),
                                          ctypes.POINTER(_P)]),
     "svm_solver_create_csr": (ctypes.c_int, [_P, _P, _P, _P, _i64, _i64,
@@ -114,6 +115,11 @@ def lib() -> ctypes.CDLL:
             fn.restype = res
             fn.argtypes = args
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libsvmb200.so so far (svm_launch_count)."""
+    return int(lib().svm_launch_count())
 
 
 def _check(rc: int):
@@ -296,3 +302,32 @@ class Solver:
         _check(lib().svm_solver_kernel_rows(self._h, rows.ctypes.data_as(_P), len(rows),
                                             K.ctypes.data_as(_P)))
         return K
+
+
+def train_sharded(X_local, row0: int, y_global, rank: int, world: int, all_gather_bytes,
+                  layout=ROW_MAJOR, **kw) -> Model:
+    """svm_shard_*: row-sharded training over `world` GPUs (one process per GPU).
+
+    X_local: this rank's rows [row0, row0 + n_local) (numpy host or torch CUDA tensor);
+    y_global: labels / targets of all rows; all_gather_bytes(b: bytes) -> list[bytes] must
+    return every rank's handle blob in rank order (e.g. torch.distributed.all_gather_object).
+    Every rank returns the identical model."""
+    n_local, d = (int(X_local.shape[0]), int(X_local.shape[1])) if layout == ROW_MAJOR else \
+        (int(X_local.shape[1]), int(X_local.shape[0]))
+    n_global = int(len(y_global))
+    p = params(d, layout=layout, **kw)
+    x, yy = _Arr(X_local, np.float32), _Arr(y_global, np.float32)
+    sh = ctypes.c_void_p()
+    _check(lib().svm_shard_create(x.p, n_local, d, int(row0), yy.p, n_global, int(rank),
+                                  int(world), ctypes.byref(p), ctypes.byref(sh)))
+    try:
+        blob = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
+        _check(lib().svm_shard_handle(sh, blob))
+        blobs = all_gather_bytes(blob.raw)
+        allh = ctypes.create_string_buffer(b"".join(blobs), SHARD_HANDLE_BYTES * world)
+        _check(lib().svm_shard_connect(sh, allh))
+        h = ctypes.c_void_p()
+        _check(lib().svm_shard_train(sh, ctypes.byref(h)))
+        return Model(h.value)
+    finally:
+        lib().svm_shard_free(sh)

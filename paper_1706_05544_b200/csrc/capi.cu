@@ -17,6 +17,12 @@
 #include <string>
 #include <vector>
 
+// ================================================================ launch counter
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+void svm_note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+extern "C" int64_t svm_launch_count(void) { return (int64_t)g_launches.load(); }
+
 // ================================================================ errors
 static thread_local std::string g_err;
 
@@ -48,6 +54,9 @@ static int fail(int code, const char* fmt, ...)
     } while (0)
 
 // ================================================================ device memory (RAII)
+// Device buffers come from the stream-ordered pool (cudaMallocAsync on the legacy stream): no
+// device-wide synchronisation on free, and repeated trainings reuse pooled memory.  Every entry
+// point synchronises its stream before returning, so pool reuse never races user work.
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -57,7 +66,7 @@ struct DBuf {
     ~DBuf() { release(); }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         bytes = 0;
     }
@@ -65,11 +74,11 @@ struct DBuf {
     {
         release();
         if (b == 0) b = 16;
-        cudaError_t e = cudaMalloc(&p, b);
+        cudaError_t e = cudaMallocAsync(&p, b, 0);
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
-            return fail(SVM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", b, cudaGetErrorString(e));
+            return fail(SVM_ENOMEM, "cudaMallocAsync(%zu bytes) failed: %s", b, cudaGetErrorString(e));
         }
         bytes = b;
         return SVM_OK;
@@ -110,6 +119,20 @@ static int to_host(std::vector<T>& dst, const T* src, int64_t n, cudaStream_t st
         CK(cudaStreamSynchronize(st));
     }
     return SVM_OK;
+}
+
+static void pool_setup()
+{
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
 }
 
 static int sm_count()
@@ -195,6 +218,7 @@ struct Data {
 
 static int pick_nblk(int64_t n)
 {
+    pool_setup();
     const char* env = getenv("SVMB200_NBLK");
     int sms = sm_count();
     if (env && atoi(env) > 0) return std::min(atoi(env), sms);

@@ -392,12 +392,14 @@ cudaError_t lay_check_finite(const float* p, int64_t n, int* d_bad, cudaStream_t
 {
     if (n <= 0) return cudaSuccess;
     unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
+    svm_note_launches(1);
     k_check_finite<<<g, 256, 0, st>>>(p, n, d_bad);
     return cudaGetLastError();
 }
 cudaError_t lay_check_csr(const int64_t* indptr, const int32_t* idx, int64_t n, int64_t d,
                           int64_t nnz, int* d_bad, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_check_csr<<<nblocks(n, 256), 256, 0, st>>>(indptr, idx, n, d, nnz, d_bad);
     return cudaGetLastError();
 }
@@ -405,6 +407,7 @@ cudaError_t lay_rowmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, 
                                cudaStream_t st)
 {
     dim3 grid(nblocks(n_pad, 32), nblocks(d, 32));
+    svm_note_launches(1);
     k_rowmajor_to_XT<<<grid, dim3(32, 8), 0, st>>>(X, n, d, XT, n_pad);
     return cudaGetLastError();
 }
@@ -412,6 +415,7 @@ cudaError_t lay_colmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, 
                                cudaStream_t st)
 {
     unsigned g = (unsigned)std::min<int64_t>((d * n_pad + 255) / 256, 65535);
+    svm_note_launches(1);
     k_colmajor_to_XT<<<g, 256, 0, st>>>(X, n, d, XT, n_pad);
     return cudaGetLastError();
 }
@@ -419,42 +423,49 @@ cudaError_t lay_XT_to_rowmajor(const float* XT, int64_t n, int64_t d, int64_t n_
                                cudaStream_t st)
 {
     dim3 grid(nblocks(d, 32), nblocks(n, 32));
+    svm_note_launches(1);
     k_XT_to_rowmajor<<<grid, dim3(32, 8), 0, st>>>(XT, n, d, n_pad, X);
     return cudaGetLastError();
 }
 cudaError_t lay_norms_XT(const float* XT, int64_t n, int64_t d, int64_t n_pad, float* xnorm,
                          cudaStream_t st)
 {
+    svm_note_launches(1);
     k_norms_XT<<<nblocks(n_pad, 256), 256, 0, st>>>(XT, n, d, n_pad, xnorm);
     return cudaGetLastError();
 }
 cudaError_t lay_norms_csr(const int64_t* indptr, const float* vals, int64_t n, int64_t n_pad,
                           float* xnorm, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_norms_csr<<<nblocks(n_pad, 256), 256, 0, st>>>(indptr, vals, n, n_pad, xnorm);
     return cudaGetLastError();
 }
 cudaError_t lay_init_state(const float* yv, int64_t n, int64_t n_pad, int ncopy, double eps,
                            double C, double* alpha, float* G, uint8_t* status, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_init_state<<<nblocks(n_pad, 256), 256, 0, st>>>(yv, n, n_pad, ncopy, eps, C, alpha, G, status);
     return cudaGetLastError();
 }
 cudaError_t lay_status_from_alpha(const double* alpha, int64_t n, int64_t n_pad, int ncopy,
                                   double C, uint8_t* status, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_status_from_alpha<<<nblocks(n, 256), 256, 0, st>>>(alpha, n, n_pad, ncopy, C, status);
     return cudaGetLastError();
 }
 cudaError_t lay_pack_state(const double* alpha, const float* G, int64_t n, int64_t n_pad,
                            int ncopy, double* a_out, float* g_out, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_pack_state<<<nblocks(n * ncopy, 256), 256, 0, st>>>(alpha, G, n, n_pad, ncopy, a_out, g_out);
     return cudaGetLastError();
 }
 cudaError_t lay_unpack_state(const double* a_in, const float* g_in, int64_t n, int64_t n_pad,
                              int ncopy, double* alpha, float* G, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_unpack_state<<<nblocks(n * ncopy, 256), 256, 0, st>>>(a_in, g_in, n, n_pad, ncopy, alpha, G);
     return cudaGetLastError();
 }
@@ -462,14 +473,17 @@ cudaError_t lay_reduce_state(const double* alpha, const float* G, const uint8_t*
                              const float* yv, int64_t n, int64_t n_pad, int ncopy, double eps,
                              double C, double* d_out5, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_init_reduce<<<1, 1, 0, st>>>(d_out5);
     unsigned g = (unsigned)std::min<int64_t>((n * ncopy + 255) / 256, 1184);
+    svm_note_launches(1);
     k_reduce_state<<<g, 256, 0, st>>>(alpha, G, status, yv, n, n_pad, ncopy, eps, C, d_out5);
     return cudaGetLastError();
 }
 cudaError_t lay_coef(const double* alpha, const uint8_t* status, int64_t n, int64_t n_pad,
                      int ncopy, double C, double* coef, uint8_t* svflag, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_coef<<<nblocks(n, 256), 256, 0, st>>>(alpha, status, n, n_pad, ncopy, C, coef, 0, svflag);
     return cudaGetLastError();
 }
@@ -477,12 +491,14 @@ cudaError_t lay_count_flags(const uint8_t* flag, int64_t n, int32_t* cnt, int* n
                             cudaStream_t st)
 {
     *nblk_out = (int)nblocks(n, 1024);
+    svm_note_launches(1);
     k_count_flags<<<*nblk_out, 1024, 0, st>>>(flag, n, cnt);
     return cudaGetLastError();
 }
 cudaError_t lay_scatter_flags(const uint8_t* flag, int64_t n, const int64_t* offs, int64_t* out,
                               cudaStream_t st)
 {
+    svm_note_launches(1);
     k_scatter_flags<<<nblocks(n, 1024), 1024, 0, st>>>(flag, n, offs, out);
     return cudaGetLastError();
 }
@@ -490,6 +506,7 @@ cudaError_t lay_gather_sv(const float* XT, int64_t n_pad, int64_t d, const float
                           const int64_t* sv_idx, int64_t nsv, int64_t nsv_pad, float* SVT,
                           float* svnorm, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_gather_sv<<<nblocks(nsv_pad, 256), 256, 0, st>>>(XT, n_pad, d, xnorm, sv_idx, nsv, nsv_pad,
                                                         SVT, svnorm);
     return cudaGetLastError();
@@ -499,12 +516,14 @@ cudaError_t lay_csr_to_XT(const int64_t* indptr, const int32_t* idx, const float
                           int64_t ld, cudaStream_t st)
 {
     if (nrows <= 0) return cudaSuccess;
+    svm_note_launches(1);
     k_csr_to_XT<<<nblocks(nrows, 256), 256, 0, st>>>(indptr, idx, vals, rows, nrows, row_base, XT, ld);
     return cudaGetLastError();
 }
 cudaError_t lay_gather_coef(const double* coef_rows, const int64_t* sv_idx, int64_t nsv,
                             int64_t nsv_pad, double* coef_sv, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_gather_coef<<<nblocks(nsv_pad, 256), 256, 0, st>>>(coef_rows, sv_idx, nsv, nsv_pad, coef_sv);
     return cudaGetLastError();
 }
@@ -512,6 +531,7 @@ cudaError_t lay_gather_coef(const double* coef_rows, const int64_t* sv_idx, int6
 cudaError_t lay_xchg(const double* vals, int K, int rank, int world, const XchgPeers& P,
                      uint32_t tag, double* out, uint64_t timeout_ns, int* err, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_xchg<<<1, 64, 0, st>>>(vals, K, rank, world, P, tag, out, timeout_ns, err);
     return cudaGetLastError();
 }
@@ -519,6 +539,7 @@ cudaError_t lay_gather_global_sv(const SvPeers& P, int64_t nsv, int64_t nsv_pad,
                                  int nprob, float* SVT, float* svn, double* coef, int64_t* grow,
                                  cudaStream_t st)
 {
+    svm_note_launches(1);
     k_gather_global_sv<<<nblocks(nsv_pad, 128), 128, 0, st>>>(P, nsv, nsv_pad, d, nprob, SVT, svn,
                                                               coef, grow);
     return cudaGetLastError();

@@ -209,10 +209,10 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     double* part = F;
     if (splits > 1) {
         if (need > g_fpart_bytes) {
-            if (g_fpart) cudaFree(g_fpart);
+            if (g_fpart) cudaFreeAsync(g_fpart, st);
             g_fpart = nullptr;
             g_fpart_bytes = 0;
-            cudaError_t e = cudaMalloc(&g_fpart, need);
+            cudaError_t e = cudaMallocAsync(&g_fpart, need, st);
             if (e != cudaSuccess) return e;
             g_fpart_bytes = need;
         }
@@ -222,6 +222,7 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     const int smem1 = decision_smem(1), smem16 = decision_smem(16);
     cudaFuncSetAttribute(k_decision<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
     cudaFuncSetAttribute(k_decision<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
+    svm_note_launches(1);
     if (n_out == 1)
         k_decision<1><<<grid, PT, smem1, st>>>(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv_pad, d, coef,
                                            n_out, kp, tps, part);
@@ -231,6 +232,7 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || splits == 1) return e;
     int64_t count = nq * n_out;
+    svm_note_launches(1);
     k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, splits, count, F);
     return cudaGetLastError();
 }
@@ -238,6 +240,7 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
 cudaError_t pred_refresh_G(const double* F, const float* yv, const uint8_t* status, int64_t n,
                            int64_t n_pad, int ncopy, double eps, float* G, cudaStream_t st)
 {
+    svm_note_launches(1);
     k_refresh_G<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(F, yv, status, n, n_pad, ncopy, eps, G);
     return cudaGetLastError();
 }
@@ -247,6 +250,7 @@ cudaError_t pred_finalize(const double* F, int64_t nq, int n_out, const double* 
                           cudaStream_t st)
 {
     if (nq <= 0) return cudaSuccess;
+    svm_note_launches(1);
     k_finalize<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(F, nq, n_out, b, mode, labels,
                                                             first_label, decision, out);
     return cudaGetLastError();

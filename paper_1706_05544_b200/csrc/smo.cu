@@ -922,6 +922,7 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
                          : (const void*)smo_persistent<false, 1, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
+    svm_note_launches(1);
     return cudaLaunchCooperativeKernel(fn, dim3(a.nblk), dim3(SMO_THREADS), args,
                                        (size_t)smem_bytes, st);
 }
@@ -933,9 +934,11 @@ cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, fl
     int grid = (int)((a.n_local + 255) / 256);
     if (a.XT == nullptr) {
         cudaFuncSetAttribute(kernel_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        svm_note_launches(1);
         kernel_rows_kernel<true><<<grid, 256, smem, st>>>(a, rows, nr, K);
     } else {
         cudaFuncSetAttribute(kernel_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        svm_note_launches(1);
         kernel_rows_kernel<false><<<grid, 256, smem, st>>>(a, rows, nr, K);
     }
     return cudaGetLastError();

@@ -158,6 +158,9 @@ struct SmoArgs {
     int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
 };
 
+// Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
+void svm_note_launches(int k);
+
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t score_elems, int64_t x_rows);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,

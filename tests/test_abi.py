@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "svmb200.h")
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:int|void|const char\*)\s+(svm_\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:int|void|const char\*|int64_t)\s+(svm_\w+)\s*\(", src, flags=re.M)
     assert len(names) >= 20
     return names
 

@@ -289,3 +289,40 @@ def test_errors_and_edge_cases():
     with pytest.raises(pkg.SvmError) as e:
         m.predict(np.zeros((3, 7), np.float32))
     assert e.value.code == -1
+
+
+def test_partition_invariance_bit_identical():
+    """Virtual shards (SURVEY 8(e) invariant): the per-row arithmetic does not depend on which CTA
+    owns a row and the candidate merge is exact, so alpha, G and the iteration count are
+    bit-identical for any number of row blocks (1-rank analogue of the P-rank invariant)."""
+    import os
+    ds = synth.make("c2", n=4000)
+    res = []
+    for nblk in ("3", "16", "40"):
+        os.environ["SVMB200_NBLK"] = nblk
+        try:
+            s = pkg.Solver(ds.X, ds.y, svm_type="eps-regression", gamma=1.0 / ds.d)
+            st = s.run(400)
+            res.append((st.iterations, *s.get_state()))
+        finally:
+            del os.environ["SVMB200_NBLK"]
+    for it, a, g in res[1:]:
+        assert it == res[0][0]
+        np.testing.assert_array_equal(a, res[0][1])
+        np.testing.assert_array_equal(g, res[0][2])
+
+
+def test_csr_equals_dense_end_to_end():
+    """The CSR path (a3 CSR variant) trains the same model as the dense path on the same data."""
+    ds = synth.make("c5", n=3000, d=60)
+    Xd = ds.dense()
+    md = pkg.train(Xd, ds.y, gamma=1.0 / 60)
+    mc = pkg.train_csr(ds.indptr, ds.indices, ds.data, ds.y, 60, gamma=1.0 / 60)
+    assert abs(md.info.dual_objective - mc.info.dual_objective) <= 1e-5 * abs(md.info.dual_objective)
+    Xh = synth.make("c5", n=500, d=60, heldout=True)
+    od, dd = md.predict(Xh.dense(), decision=True)
+    oc, dc = mc.predict_csr(Xh.indptr, Xh.indices, Xh.data, 60, decision=True)
+    assert np.abs(dd - dc).max() <= 1e-3
+    om = ora.train(Xd, ds.y, gamma=1.0 / 60)
+    assert abs(mc.info.dual_objective - om.results[0]["dual"]) <= 1e-4 * abs(om.results[0]["dual"])
+    assert np.abs(dc[:, 0] - om.decision_function(Xh.dense())[:, 0]).max() <= 1e-3
