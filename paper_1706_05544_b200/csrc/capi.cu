@@ -405,8 +405,12 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.n_global = D.n;
     a.rows_per_cta = D.rows_per_cta;
     a.ncopy = P.ncopy;
-    a.rpt = (!D.csr && D.rows_per_cta >= 4 * 32 * SMO_WARPS) ? 4 : 1;
-    if (const char* e = getenv("SVMB200_RPT")) a.rpt = (atoi(e) == 4 && !D.csr) ? 4 : 1;
+    // rows per thread: enough chunks to keep ~12 warps busy, fewer LDS per FMA when rows allow
+    a.rpt = D.csr ? 1 : (D.rows_per_cta >= 12 * 128 ? 4 : (D.rows_per_cta >= 6 * 64 ? 2 : 1));
+    if (const char* e = getenv("SVMB200_RPT")) {
+        int v = atoi(e);
+        a.rpt = D.csr ? 1 : (v == 4 ? 4 : (v == 2 ? 2 : 1));
+    }
     a.alpha = P.alpha.as<double>();
     a.G = P.G.as<float>();
     a.status = P.status.as<uint8_t>();
@@ -429,6 +433,8 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.rank_rpc[0] = D.rows_per_cta;
     a.peer_xw[0] = E.xw.as<uint64_t>();
     a.timeout_ns = 30ull * 1000000000ull;
+    a.overlap = 1;
+    if (const char* e = getenv("SVMB200_OVERLAP")) a.overlap = atoi(e) != 0;
     a.info = E.info.as<SmoInfo>();
     if (sc && sc->world > 1) {
         a.rank = sc->rank;
@@ -458,26 +464,20 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     a.tag0 = E.epoch;
     a.max_iter = max_iter;
     CK(cudaMemsetAsync(E.info.p, 0, sizeof(SmoInfo), st));
-    const int64_t score_elems = D.rows_per_cta * P.ncopy;
+    const int64_t pos_elems = D.rows_per_cta * P.ncopy;
     const int64_t smem_cap = 200 * 1024;
-    DBuf score_glb;
-    int smem = smo_smem_bytes(D.d, a.world, D.nblk, score_elems, D.csr ? 0 : D.rows_per_cta);
+    int smem = smo_smem_bytes(D.d, a.world, D.nblk, D.csr ? 0 : D.rows_per_cta);
     if (!D.csr && smem <= smem_cap && !getenv("SVMB200_NO_XSMEM")) {
         a.x_in_smem = 1;  // this CTA's X slice stays resident in shared memory
     } else {
-        smem = smo_smem_bytes(D.d, a.world, D.nblk, score_elems, 0);
-        if (smem > smem_cap) {  // score arrays do not fit next to X_W: keep them in global (L2)
-            TRY(score_glb.alloc(sizeof(uint32_t) * 2 * score_elems * D.nblk));
-            a.score_global = score_glb.as<uint32_t>();
-            smem = smo_smem_bytes(D.d, a.world, D.nblk, 0, 0);
-        }
+        smem = smo_smem_bytes(D.d, a.world, D.nblk, 0);
     }
     if (smem > 220 * 1024)
         return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d lists)", smem,
                     (long long)D.d, a.world * D.nblk);
-    if (score_elems > 65535)
+    if (pos_elems > 65535)
         return fail(SVM_EINVAL, "%lld dual variables per CTA exceed the 16-bit candidate position",
-                    (long long)score_elems);
+                    (long long)pos_elems);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -525,6 +525,11 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
                 tot / (double)std::max<int64_t>(1, info.iterations),
                 info.inner_total / (double)std::max<int64_t>(1, info.iterations));
         (void)clk;
+        const double it = (double)std::max<int64_t>(1, info.iterations);
+        fprintf(stderr, "[svmb200]   worker warp 0 (cycles/iter): dots %.0f wait-c %.0f epilogue %.0f "
+                "merge %.0f tail %.0f finish %.0f\n", info.phase_cycles[8] / it, info.phase_cycles[9] / it,
+                info.phase_cycles[10] / it, info.phase_cycles[11] / it, info.phase_cycles[12] / it,
+                info.phase_cycles[13] / it);
     }
     if (info_out) *info_out = info;
     return SVM_OK;

@@ -103,6 +103,9 @@ __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64
         if constexpr (RPT == 4) {
             float4 v = *reinterpret_cast<const float4*>(p);
             x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+        } else if constexpr (RPT == 2) {
+            float2 v = *reinterpret_cast<const float2*>(p);
+            x[0] = v.x; x[1] = v.y;
         } else {
             x[0] = *p;
         }
@@ -169,95 +172,92 @@ struct SmoShared {
 };
 
 // Per-row epilogue shared by the scan (do_update = false) and the pass: kernel values from the
-// dot products, G update, and the row's up / low scores (0 = not a candidate) into the CTA's
-// score arrays at position c * rows_per_cta + (li - cta_begin).
+// dot products, G update, and each dual's 64-bit up / low candidate keys (score << 32 | ~index;
+// 0 = not a candidate) kept in registers: ku[2 j + c], kl[2 j + c] for row j, copy c.
 template <int RPT>
 __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& sh, int64_t li0,
-                                             int64_t cta_begin, int64_t cta_end, bool do_update,
-                                             const float (&acc)[RPT][SVM_WS], uint32_t* scU,
-                                             uint32_t* scL)
+                                             int64_t cta_end, bool do_update,
+                                             const float (&acc)[RPT][SVM_WS],
+                                             uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT])
 {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-        int64_t li = li0 + j;
+        const int64_t li = li0 + j;
+        ku[2 * j] = ku[2 * j + 1] = kl[2 * j] = kl[2 * j + 1] = 0ull;
         if (li >= cta_end) continue;
         float S = 0.0f;
         if (do_update) {
-            float xn = __ldg(a.xnorm + li);
+            const float xn = __ldg(a.xnorm + li);
 #pragma unroll
             for (int r = 0; r < SVM_WS; ++r)
                 S = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]), S);
         }
-        for (int c = 0; c < a.ncopy; ++c) {
-            int64_t idx = (int64_t)c * a.n_pad + li;
-            uint32_t st = a.status[idx];
-            float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (c >= a.ncopy) break;
+            const int64_t idx = (int64_t)c * a.n_pad + li;
+            const uint32_t st = a.status[idx];
+            const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
             float g = a.G[idx];
             if (do_update) {
                 g = fmaf(yv, S, g);
                 a.G[idx] = g;
             }
-            float sc = -yv * g;
-            int pos = c * (int)a.rows_per_cta + (int)(li - cta_begin);
-            scU[pos] = st_in_up(st) ? ord_f32(sc) : 0u;
-            scL[pos] = st_in_low(st) ? ord_f32(-sc) : 0u;
+            const float sc = -yv * g;
+            const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(a.row0 + li);
+            const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)gi);
+            if (st_in_up(st)) ku[2 * j + c] = ((uint64_t)ord_f32(sc) << 32) | lo;
+            if (st_in_low(st)) kl[2 * j + c] = ((uint64_t)ord_f32(-sc) << 32) | lo;
         }
     }
 }
 
-// Top-8 keys of one warp's segment of a CTA score array by extraction rounds (warp max; only the
-// winning lane rescans its positions below the extracted key).  Both arrays at once for ILP.
-__device__ __forceinline__ void warp_select2(const uint32_t* scU, const uint32_t* scL, int Rn,
-                                             int R, int nvalid, uint64_t gbase, uint64_t n_global,
-                                             int w, int lane, uint64_t* outU, uint64_t* outL)
+// Merge one chunk's candidate keys (NK per lane) into the warp's running top-8 lists (lane l < 8
+// holds the l-th best; 0 = empty), up and low together: extraction rounds of a 64-bit warp max,
+// the winning lane dropping the extracted key.  A chunk with no key above the current 8th is
+// skipped.  Keys are unique, so the result is exact.
+template <int NK>
+__device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[NK], uint64_t& wlu,
+                                            uint64_t& wll, int lane)
 {
-    const int seg = (Rn + SMO_WARPS - 1) / SMO_WARPS;
-    const int p0 = w * seg, p1 = min(p0 + seg, Rn);
-    auto key_at = [&](const uint32_t* sc, int p) -> uint64_t {
-        int c = p >= R ? 1 : 0;
-        int li = p - c * R;
-        uint32_t v = sc[p];
-        if (li >= nvalid || v == 0u) return 0ull;
-        uint64_t g = (uint64_t)c * n_global + gbase + (uint64_t)li;
-        return ((uint64_t)v << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
+    const uint64_t thu = __shfl_sync(FULL, wlu, 7), thl = __shfl_sync(FULL, wll, 7);
+    bool au = false, alo = false;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        au |= ku[k] > thu;
+        alo |= kl[k] > thl;
+    }
+    const bool doU = __any_sync(FULL, au), doL = __any_sync(FULL, alo);
+    if (!doU && !doL) return;
+    uint64_t ou = lane < 8 ? wlu : 0ull, ol = lane < 8 ? wll : 0ull;
+    auto lmax = [&](const uint64_t (&k)[NK], uint64_t own) {
+        uint64_t m = own;
+#pragma unroll
+        for (int q = 0; q < NK; ++q) m = k[q] > m ? k[q] : m;
+        return m;
     };
-    uint64_t lu = 0, ll = 0;
-    for (int p = p0 + lane; p < p1; p += 32) {
-        uint64_t ku = key_at(scU, p), kl = key_at(scL, p);
-        lu = ku > lu ? ku : lu;
-        ll = kl > ll ? kl : ll;
-    }
-    bool doneU = false, doneL = false;
+    uint64_t lu = doU ? lmax(ku, ou) : 0ull, ll = doL ? lmax(kl, ol) : 0ull;
+    uint64_t nu = 0ull, nl = 0ull;
     for (int r = 0; r < 8; ++r) {
-        uint64_t bu = warp_max_u64(lu);
-        uint64_t bl = warp_max_u64(ll);
-        if (lane == 0) {
-            outU[r] = doneU ? 0 : bu;
-            outL[r] = doneL ? 0 : bl;
+        const uint64_t bu = warp_max_u64(lu);
+        const uint64_t bl = warp_max_u64(ll);
+        if (lane == r) { nu = bu; nl = bl; }
+        if (bu == 0ull && bl == 0ull) break;
+        if (bu != 0ull && lu == bu) {
+            if (ou == bu) ou = 0ull;
+#pragma unroll
+            for (int q = 0; q < NK; ++q) ku[q] = ku[q] == bu ? 0ull : ku[q];
+            lu = lmax(ku, ou);
         }
-        doneU = doneU || bu == 0;
-        doneL = doneL || bl == 0;
-        if (doneU && doneL) {
-            if (lane > r && lane < 8) { outU[lane] = 0; outL[lane] = 0; }
-            break;
-        }
-        const bool wu = !doneU && lu == bu, wl = !doneL && ll == bl;
-        if (wu || wl) {
-            uint64_t nu = 0, nl = 0;
-            for (int p = p0 + lane; p < p1; p += 32) {
-                if (wu) {
-                    uint64_t k = key_at(scU, p);
-                    if (k < bu && k > nu) nu = k;
-                }
-                if (wl) {
-                    uint64_t k = key_at(scL, p);
-                    if (k < bl && k > nl) nl = k;
-                }
-            }
-            if (wu) lu = nu;
-            if (wl) ll = nl;
+        if (bl != 0ull && ll == bl) {
+            if (ol == bl) ol = 0ull;
+#pragma unroll
+            for (int q = 0; q < NK; ++q) kl[q] = kl[q] == bl ? 0ull : kl[q];
+            ll = lmax(kl, ol);
         }
     }
+    if (doU) wlu = nu;
+    if (doL) wll = nl;
 }
 
 // Merge SMO_WARPS sorted warp lists into the CTA top-8 (one warp).
@@ -282,7 +282,7 @@ __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* 
 }
 
 // Global merge of L sorted 8-lists (staged in shared memory as keys[L][8]) into the top-8 (one
-// warp).  Lane l owns lists l, l + 32, ... (at most MAXK); heads, current and next keys live in
+// warp).  Lane l owns lists l, l + 32, ... (at most MAXK); current and next keys live in
 // registers.  src receives list * 8 + position of each winner.
 template <int MAXK>
 __device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64_t* out,
@@ -362,12 +362,6 @@ __device__ __forceinline__ int owner_rank(const SmoArgs& a, int64_t row)
     return r;
 }
 
-// The |W|-variable subproblem (a2) on warp 0, lane a = position a: max-violating-pair steps in
-// fp64 (SURVEY 8(c) step 5; P:53 "optimized based on the local gradient").  argmax_{I_up} s and
-// argmin_{I_low} s are exact 64-bit REDUX reductions of order-preserving keys, ties to the lowest
-// lane = lowest position.  The step in score form (s_a = -y_a G_a):
-//   t = (s_i - s_j) / eta_ij clipped to the box;  s_a += t (K_aj - K_ai)
-// which is the oracle's G_W += Q_Wi y_i t - Q_Wj y_j t, since Q_ab = y_a y_b K_ab.
 __device__ __forceinline__ double lds_f64(uint32_t addr)
 {
     double v;
@@ -375,6 +369,12 @@ __device__ __forceinline__ double lds_f64(uint32_t addr)
     return v;
 }
 
+// The |W|-variable subproblem (a2) on one warp, lane a = position a: max-violating-pair steps in
+// fp64 (SURVEY 8(c) step 5; P:53 "optimized based on the local gradient").  argmax_{I_up} s and
+// argmin_{I_low} s are exact 64-bit REDUX reductions of order-preserving keys, ties to the lowest
+// lane = lowest position.  The step in score form (s_a = -y_a G_a):
+//   t = (s_i - s_j) / eta_ij clipped to the box;  s_a += t (K_aj - K_ai)
+// which is the oracle's G_W += Q_Wi y_i t - Q_Wj y_j t, since Q_ab = y_a y_b K_ab.
 __device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C, double inner_tol,
                                                 int inner_max, int lane)
 {
@@ -433,17 +433,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int d = (int)a.d;
     const int dp = (d + 3) & ~3;
     const int R = (int)a.rows_per_cta;
-    const int Rn = R * a.ncopy;
-    float* sXW = reinterpret_cast<float*>(dyn_smem);                        // [d][16]
-    float* sXWr = sXW + (size_t)d * SVM_WS;                                  // [16][dp]
-    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWr + (size_t)SVM_WS * dp);  // [L][8]
+    float* sXW = reinterpret_cast<float*>(dyn_smem);                        // [d][16] fp32
+    double* sXWd = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);      // [16][dp] fp64
+    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWd + (size_t)SVM_WS * dp); // [L][8]
     uint64_t* sKL = sKU + (size_t)L * 8;                                     // [L][8]
-    uint32_t* scU = a.score_global ? a.score_global + (size_t)blockIdx.x * 2 * Rn
-                                   : reinterpret_cast<uint32_t*>(sKL + (size_t)L * 8);
-    uint32_t* scL = scU + Rn;
-    float* sX = reinterpret_cast<float*>(
-        a.score_global ? reinterpret_cast<unsigned char*>(sKL + (size_t)L * 8)
-                       : reinterpret_cast<unsigned char*>(scL + ((Rn + 3) & ~3)));  // [d][R]
+    float* sX = reinterpret_cast<float*>(sKL + (size_t)L * 8);               // [d][R] (XS)
 
     const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
     const int64_t cta_end = min(cta_begin + a.rows_per_cta, a.n_local);
@@ -453,24 +447,23 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int slot = a.rank * a.nblk + blockIdx.x;
     const bool sys = a.world > 1;
     const bool reporter = blockIdx.x == 0;  // CTA 0 of every rank reports for its rank
-    const uint64_t gbase = (uint64_t)(a.row0 + cta_begin);
     uint64_t* rxw = a.peer_xw[a.rank];       // this rank's receive buffer
 
     // stage this CTA's X^T slice into shared memory once (resident across iterations)
     if constexpr (XS) {
-        for (int i = tid; i < d * R; i += SMO_THREADS) {
-            int k = i / R, r = i - k * R;
-            sX[i] = a.XT[(int64_t)k * a.n_pad + cta_begin + r];
-        }
+        for (int k = warp; k < d; k += SMO_WARPS)
+            for (int r = lane; r < R; r += 32)
+                sX[(size_t)k * R + r] = a.XT[(int64_t)k * a.n_pad + cta_begin + r];
     }
     const float* xbase = XS ? sX : a.XT + cta_begin;
     const int64_t xld = XS ? R : a.n_pad;
 
-    // ---- CTA selection: per-warp top-8 of the score arrays, then the CTA merge ----------------
-    auto select_cta = [&]() {
-        __syncthreads();
-        warp_select2(scU, scL, Rn, R, nvalid, gbase, (uint64_t)a.n_global, warp, lane,
-                     sh.warp_up[warp], sh.warp_low[warp]);
+    // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
+    auto finish_lists = [&](uint64_t wlu, uint64_t wll) {
+        if (lane < 8) {
+            sh.warp_up[warp][lane] = wlu;
+            sh.warp_low[warp][lane] = wll;
+        }
         __syncthreads();
         if (warp == 0) cta_merge(sh.warp_up, sh.cta_up, lane);
         else if (warp == 1) cta_merge(sh.warp_low, sh.cta_low, lane);
@@ -482,21 +475,21 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         const int par = tag & 1;
         const uint64_t tg = tag16_of(tag);
         if (tid < 16) {
-            uint64_t k = tid < 8 ? sh.cta_up[tid] : sh.cta_low[tid - 8];
+            const uint64_t k = tid < 8 ? sh.cta_up[tid] : sh.cta_low[tid - 8];
             uint64_t wkey = tg, w0 = tg, w1 = tg, w2 = tg;
             if (k) {
-                uint64_t g = key_index(k);
-                int c = g >= (uint64_t)a.n_global ? 1 : 0;
-                int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - a.row0;
-                int64_t idx = (int64_t)c * a.n_pad + li;
-                uint64_t pos = (uint64_t)c * (uint64_t)R + (uint64_t)(li - cta_begin);
+                const uint64_t g = key_index(k);
+                const int c = g >= (uint64_t)a.n_global ? 1 : 0;
+                const int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - a.row0;
+                const int64_t idx = (int64_t)c * a.n_pad + li;
+                const uint64_t pos = (uint64_t)c * (uint64_t)R + (uint64_t)(li - cta_begin);
                 wkey = tg | ((k >> 32) << 16) | pos;
-                uint64_t ab = (uint64_t)__double_as_longlong(a.alpha[idx]);
+                const uint64_t ab = (uint64_t)__double_as_longlong(a.alpha[idx]);
                 w0 = tg | (ab >> 16);
                 w1 = tg | ((ab & 0xffffull) << 32) | (uint64_t)__float_as_uint(a.G[idx]);
                 w2 = tg | (uint64_t)a.status[idx];
             }
-            size_t base = ((size_t)par * L + slot) * XW_PER_SLOT;
+            const size_t base = ((size_t)par * L + slot) * XW_PER_SLOT;
             for (int r = 0; r < a.world; ++r) {
                 uint64_t* dst = a.peer_xw[r] + base;
                 st_relaxed_u64(dst + 16 + 3 * tid, w0, sys);
@@ -509,17 +502,27 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 
     // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
     {
+        uint64_t wlu = 0, wll = 0;
         float acc[RPT][SVM_WS];
         zero_acc<RPT>(acc);
         for (int ch = warp; ch < nchunks; ch += SMO_WARPS) {
-            int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
-            row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, false, acc, scU, scL);
+            const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+            uint64_t ku[2 * RPT], kl[2 * RPT];
+            row_epilogue<RPT>(a, sh, li0, cta_end, false, acc, ku, kl);
+            merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
         }
-        select_cta();
+        finish_lists(wlu, wll);
         publish(a.tag0 + 1);
     }
 
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long wprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // worker view (warp 0)
+    long long wprev = 0;
+    auto wmark = [&](int ph) {
+        long long now = clock64();
+        if (ph >= 0) wprof[ph] += now - wprev;
+        wprev = now;
+    };
     long long tprev = clock64();
     auto mark = [&](int ph) {
         long long now = clock64();
@@ -534,33 +537,46 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         if (tid == 0) sh.timeout = 0;
         {
             const uint64_t* src = rxw + (size_t)par * L * XW_PER_SLOT;
+            constexpr int SW = 8;  // words per thread per batch: all loads in flight at once
             uint64_t t0 = 0;
-            for (int i = tid; i < L * 16; i += SMO_THREADS) {
-                const int sl = i >> 4, q = i & 15;
-                const uint64_t* pw = src + (size_t)sl * XW_PER_SLOT + q;
-                uint64_t w = ld_relaxed_u64(pw, sys);
-                int spins = 0;
-                while ((w & 0xffff000000000000ull) != tg) {
-                    if (++spins == 256) {
-                        spins = 0;
-                        uint64_t now = globaltimer_ns();
-                        if (t0 == 0) t0 = now;
-                        else if (now - t0 > a.timeout_ns) { sh.timeout = 1; break; }
+            for (int base = 0; base < L * 16; base += SMO_THREADS * SW) {
+                uint64_t w[SW];
+#pragma unroll
+                for (int u = 0; u < SW; ++u) {
+                    const int i = base + tid + u * SMO_THREADS;
+                    w[u] = i < L * 16 ? ld_relaxed_u64(src + (size_t)(i >> 4) * XW_PER_SLOT + (i & 15), sys)
+                                      : tg;
+                }
+#pragma unroll
+                for (int u = 0; u < SW; ++u) {
+                    const int i = base + tid + u * SMO_THREADS;
+                    if (i >= L * 16) continue;
+                    const int sl = i >> 4, q = i & 15;
+                    const uint64_t* pw = src + (size_t)sl * XW_PER_SLOT + q;
+                    int spins = 0;
+                    while ((w[u] & 0xffff000000000000ull) != tg) {
+                        if (++spins == 256) {
+                            spins = 0;
+                            const uint64_t now = globaltimer_ns();
+                            if (t0 == 0) t0 = now;
+                            else if (now - t0 > a.timeout_ns) { sh.timeout = 1; break; }
+                        }
+                        w[u] = ld_relaxed_u64(pw, sys);
                     }
-                    w = ld_relaxed_u64(pw, sys);
+                    uint64_t key = 0;
+                    const uint32_t score = (uint32_t)(w[u] >> 16);
+                    if (score) {
+                        int r = 0, blk = sl;
+                        if (a.world > 1) { r = sl / a.nblk; blk = sl - r * a.nblk; }
+                        const uint64_t Rr = (uint64_t)a.rank_rpc[r];
+                        const uint64_t pos = w[u] & 0xffffull;
+                        const uint64_t c = pos >= Rr ? 1 : 0;
+                        const uint64_t row = (uint64_t)a.rank_row0[r] + (uint64_t)blk * Rr + pos - c * Rr;
+                        const uint64_t g = c * (uint64_t)a.n_global + row;
+                        key = ((uint64_t)score << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
+                    }
+                    (q < 8 ? sKU : sKL)[sl * 8 + (q & 7)] = key;
                 }
-                uint64_t key = 0;
-                const uint32_t score = (uint32_t)(w >> 16);
-                if (score) {
-                    const int r = sl / a.nblk, blk = sl - r * a.nblk;
-                    const int64_t Rr = a.rank_rpc[r];
-                    const uint64_t pos = w & 0xffffull;
-                    const uint64_t c = pos >= (uint64_t)Rr ? 1 : 0;
-                    const uint64_t row = (uint64_t)a.rank_row0[r] + (uint64_t)blk * Rr + pos - c * Rr;
-                    const uint64_t g = c * (uint64_t)a.n_global + row;
-                    key = ((uint64_t)score << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
-                }
-                (q < 8 ? sKU : sKL)[sl * 8 + (q & 7)] = key;
             }
         }
         __syncthreads();
@@ -609,13 +625,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 #pragma unroll
             for (int j = 0; j < 16; ++j) rank += (((vm >> j) & 1u) && gj[j] < g) ? 1 : 0;
             const int nw = __popc(vm);
-            // position `rank` now holds g; gather per position via a ballot-ordered shuffle
             const int64_t row = valid ? (int64_t)(g >= (uint64_t)a.n_global ? g - a.n_global : g) : -1;
             if (valid) {
                 sh.w_gidx[rank] = (int64_t)g;
                 sh.w_src[rank] = src;
             }
-            // distinct rows in position order: lane p looks at the rows of all positions
+            // distinct rows in position order (eps-SVR may select both copies of one row)
             int64_t rowp[16];
             int rk[16];
 #pragma unroll
@@ -623,19 +638,15 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 rowp[j] = __shfl_sync(FULL, row, j);
                 rk[j] = __shfl_sync(FULL, rank, j);
             }
-            // position p's row (lane p): the entry with rank == p
             int64_t myrow = -1;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
                 if (((vm >> j) & 1u) && rk[j] == lane) myrow = rowp[j];
-            // first position with the same row (fo) and distinct-row slot
             int fo = lane;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
                 if (((vm >> j) & 1u) && rowp[j] == myrow && rk[j] < fo) fo = rk[j];
             const uint32_t firsts = __ballot_sync(FULL, lane < nw && fo == lane);
-            const int first_of = __shfl_sync(FULL, fo, lane);  // (own)
-            (void)first_of;
             if (lane < nw) {
                 const int sl = __popc(firsts & ((1u << fo) - 1u));
                 sh.w_slot[lane] = sl;
@@ -644,9 +655,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             if (lane == 0) {
                 sh.nw = nw;
                 sh.nr = __popc(firsts);
-                const uint64_t ku = sh.win_up[0], kl = sh.win_low[0];
-                sh.m_up = ku ? (double)unord_f32((uint32_t)(ku >> 32)) : -INFINITY;
-                sh.M_low = kl ? -(double)unord_f32((uint32_t)(kl >> 32)) : INFINITY;
+                const uint64_t ku0 = sh.win_up[0], kl0 = sh.win_low[0];
+                sh.m_up = ku0 ? (double)unord_f32((uint32_t)(ku0 >> 32)) : -INFINITY;
+                sh.M_low = kl0 ? -(double)unord_f32((uint32_t)(kl0 >> 32)) : INFINITY;
                 sh.stop = (sh.m_up - sh.M_low <= a.tol) || (t >= a.max_iter) || nw == 0;
                 sh.next_chunk = 0;
             }
@@ -662,68 +673,57 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
             if (reporter && tid == SOLVER_WARP * 32)
                 for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[ph] = prof[ph];
+            if (reporter && tid == 0)
+                for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[8 + ph] = wprof[ph];
             return;
         }
-        // ---- a2 setup: X_W rows (both layouts), their norms, and the W payloads --------------
+        // ---- a2 setup: X_W rows (fp32 [d][16] for the pass, fp64 [16][dp] for K_WW), their
+        // norms and the W payloads; one warp per row, no integer division -------------------
         const int nw = sh.nw, nr = sh.nr;
-        if constexpr (!CSR) {
-            const int tot = nr * dp;
-            for (int i = tid; i < tot; i += SMO_THREADS) {
-                const int r = i / dp, k = i - r * dp;
-                float v = 0.0f;
-                if (k < d) {
-                    const int64_t row = sh.r_row[r];
-                    const int o = owner_rank(a, row);
-                    v = __ldg(a.peer_XR[o] + (row - a.rank_row0[o]) * a.d + k);
-                    sXW[k * SVM_WS + r] = v;
-                }
-                sXWr[r * dp + k] = v;
-            }
-            for (int i = tid; i < (SVM_WS - nr) * d; i += SMO_THREADS) {
-                const int r = nr + i / d, k = i % d;
-                sXW[k * SVM_WS + r] = 0.0f;
-            }
-        } else {
-            for (int i = tid; i < d * SVM_WS; i += SMO_THREADS) sXW[i] = 0.0f;
-            for (int i = tid; i < SVM_WS * dp; i += SMO_THREADS) sXWr[i] = 0.0f;
+        for (int i = tid; i < d * SVM_WS; i += SMO_THREADS)
+            if ((i & 15) >= nr || CSR) sXW[i] = 0.0f;
+        if constexpr (CSR) {
+            for (int i = tid; i < nr * dp; i += SMO_THREADS) sXWd[i] = 0.0;
             __syncthreads();
-            for (int r = warp; r < nr; r += SMO_WARPS) {
-                const int64_t row = sh.r_row[r];
-                const int o = owner_rank(a, row);
-                const int64_t lr = row - a.rank_row0[o];
-                const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
-                for (int64_t p = b + lane; p < e; p += 32) {
-                    const int k = a.peer_indices[o][p];
-                    const float v = a.peer_vals[o][p];
-                    sXW[k * SVM_WS + r] = v;
-                    sXWr[r * dp + k] = v;
-                }
-            }
         }
-        if (tid >= SMO_THREADS - SVM_WS) {
-            const int r = tid - (SMO_THREADS - SVM_WS);
-            float xn = 0.0f;
-            if (r < nr) {
-                const int64_t row = sh.r_row[r];
-                const int o = owner_rank(a, row);
-                xn = a.peer_xnorm[o][row - a.rank_row0[o]];
-            }
-            sh.xn[r] = xn;
-        } else if (tid >= SMO_THREADS - 2 * SVM_WS && tid < SMO_THREADS - 2 * SVM_WS + nw) {
-            const int p = tid - (SMO_THREADS - 2 * SVM_WS);
-            const uint64_t* pw = rxw + (size_t)par * L * XW_PER_SLOT + sh.w_src[p];
-            // payload words of candidate q live at 16 + 3q .. 18 + 3q of its slot
+        if (warp == SMO_WARPS - 1 && lane < nw) {  // payloads of W (tagged words)
+            const int p = lane;
             const int q = sh.w_src[p] % XW_PER_SLOT;
-            const uint64_t* pl = pw - q + 16 + 3 * q;
-            uint64_t w0, w1, w2;
-            do { w0 = ld_relaxed_u64(pl, sys); } while ((w0 & 0xffff000000000000ull) != tg);
-            do { w1 = ld_relaxed_u64(pl + 1, sys); } while ((w1 & 0xffff000000000000ull) != tg);
-            do { w2 = ld_relaxed_u64(pl + 2, sys); } while ((w2 & 0xffff000000000000ull) != tg);
+            const uint64_t* pl = rxw + (size_t)par * L * XW_PER_SLOT + sh.w_src[p] - q + 16 + 3 * q;
+            uint64_t w0 = ld_relaxed_u64(pl, sys), w1 = ld_relaxed_u64(pl + 1, sys),
+                     w2 = ld_relaxed_u64(pl + 2, sys);
+            while ((w0 & 0xffff000000000000ull) != tg) w0 = ld_relaxed_u64(pl, sys);
+            while ((w1 & 0xffff000000000000ull) != tg) w1 = ld_relaxed_u64(pl + 1, sys);
+            while ((w2 & 0xffff000000000000ull) != tg) w2 = ld_relaxed_u64(pl + 2, sys);
             const uint64_t ab = ((w0 & 0xffffffffffffull) << 16) | ((w1 >> 32) & 0xffffull);
             sh.w_alpha[p] = __longlong_as_double((long long)ab);
             sh.w_G[p] = (double)__uint_as_float((uint32_t)w1);
             sh.w_y[p] = ((uint32_t)w2 & ST_YPOS) ? 1 : -1;
         }
+        if (warp < nr) {  // one warp per distinct W row (coalesced along the row)
+            const int r = warp;
+            const int64_t row = sh.r_row[r];
+            const int o = owner_rank(a, row);
+            const int64_t lr = row - a.rank_row0[o];
+            if constexpr (!CSR) {
+                const float* src = a.peer_XR[o] + lr * a.d;
+                for (int k = lane; k < dp; k += 32) {
+                    const float v = k < d ? __ldg(src + k) : 0.0f;
+                    if (k < d) sXW[k * SVM_WS + r] = v;
+                    sXWd[r * dp + k] = (double)v;
+                }
+            } else {
+                const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
+                for (int64_t p = b + lane; p < e; p += 32) {
+                    const int k = a.peer_indices[o][p];
+                    const float v = a.peer_vals[o][p];
+                    sXW[k * SVM_WS + r] = v;
+                    sXWd[r * dp + k] = (double)v;
+                }
+            }
+            if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];
+        }
+        if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
         __syncthreads();
         mark(2);
         // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
@@ -736,29 +736,33 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 int r = 0, rem = p;
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
                 const int sidx = r + rem;
-                const float4* xr = reinterpret_cast<const float4*>(sXWr + r * dp);
-                const float4* xs = reinterpret_cast<const float4*>(sXWr + sidx * dp);
-                const int k0 = part * klen, k1 = min(k0 + klen, dp);
                 double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-                if (a.kp.kernel == 2) {
+                if (sidx != r || a.kp.kernel != 2) {
+                    const double2* xr = reinterpret_cast<const double2*>(sXWd + r * dp);
+                    const double2* xs = reinterpret_cast<const double2*>(sXWd + sidx * dp);
+                    const int k0 = part * klen, k1 = min(k0 + klen, dp);
+                    if (a.kp.kernel == 2) {
 #pragma unroll 4
-                    for (int k = k0; k < k1; k += 4) {
-                        const float4 u = xr[k >> 2], v = xs[k >> 2];
-                        const double t0 = (double)u.x - (double)v.x, t1 = (double)u.y - (double)v.y;
-                        const double t2 = (double)u.z - (double)v.z, t3 = (double)u.w - (double)v.w;
-                        acc0 = fma(t0, t0, acc0);
-                        acc1 = fma(t1, t1, acc1);
-                        acc2 = fma(t2, t2, acc2);
-                        acc3 = fma(t3, t3, acc3);
-                    }
-                } else {
+                        for (int k = k0; k < k1; k += 4) {
+                            const double2 u0 = xr[k >> 1], v0 = xs[k >> 1];
+                            const double2 u1 = xr[(k >> 1) + 1], v1 = xs[(k >> 1) + 1];
+                            const double t0 = u0.x - v0.x, t1 = u0.y - v0.y;
+                            const double t2 = u1.x - v1.x, t3 = u1.y - v1.y;
+                            acc0 = fma(t0, t0, acc0);
+                            acc1 = fma(t1, t1, acc1);
+                            acc2 = fma(t2, t2, acc2);
+                            acc3 = fma(t3, t3, acc3);
+                        }
+                    } else {
 #pragma unroll 4
-                    for (int k = k0; k < k1; k += 4) {
-                        const float4 u = xr[k >> 2], v = xs[k >> 2];
-                        acc0 = fma((double)u.x, (double)v.x, acc0);
-                        acc1 = fma((double)u.y, (double)v.y, acc1);
-                        acc2 = fma((double)u.z, (double)v.z, acc2);
-                        acc3 = fma((double)u.w, (double)v.w, acc3);
+                        for (int k = k0; k < k1; k += 4) {
+                            const double2 u0 = xr[k >> 1], v0 = xs[k >> 1];
+                            const double2 u1 = xr[(k >> 1) + 1], v1 = xs[(k >> 1) + 1];
+                            acc0 = fma(u0.x, v0.x, acc0);
+                            acc1 = fma(u0.y, v0.y, acc1);
+                            acc2 = fma(u1.x, v1.x, acc2);
+                            acc3 = fma(u1.y, v1.y, acc3);
+                        }
                     }
                 }
                 sh.qpart[p * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
@@ -791,9 +795,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         }
         mark(3);
 
+        uint64_t wlu = 0, wll = 0;  // this warp's running top-8 lists
         if (warp == SOLVER_WARP) {
             // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
-            // arbiter favours high ids, so the serial chain is not starved by the FMA warps) ---
+            // arbiter favours high ids), overlapped with the other warps' dot products ----------
             const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
             __syncwarp();
             if (lane < nw) sh.w_dalpha[lane] = sh.w_anew[lane] - sh.w_alpha[lane];
@@ -829,7 +834,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             __threadfence_block();
             named_bar_arrive(1, SMO_THREADS);
             mark(4);
-            for (;;) {  // warp 0 joins the pass
+            for (;;) {  // the solver warp joins the pass
                 int ch = 0;
                 if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
                 ch = __shfl_sync(FULL, ch, 0);
@@ -838,31 +843,46 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
                 else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
-                row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, true, acc, scU, scL);
+                uint64_t ku[2 * RPT], kl[2 * RPT];
+                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, ku, kl);
+                merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
             }
         } else {
             // ---- a3: the fused kernel-row + gradient pass (first chunk overlaps a2) -----------
             bool waited = false;
+            wmark(-1);
             for (;;) {
                 int ch = 0;
                 if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
                 ch = __shfl_sync(FULL, ch, 0);
                 if (ch >= nchunks) break;
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                if (!waited && !a.overlap) {
+                    named_bar_sync(1, SMO_THREADS);
+                    waited = true;
+                }
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
                 else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
+                wmark(0);
                 if (!waited) {
                     named_bar_sync(1, SMO_THREADS);
                     waited = true;
                 }
-                row_epilogue<RPT>(a, sh, li0, cta_begin, cta_end, true, acc, scU, scL);
+                wmark(1);
+                uint64_t ku[2 * RPT], kl[2 * RPT];
+                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, ku, kl);
+                wmark(2);
+                merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
+                wmark(3);
             }
             if (!waited) named_bar_sync(1, SMO_THREADS);
+            wmark(4);
         }
         mark(5);
-        select_cta();
+        finish_lists(wlu, wll);
         mark(6);
+        wmark(5);
         publish(tag + 1);
         mark(7);
     }
@@ -904,11 +924,11 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
 
 }  // namespace
 
-int smo_smem_bytes(int64_t d, int world, int nblk, int64_t score_elems, int64_t x_rows)
+int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)
 {
     int64_t L = (int64_t)world * nblk;
     int64_t dp = (d + 3) & ~3;
-    return (int)(d * 64 + 64 * dp + L * 8 * 8 * 2 + 4 * (2 * score_elems + 4) + 4 * d * x_rows);
+    return (int)(d * 64 + 128 * dp + L * 8 * 8 * 2 + 4 * d * x_rows);
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
@@ -916,10 +936,14 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
     void* args[] = {const_cast<SmoArgs*>(&a)};
     const void* fn;
     if (a.XT == nullptr) fn = (const void*)smo_persistent<true, 1, false>;
-    else if (a.x_in_smem) fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, true>
-                                          : (const void*)smo_persistent<false, 1, true>;
-    else fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, false>
-                         : (const void*)smo_persistent<false, 1, false>;
+    else if (a.x_in_smem)
+        fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, true>
+           : a.rpt == 2 ? (const void*)smo_persistent<false, 2, true>
+                        : (const void*)smo_persistent<false, 1, true>;
+    else
+        fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, false>
+           : a.rpt == 2 ? (const void*)smo_persistent<false, 2, false>
+                        : (const void*)smo_persistent<false, 1, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
     svm_note_launches(1);

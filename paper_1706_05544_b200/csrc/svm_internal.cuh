@@ -117,7 +117,7 @@ struct SmoInfo {
     int64_t last_w[SVM_WS];
     double last_dalpha[SVM_WS];
     int64_t inner_total;
-    int64_t phase_cycles[8];  // CTA 0, thread 0: clock64 per phase, summed over iterations
+    int64_t phase_cycles[16]; // CTA 0: clock64 per phase (solver [0,8), worker warp 0 [8,16))
 };
 
 // All arguments of the persistent working-set kernel (passed by value).
@@ -131,7 +131,7 @@ struct SmoArgs {
     int64_t n_local, n_pad, d, row0, n_global;
     int64_t rows_per_cta;     // multiple of 4
     int32_t ncopy;            // 1 = SVC (m = n), 2 = eps-SVR (m = 2n, Eq. 1)
-    int32_t rpt;              // rows per thread in the dense pass: 1 or 4
+    int32_t rpt;              // rows per thread in the dense pass: 1, 2 or 4
     // per-dual state of the local rows, copy-major: dual (c, i) at c * n_pad + i
     double* alpha;
     float* G;
@@ -154,14 +154,14 @@ struct SmoArgs {
     int64_t max_iter;         // iterations allowed in this launch
     uint64_t timeout_ns;
     SmoInfo* info;
-    uint32_t* score_global;   // per-CTA score arrays in global memory when they exceed smem
     int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
+    int32_t overlap;          // 1: the pass's dot products overlap the subproblem
 };
 
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
 void svm_note_launches(int k);
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
-int smo_smem_bytes(int64_t d, int world, int nblk, int64_t score_elems, int64_t x_rows);
+int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);
