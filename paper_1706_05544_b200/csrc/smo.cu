@@ -65,6 +65,13 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t k)
     return ((uint64_t)mh << 32) | ml;
 }
 
+__device__ __forceinline__ float exp2f_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Order-preserving map of fp64 to u64 (exact, so argmax over keys == argmax over values).
 __device__ __forceinline__ uint64_t mono64(double x)
 {
@@ -174,7 +181,7 @@ struct SmoShared {
 // Per-row epilogue shared by the scan (do_update = false) and the pass: kernel values from the
 // dot products, G update, and each dual's 64-bit up / low candidate keys (score << 32 | ~index;
 // 0 = not a candidate) kept in registers: ku[2 j + c], kl[2 j + c] for row j, copy c.
-template <int RPT>
+template <int RPT, bool RBFK>
 __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& sh, int64_t li0,
                                              int64_t cta_end, bool do_update,
                                              const float (&acc)[RPT][SVM_WS],
@@ -188,9 +195,18 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
         float S = 0.0f;
         if (do_update) {
             const float xn = __ldg(a.xnorm + li);
+            if constexpr (RBFK) {  // exp(-gamma |x_i - x_r|^2) with the distance from the norms
+                const float ng = -a.kp.gamma * 1.4426950408889634f;  // exp(z) = 2^(z log2 e)
 #pragma unroll
-            for (int r = 0; r < SVM_WS; ++r)
-                S = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]), S);
+                for (int r = 0; r < SVM_WS; ++r) {
+                    const float d2 = fmaxf(fmaf(-2.0f, acc[j][r], xn + sh.xn[r]), 0.0f);
+                    S = fmaf(sh.c[r], exp2f_approx(ng * d2), S);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < SVM_WS; ++r)
+                    S = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]), S);
+            }
         }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -238,6 +254,7 @@ __device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[N
     };
     uint64_t lu = doU ? lmax(ku, ou) : 0ull, ll = doL ? lmax(kl, ol) : 0ull;
     uint64_t nu = 0ull, nl = 0ull;
+#pragma unroll 1
     for (int r = 0; r < 8; ++r) {
         const uint64_t bu = warp_max_u64(lu);
         const uint64_t bl = warp_max_u64(ll);
@@ -266,6 +283,7 @@ __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* 
     int idx = 0;
     uint64_t head = lane < SMO_WARPS ? lists[lane][0] : 0;
     uint64_t next = lane < SMO_WARPS ? lists[lane][1] : 0;
+#pragma unroll 1
     for (int r = 0; r < 8; ++r) {
         uint64_t best = warp_max_u64(head);
         if (lane == 0) out[r] = best;
@@ -297,6 +315,7 @@ __device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64
         nxt[k] = l < L ? keys[l * 8 + 1] : 0;
         hd[k] = 0;
     }
+#pragma unroll 1
     for (int r = 0; r < 8; ++r) {
         uint64_t lb = cur[0];
 #pragma unroll
@@ -381,17 +400,18 @@ __device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C,
     const int pa = lane & 15;
     const bool valid = lane < nw;
     const int y = valid ? sh.w_y[lane] : 1;
-    double al = valid ? sh.w_alpha[lane] : 0.0;
+    const double al0 = valid ? sh.w_alpha[lane] : 0.0;
     double s = valid ? -(double)y * sh.w_G[lane] : 0.0;
-    const uint32_t ypos = __ballot_sync(FULL, y > 0);
     // shared-window addresses computed once (keeps S2R/LEA off the per-step chain)
     const uint32_t a_ie = (uint32_t)__cvta_generic_to_shared(sh.inv_eta);
     const uint32_t a_krow = (uint32_t)__cvta_generic_to_shared(sh.kpos + pa * SVM_WS);
+    // room to move y_a alpha_a up (> 0 <=> a in I_up) and down (> 0 <=> a in I_low)
+    double up_room = valid ? (y > 0 ? C - al0 : al0) : 0.0;
+    double dn_room = valid ? (y > 0 ? al0 : C - al0) : 0.0;
     int step = 0;
     for (; step < inner_max; ++step) {
-        const bool upok = valid && (y > 0 ? al < C : al > 0.0);
-        const bool lowok = valid && (y > 0 ? al > 0.0 : al < C);
-        const uint64_t ku = upok ? mono64(s) : 0ull, kl = lowok ? mono64(-s) : 0ull;
+        const uint64_t ku = up_room > 0.0 ? mono64(s) : 0ull;
+        const uint64_t kl = dn_room > 0.0 ? mono64(-s) : 0ull;
         const uint32_t hu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32));
         const uint32_t hl = __reduce_max_sync(FULL, (uint32_t)(kl >> 32));
         const uint32_t lu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32) == hu ? (uint32_t)ku : 0u);
@@ -404,26 +424,29 @@ __device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C,
         const double ie = lds_f64(a_ie + 8u * (uint32_t)(i * SVM_WS + j));
         const double kai = lds_f64(a_krow + 8u * (uint32_t)i);
         const double kaj = lds_f64(a_krow + 8u * (uint32_t)j);
-        const double ai = __shfl_sync(FULL, al, i), aj = __shfl_sync(FULL, al, j);
-        const bool yi = (ypos >> i) & 1u, yj = (ypos >> j) & 1u;
+        // lim_i = room of i to move up, lim_j = room of j to move down
+        const double lim_i = __shfl_sync(FULL, up_room, i), lim_j = __shfl_sync(FULL, dn_room, j);
         double t = (si - sj) * ie;
-        const double lim_i = yi ? C - ai : ai;
-        const double lim_j = yj ? aj : C - aj;
         const bool ci = t >= lim_i;
         t = ci ? lim_i : t;
         const bool cj = t >= lim_j;
         t = cj ? lim_j : t;
         const bool clip_i = ci && (!cj || lim_i == lim_j);
-        const double ni = clip_i ? (yi ? C : 0.0) : (yi ? ai + t : ai - t);
-        const double nj = cj ? (yj ? 0.0 : C) : (yj ? aj - t : aj + t);
-        al = lane == i ? ni : (lane == j ? nj : al);
+        if (lane == i) {  // y_i alpha_i += t; clipped -> exactly at its bound
+            up_room = clip_i ? 0.0 : up_room - t;
+            dn_room = clip_i ? C : dn_room + t;
+        }
+        if (lane == j) {  // y_j alpha_j -= t
+            dn_room = cj ? 0.0 : dn_room - t;
+            up_room = cj ? C : up_room + t;
+        }
         s = fma(t, kaj - kai, s);
     }
-    if (lane < SVM_WS) sh.w_anew[lane] = al;
+    if (lane < SVM_WS) sh.w_anew[lane] = valid ? (y > 0 ? C - up_room : up_room) : 0.0;
     return step;
 }
 
-template <bool CSR, int RPT, bool XS>
+template <bool CSR, int RPT, bool XS, bool RBFK>
 __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a)
 {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -508,13 +531,14 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         for (int ch = warp; ch < nchunks; ch += SMO_WARPS) {
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             uint64_t ku[2 * RPT], kl[2 * RPT];
-            row_epilogue<RPT>(a, sh, li0, cta_end, false, acc, ku, kl);
+            row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, false, acc, ku, kl);
             merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
         }
         finish_lists(wlu, wll);
         publish(a.tag0 + 1);
     }
 
+#ifdef SMO_PROFILE
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long wprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // worker view (warp 0)
     long long wprev = 0;
@@ -523,12 +547,19 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         if (ph >= 0) wprof[ph] += now - wprev;
         wprev = now;
     };
+#else
+    auto wmark = [](int) {};
+#endif
+#ifdef SMO_PROFILE
     long long tprev = clock64();
     auto mark = [&](int ph) {
         long long now = clock64();
         prof[ph] += now - tprev;
         tprev = now;
     };
+#else
+    auto mark = [](int) {};
+#endif
     for (int64_t t = 0;; ++t) {
         const uint32_t tag = a.tag0 + 1 + (uint32_t)t;
         const int par = tag & 1;
@@ -590,9 +621,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             const uint64_t* keys = warp == 0 ? sKU : sKL;
             uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
             int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
-            if (L <= 32) global_merge<1>(keys, L, out, srcs, lane);
-            else if (L <= 64) global_merge<2>(keys, L, out, srcs, lane);
-            else if (L <= 160) global_merge<5>(keys, L, out, srcs, lane);
+            if (L <= 160) global_merge<5>(keys, L, out, srcs, lane);
             else global_merge_smem(keys, reinterpret_cast<uint8_t*>(sh.qpart) + warp * 2048, L,
                                    out, srcs, lane);
         }
@@ -671,10 +700,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 a.info->M_low = sh.M_low;
                 a.info->converged = (sh.m_up - sh.M_low <= a.tol) ? 1 : 0;
             }
+#ifdef SMO_PROFILE
             if (reporter && tid == SOLVER_WARP * 32)
                 for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[ph] = prof[ph];
             if (reporter && tid == 0)
                 for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[8 + ph] = wprof[ph];
+#endif
             return;
         }
         // ---- a2 setup: X_W rows (fp32 [d][16] for the pass, fp64 [16][dp] for K_WW), their
@@ -796,6 +827,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         mark(3);
 
         uint64_t wlu = 0, wll = 0;  // this warp's running top-8 lists
+        bool waited = !a.overlap && warp != SOLVER_WARP;
+        if (waited) named_bar_sync(1, SMO_THREADS);
         if (warp == SOLVER_WARP) {
             // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
             // arbiter favours high ids), overlapped with the other warps' dot products ----------
@@ -833,52 +866,35 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
             __threadfence_block();
             named_bar_arrive(1, SMO_THREADS);
+            waited = true;
             mark(4);
-            for (;;) {  // the solver warp joins the pass
-                int ch = 0;
-                if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
-                ch = __shfl_sync(FULL, ch, 0);
-                if (ch >= nchunks) break;
-                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
-                float acc[RPT][SVM_WS];
-                if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
-                else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
-                uint64_t ku[2 * RPT], kl[2 * RPT];
-                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, ku, kl);
-                merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
-            }
-        } else {
-            // ---- a3: the fused kernel-row + gradient pass (first chunk overlaps a2) -----------
-            bool waited = false;
-            wmark(-1);
-            for (;;) {
-                int ch = 0;
-                if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
-                ch = __shfl_sync(FULL, ch, 0);
-                if (ch >= nchunks) break;
-                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
-                if (!waited && !a.overlap) {
-                    named_bar_sync(1, SMO_THREADS);
-                    waited = true;
-                }
-                float acc[RPT][SVM_WS];
-                if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
-                else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
-                wmark(0);
-                if (!waited) {
-                    named_bar_sync(1, SMO_THREADS);
-                    waited = true;
-                }
-                wmark(1);
-                uint64_t ku[2 * RPT], kl[2 * RPT];
-                row_epilogue<RPT>(a, sh, li0, cta_end, true, acc, ku, kl);
-                wmark(2);
-                merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
-                wmark(3);
-            }
-            if (!waited) named_bar_sync(1, SMO_THREADS);
-            wmark(4);
         }
+        // ---- a3: the fused kernel-row + gradient pass; every warp takes chunks, the workers'
+        // first chunk overlapping a2 (they wait for c only before its epilogue) --------------
+        wmark(-1);
+        for (;;) {
+            int ch = 0;
+            if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
+            ch = __shfl_sync(FULL, ch, 0);
+            if (ch >= nchunks) break;
+            const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+            float acc[RPT][SVM_WS];
+            if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
+            else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
+            wmark(0);
+            if (!waited) {
+                named_bar_sync(1, SMO_THREADS);
+                waited = true;
+            }
+            wmark(1);
+            uint64_t ku[2 * RPT], kl[2 * RPT];
+            row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, true, acc, ku, kl);
+            wmark(2);
+            merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
+            wmark(3);
+        }
+        if (!waited) named_bar_sync(1, SMO_THREADS);
+        wmark(4);
         mark(5);
         finish_lists(wlu, wll);
         mark(6);
@@ -935,15 +951,15 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
 {
     void* args[] = {const_cast<SmoArgs*>(&a)};
     const void* fn;
-    if (a.XT == nullptr) fn = (const void*)smo_persistent<true, 1, false>;
+    const bool rbf = a.kp.kernel == 2;
+#define SMO_PICK(CSR_, RPT_, XS_) \
+    (rbf ? (const void*)smo_persistent<CSR_, RPT_, XS_, true> : (const void*)smo_persistent<CSR_, RPT_, XS_, false>)
+    if (a.XT == nullptr) fn = SMO_PICK(true, 1, false);
     else if (a.x_in_smem)
-        fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, true>
-           : a.rpt == 2 ? (const void*)smo_persistent<false, 2, true>
-                        : (const void*)smo_persistent<false, 1, true>;
+        fn = a.rpt == 4 ? SMO_PICK(false, 4, true) : a.rpt == 2 ? SMO_PICK(false, 2, true) : SMO_PICK(false, 1, true);
     else
-        fn = a.rpt == 4 ? (const void*)smo_persistent<false, 4, false>
-           : a.rpt == 2 ? (const void*)smo_persistent<false, 2, false>
-                        : (const void*)smo_persistent<false, 1, false>;
+        fn = a.rpt == 4 ? SMO_PICK(false, 4, false) : a.rpt == 2 ? SMO_PICK(false, 2, false) : SMO_PICK(false, 1, false);
+#undef SMO_PICK
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
     svm_note_launches(1);

