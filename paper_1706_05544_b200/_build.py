@@ -20,6 +20,8 @@ HEADERS = ["svm_internal.cuh", "layout.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
+if os.environ.get("SVMB200_PROFILE_BUILD"):  # per-phase clock64 instrumentation of smo.cu
+    FLAGS = FLAGS + ["-DSMO_PROFILE"]
 
 
 def _nvcc() -> str:

@@ -60,15 +60,37 @@ static int fail(int code, const char* fmt, ...)
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool plain = false;  // cudaMalloc'd (exportable with cudaIpcGetMemHandle; pool memory is not)
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() { release(); }
     void release()
     {
-        if (p) cudaFreeAsync(p, 0);
+        if (p) {
+            if (plain) cudaFree(p);
+            else cudaFreeAsync(p, 0);
+        }
         p = nullptr;
         bytes = 0;
+        plain = false;
+    }
+    // Re-allocate an existing buffer as plain cudaMalloc memory (for peer export), keeping data.
+    int make_plain()
+    {
+        if (!p || plain) return SVM_OK;
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SVM_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+        }
+        cudaMemcpy(q, p, bytes, cudaMemcpyDeviceToDevice);
+        cudaFreeAsync(p, 0);
+        cudaDeviceSynchronize();
+        p = q;
+        plain = true;
+        return SVM_OK;
     }
     int alloc(size_t b)
     {
@@ -470,11 +492,22 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     if (!D.csr && smem <= smem_cap && !getenv("SVMB200_NO_XSMEM")) {
         a.x_in_smem = 1;  // this CTA's X slice stays resident in shared memory
     } else {
-        smem = smo_smem_bytes(D.d, a.world, D.nblk, 0);
+        a.x_ring = (!D.csr && a.rpt >= 2) ? 1 : 0;
+        if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
+        smem = smo_smem_bytes(D.d, a.world, D.nblk, 0) + (D.csr ? 0 : smo_ring_bytes(a.rpt));
     }
     if (smem > 220 * 1024)
         return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d lists)", smem,
                     (long long)D.d, a.world * D.nblk);
+    {   // buffer the dot products of as many rows as fit (64 B per row), whole chunks only
+        const int64_t chunk = 32 * a.rpt;
+        int64_t rows = (210 * 1024 - smem) / 64;
+        rows = std::min<int64_t>(rows, (D.rows_per_cta + chunk - 1) / chunk * chunk);
+        rows = rows / chunk * chunk;
+        if (getenv("SVMB200_NO_DBUF")) rows = 0;
+        a.dbuf_rows = (int32_t)std::max<int64_t>(rows, 0);
+        smem += (int)(64 * a.dbuf_rows);
+    }
     if (pos_elems > 65535)
         return fail(SVM_EINVAL, "%lld dual variables per CTA exceed the 16-bit candidate position",
                     (long long)pos_elems);
@@ -512,7 +545,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         double tot = 0;
         for (int i = 0; i < 8; ++i) tot += (double)info.phase_cycles[i];
         fprintf(stderr, "[svmb200] %lld iters, %.1f ms: phases (cycles/iter) wait+stage %.0f merge+W %.0f rows %.0f "
-                "qww %.0f sub %.0f pass %.0f select %.0f publish %.0f | total %.0f | inner/iter %.1f\n",
+                "qww %.0f sub %.0f A+sync %.0f B+finish %.0f publish %.0f | total %.0f | inner/iter %.1f\n",
                 (long long)info.iterations, ms,
                 info.phase_cycles[0] / (double)std::max<int64_t>(1, info.iterations),
                 info.phase_cycles[1] / (double)std::max<int64_t>(1, info.iterations),
@@ -526,8 +559,8 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
                 info.inner_total / (double)std::max<int64_t>(1, info.iterations));
         (void)clk;
         const double it = (double)std::max<int64_t>(1, info.iterations);
-        fprintf(stderr, "[svmb200]   worker warp 0 (cycles/iter): dots %.0f wait-c %.0f epilogue %.0f "
-                "merge %.0f tail %.0f finish %.0f\n", info.phase_cycles[8] / it, info.phase_cycles[9] / it,
+        fprintf(stderr, "[svmb200]   worker warp 0 (cycles/iter): B-dots %.0f - %.0f B-epilogue %.0f "
+                "B-merge %.0f B-tail %.0f finish %.0f\n", info.phase_cycles[8] / it, info.phase_cycles[9] / it,
                 info.phase_cycles[10] / it, info.phase_cycles[11] / it, info.phase_cycles[12] / it,
                 info.phase_cycles[13] / it);
     }
@@ -1269,6 +1302,16 @@ static int shard_create_common(svm_shard* S, const float* y_global, const svm_pa
         if (!S->D.vals_own.p) { TRY(to_device(S->D.vals_own, S->D.vals, S->D.nnz, S->st)); S->D.vals = S->D.vals_own.as<float>(); }
     }
     CK(cudaStreamSynchronize(S->st));
+    // everything a peer maps must be a cudaMalloc base (IPC cannot export pool memory)
+    DBuf* exported[] = {&S->E.xw, &S->xbuf, &S->xflags, &S->D.XR_own, &S->D.norms,
+                        &S->D.indptr_own, &S->D.indices_own, &S->D.vals_own, &S->svidx, &S->coefx};
+    for (DBuf* b : exported) TRY(b->make_plain());
+    if (!S->D.csr) S->D.XR = S->D.XR_own.as<float>();
+    else {
+        S->D.indptr = S->D.indptr_own.as<int64_t>();
+        S->D.indices = S->D.indices_own.as<int32_t>();
+        S->D.vals = S->D.vals_own.as<float>();
+    }
     return SVM_OK;
 }
 

@@ -131,6 +131,74 @@ __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64
     }
 }
 
+// Streamed X (global): each lane keeps a private ring of PF_X feature slots in shared memory,
+// filled by cp.async (one commit group per feature), so PF_X features of its rows are in flight
+// without holding registers -- with 64 accumulators per thread ptxas keeps only ~2 plain loads
+// in flight, which left the streamed pass latency-bound.
+constexpr int PF_X = 8;
+template <int RPT>
+__device__ __forceinline__ void cp_async_x(uint32_t dst, const float* src)
+{
+    if constexpr (RPT == 4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    else if constexpr (RPT == 2)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int RPT>
+__device__ __forceinline__ void dots_dense_async(const float* __restrict__ xcol, int64_t ld, int d,
+                                                 bool active, const float* sXW, uint32_t ring,
+                                                 float (&acc)[RPT][SVM_WS])
+{
+    zero_acc<RPT>(acc);
+    if (!active) return;
+    constexpr uint32_t SLOT = 32u * 4u * RPT;  // bytes per slot across the warp
+    const float4* w4 = reinterpret_cast<const float4*>(sXW);
+#pragma unroll
+    for (int f = 0; f < PF_X; ++f) {
+        if (f < d) cp_async_x<RPT>(ring + f * SLOT, xcol + (int64_t)f * ld);
+        cp_async_commit();
+    }
+#pragma unroll 2
+    for (int k = 0; k < d; ++k) {
+        cp_async_wait<PF_X - 1>();
+        const uint32_t sa = ring + (uint32_t)(k & (PF_X - 1)) * SLOT;
+        float x[RPT];
+        if constexpr (RPT == 4) {
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sa) : "memory");
+            x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+        } else if constexpr (RPT == 2) {
+            float2 v;
+            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sa) : "memory");
+            x[0] = v.x; x[1] = v.y;
+        } else {
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(sa) : "memory");
+        }
+        float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[j][4 * q + 0] = fmaf(x[j], wv[q].x, acc[j][4 * q + 0]);
+                acc[j][4 * q + 1] = fmaf(x[j], wv[q].y, acc[j][4 * q + 1]);
+                acc[j][4 * q + 2] = fmaf(x[j], wv[q].z, acc[j][4 * q + 2]);
+                acc[j][4 * q + 3] = fmaf(x[j], wv[q].w, acc[j][4 * q + 3]);
+            }
+        }
+        // refill the slot just consumed with feature k + PF_X
+        if (k + PF_X < d) cp_async_x<RPT>(sa, xcol + (int64_t)(k + PF_X) * ld);
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+}
+
 // CSR kernel-row dot products for one row: sum over its nnz of v * X_W^T[col][r].
 __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
                                          const int32_t* __restrict__ indices,
@@ -174,7 +242,7 @@ struct SmoShared {
     int32_t w_y[SVM_WS];
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
     float xn[SVM_WS];                    // |x_r|^2 of the distinct rows
-    int32_t nw, nr, stop, timeout, next_chunk, inner_steps;
+    int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps;
     double m_up, M_low;
 };
 
@@ -228,10 +296,27 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
     }
 }
 
+// Descending sort of a lane's NK keys (odd-even transposition network, fully unrolled).
+template <int NK>
+__device__ __forceinline__ void sort_desc(uint64_t (&k)[NK])
+{
+#pragma unroll
+    for (int i = 0; i < NK; ++i) {
+#pragma unroll
+        for (int j = (i & 1); j + 1 < NK; j += 2) {
+            const uint64_t x = k[j], y = k[j + 1];
+            const bool sw = y > x;
+            k[j] = sw ? y : x;
+            k[j + 1] = sw ? x : y;
+        }
+    }
+}
+
 // Merge one chunk's candidate keys (NK per lane) into the warp's running top-8 lists (lane l < 8
-// holds the l-th best; 0 = empty), up and low together: extraction rounds of a 64-bit warp max,
-// the winning lane dropping the extracted key.  A chunk with no key above the current 8th is
-// skipped.  Keys are unique, so the result is exact.
+// holds the l-th best; 0 = empty), up and low together.  Each lane sorts its keys once; every
+// extraction round takes the 64-bit warp max of the lanes' heads (own list entry vs sorted
+// chunk keys) and the winning lane pops its head -- no rescans.  A side with no key above the
+// current 8th is skipped.  Keys are unique, so the result is exact.
 template <int NK>
 __device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[NK], uint64_t& wlu,
                                             uint64_t& wll, int lane)
@@ -245,32 +330,32 @@ __device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[N
     }
     const bool doU = __any_sync(FULL, au), doL = __any_sync(FULL, alo);
     if (!doU && !doL) return;
+    if (doU) sort_desc<NK>(ku);
+    if (doL) sort_desc<NK>(kl);
     uint64_t ou = lane < 8 ? wlu : 0ull, ol = lane < 8 ? wll : 0ull;
-    auto lmax = [&](const uint64_t (&k)[NK], uint64_t own) {
-        uint64_t m = own;
-#pragma unroll
-        for (int q = 0; q < NK; ++q) m = k[q] > m ? k[q] : m;
-        return m;
-    };
-    uint64_t lu = doU ? lmax(ku, ou) : 0ull, ll = doL ? lmax(kl, ol) : 0ull;
     uint64_t nu = 0ull, nl = 0ull;
 #pragma unroll 1
     for (int r = 0; r < 8; ++r) {
-        const uint64_t bu = warp_max_u64(lu);
-        const uint64_t bl = warp_max_u64(ll);
+        const uint64_t hu = doU ? (ku[0] > ou ? ku[0] : ou) : 0ull;
+        const uint64_t hl = doL ? (kl[0] > ol ? kl[0] : ol) : 0ull;
+        const uint64_t bu = warp_max_u64(hu);
+        const uint64_t bl = warp_max_u64(hl);
         if (lane == r) { nu = bu; nl = bl; }
-        if (bu == 0ull && bl == 0ull) break;
-        if (bu != 0ull && lu == bu) {
+        if (bu != 0ull && hu == bu) {
             if (ou == bu) ou = 0ull;
+            else {
 #pragma unroll
-            for (int q = 0; q < NK; ++q) ku[q] = ku[q] == bu ? 0ull : ku[q];
-            lu = lmax(ku, ou);
+                for (int q = 0; q + 1 < NK; ++q) ku[q] = ku[q + 1];
+                ku[NK - 1] = 0ull;
+            }
         }
-        if (bl != 0ull && ll == bl) {
+        if (bl != 0ull && hl == bl) {
             if (ol == bl) ol = 0ull;
+            else {
 #pragma unroll
-            for (int q = 0; q < NK; ++q) kl[q] = kl[q] == bl ? 0ull : kl[q];
-            ll = lmax(kl, ol);
+                for (int q = 0; q + 1 < NK; ++q) kl[q] = kl[q + 1];
+                kl[NK - 1] = 0ull;
+            }
         }
     }
     if (doU) wlu = nu;
@@ -461,6 +546,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWd + (size_t)SVM_WS * dp); // [L][8]
     uint64_t* sKL = sKU + (size_t)L * 8;                                     // [L][8]
     float* sX = reinterpret_cast<float*>(sKL + (size_t)L * 8);               // [d][R] (XS)
+    // dot-product buffer: [16][dbuf_rows] fp32, column r holds x_i . x_{W_r} for the CTA's first
+    // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
+    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? 0 : (size_t)SMO_THREADS * PF_X * RPT));
+    const int dbuf_rows = a.dbuf_rows;
 
     const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
     const int64_t cta_end = min(cta_begin + a.rows_per_cta, a.n_local);
@@ -480,6 +569,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     }
     const float* xbase = XS ? sX : a.XT + cta_begin;
     const int64_t xld = XS ? R : a.n_pad;
+    // per-lane cp.async ring for streamed X (in the place of the resident slice)
+    const uint32_t xring = (uint32_t)__cvta_generic_to_shared(sX) +
+                           (uint32_t)(warp * PF_X * 32 * 4 * RPT + lane * 4 * RPT);
 
     // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
     auto finish_lists = [&](uint64_t wlu, uint64_t wll) {
@@ -523,8 +615,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         }
     };
 
-    // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
-    {
+    // ---- exact CTA selection from the stored G / status (prologue, and the rare fallback when a
+    // lane's top-3 may have truncated its candidates): per-warp extraction over fixed chunks ---
+    auto exact_select = [&]() {
         uint64_t wlu = 0, wll = 0;
         float acc[RPT][SVM_WS];
         zero_acc<RPT>(acc);
@@ -535,15 +628,25 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
         }
         finish_lists(wlu, wll);
-        publish(a.tag0 + 1);
-    }
+    };
+
+    // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
+    exact_select();
+    publish(a.tag0 + 1);
 
 #ifdef SMO_PROFILE
+    // B200 __syncthreads is BAR.SYNC.DEFER_BLOCKING: the warp only blocks at the next use of
+    // barrier-protected state, so each timestamp first consumes a shared-memory load.
+    auto fenced_clock = [&]() -> long long {
+        int v = *reinterpret_cast<volatile int*>(&sh.nw);
+        asm volatile("" ::"r"(v) : "memory");
+        return clock64();
+    };
     long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long wprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // worker view (warp 0)
     long long wprev = 0;
     auto wmark = [&](int ph) {
-        long long now = clock64();
+        long long now = fenced_clock();
         if (ph >= 0) wprof[ph] += now - wprev;
         wprev = now;
     };
@@ -553,7 +656,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 #ifdef SMO_PROFILE
     long long tprev = clock64();
     auto mark = [&](int ph) {
-        long long now = clock64();
+        long long now = fenced_clock();
         prof[ph] += now - tprev;
         tprev = now;
     };
@@ -689,6 +792,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 sh.M_low = kl0 ? -(double)unord_f32((uint32_t)(kl0 >> 32)) : INFINITY;
                 sh.stop = (sh.m_up - sh.M_low <= a.tol) || (t >= a.max_iter) || nw == 0;
                 sh.next_chunk = 0;
+                sh.next_chunk2 = 0;
             }
         }
         __syncthreads();
@@ -826,12 +930,33 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         }
         mark(3);
 
-        uint64_t wlu = 0, wll = 0;  // this warp's running top-8 lists
-        bool waited = !a.overlap && warp != SOLVER_WARP;
-        if (waited) named_bar_sync(1, SMO_THREADS);
+        uint64_t wlu = 0, wll = 0;  // this warp's running top-8 lists (exact, per chunk)
+        const int nbuf = dbuf_rows / rows_per_chunk < nchunks ? dbuf_rows / rows_per_chunk : nchunks;
+        // ---- phase A: dot products x_i . X_W of the buffered chunks into shared memory --------
+        auto phase_a = [&]() {
+            for (;;) {
+                int ch = 0;
+                if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
+                ch = __shfl_sync(FULL, ch, 0);
+                if (ch >= nbuf) break;
+                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                float acc[RPT][SVM_WS];
+                if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
+                else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
+                else dots_dense_async<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, xring, acc);
+                const int lr = (int)(li0 - cta_begin);
+#pragma unroll
+                for (int r = 0; r < SVM_WS; ++r) {
+                    float* dst = sDot + (size_t)r * dbuf_rows + lr;
+                    if constexpr (RPT == 4) *reinterpret_cast<float4*>(dst) = make_float4(acc[0][r], acc[1][r], acc[2][r], acc[3][r]);
+                    else if constexpr (RPT == 2) *reinterpret_cast<float2*>(dst) = make_float2(acc[0][r], acc[1][r]);
+                    else *dst = acc[0][r];
+                }
+            }
+        };
         if (warp == SOLVER_WARP) {
             // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
-            // arbiter favours high ids), overlapped with the other warps' dot products ----------
+            // arbiter favours high ids), overlapped with phase A on the other warps ------------
             const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
             __syncwarp();
             if (lane < nw) sh.w_dalpha[lane] = sh.w_anew[lane] - sh.w_alpha[lane];
@@ -864,38 +989,50 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     a.info->inner_total += steps;
                 }
             }
-            __threadfence_block();
-            named_bar_arrive(1, SMO_THREADS);
-            waited = true;
             mark(4);
         }
-        // ---- a3: the fused kernel-row + gradient pass; every warp takes chunks, the workers'
-        // first chunk overlapping a2 (they wait for c only before its epilogue) --------------
+        phase_a();   // the solver warp joins phase A once its subproblem is done
+        __syncthreads();
+        mark(5);
         wmark(-1);
+        // ---- phase B / a3: epilogue of every chunk (buffered dots, or computed now) ----------
         for (;;) {
             int ch = 0;
-            if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
+            if (lane == 0) ch = atomicAdd(&sh.next_chunk2, 1);
             ch = __shfl_sync(FULL, ch, 0);
             if (ch >= nchunks) break;
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             float acc[RPT][SVM_WS];
-            if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
-            else dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
-            wmark(0);
-            if (!waited) {
-                named_bar_sync(1, SMO_THREADS);
-                waited = true;
+            if (ch < nbuf) {
+                const int lr = (int)(li0 - cta_begin);
+#pragma unroll
+                for (int r = 0; r < SVM_WS; ++r) {
+                    const float* src = sDot + (size_t)r * dbuf_rows + lr;
+                    if constexpr (RPT == 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(src);
+                        acc[0][r] = v.x; acc[1][r] = v.y; acc[2][r] = v.z; acc[3][r] = v.w;
+                    } else if constexpr (RPT == 2) {
+                        const float2 v = *reinterpret_cast<const float2*>(src);
+                        acc[0][r] = v.x; acc[1][r] = v.y;
+                    } else {
+                        acc[0][r] = *src;
+                    }
+                }
+            } else if constexpr (CSR) {
+                dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
+            } else if (XS || !a.x_ring) {
+                dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
+            } else {
+                dots_dense_async<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, xring, acc);
             }
-            wmark(1);
+            wmark(0);
             uint64_t ku[2 * RPT], kl[2 * RPT];
             row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, true, acc, ku, kl);
             wmark(2);
             merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
             wmark(3);
         }
-        if (!waited) named_bar_sync(1, SMO_THREADS);
         wmark(4);
-        mark(5);
         finish_lists(wlu, wll);
         mark(6);
         wmark(5);
@@ -940,11 +1077,13 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
 
 }  // namespace
 
+int smo_ring_bytes(int rpt) { return SMO_THREADS * PF_X * 4 * rpt; }
+
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)
 {
     int64_t L = (int64_t)world * nblk;
     int64_t dp = (d + 3) & ~3;
-    return (int)(d * 64 + 128 * dp + L * 8 * 8 * 2 + 4 * d * x_rows);
+    return (int)(d * 64 + 128 * dp + L * 8 * 8 * 2 + 4 * d * x_rows);  // + 64 B per buffered row
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)

@@ -155,7 +155,9 @@ struct SmoArgs {
     uint64_t timeout_ns;
     SmoInfo* info;
     int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
-    int32_t overlap;          // 1: the pass's dot products overlap the subproblem
+    int32_t overlap;          // (unused, kept for ABI-internal compatibility)
+    int32_t dbuf_rows;        // rows whose 16 dot products are buffered in shared memory
+    int32_t x_ring;           // streamed X through a per-lane cp.async ring (RPT >= 2)
 };
 
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
@@ -163,5 +165,6 @@ void svm_note_launches(int k);
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
+int smo_ring_bytes(int rpt);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);

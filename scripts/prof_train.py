@@ -9,8 +9,12 @@ name, _, n = cfg.partition(":")
 mi = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 ds = synth.make(name, n=int(n) if n else None)
 reg = ds.svm_type == synth.EPS_REGRESSION
-X = torch.from_numpy(ds.X).cuda(); y = torch.from_numpy(ds.y).cuda()
-m = pkg.train(X, y, svm_type="eps-regression" if reg else "C-classification", gamma=1.0 / ds.d,
-              max_iter=mi, certify=0)
+kw = dict(svm_type="eps-regression" if reg else "C-classification", gamma=1.0 / ds.d, max_iter=mi,
+          certify=0)
+if ds.is_csr:
+    m = pkg.train_csr(torch.from_numpy(ds.indptr).cuda(), torch.from_numpy(ds.indices).cuda(),
+                      torch.from_numpy(ds.data).cuda(), torch.from_numpy(ds.y).cuda(), ds.d, **kw)
+else:
+    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), **kw)
 i = m.info
 print(f"{cfg}: iters {i.iterations} loop {i.loop_ms:.2f} ms us/iter {i.loop_ms*1e3/max(1,i.iterations):.2f}")

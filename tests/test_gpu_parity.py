@@ -341,3 +341,22 @@ def test_csr_equals_dense_end_to_end():
     om = ora.train(Xd, ds.y, gamma=1.0 / 60)
     assert abs(mc.info.dual_objective - om.results[0]["dual"]) <= 1e-4 * abs(om.results[0]["dual"])
     assert np.abs(dc[:, 0] - om.decision_function(Xh.dense())[:, 0]).max() <= 1e-3
+
+
+def test_sharded_api_world1_matches_single_gpu():
+    """svm_shard_* at world = 1 runs the sharded code path end to end (cudaIpc handle export,
+    connect, device-side rank exchange, global SV gather over peer pointers) and must train the
+    same model as svm_train (same CTA partition -> bit-identical alpha)."""
+    from paper_1706_05544_b200.binding import train_sharded
+    for cfg, kw in (("c2", dict(svm_type="eps-regression")), ("c1", {})):
+        ds = synth.make(cfg, n=3000)
+        m1 = pkg.train(ds.X, ds.y, gamma=1.0 / ds.d, **kw)
+        ms = train_sharded(ds.X, 0, ds.y, 0, 1, lambda b: [b], gamma=1.0 / ds.d, **kw)
+        i1, c1 = m1.support()
+        i2, c2 = ms.support()
+        np.testing.assert_array_equal(i1, i2)
+        np.testing.assert_array_equal(c1, c2)
+        assert ms.info.iterations == m1.info.iterations
+        assert ms.info.b[0] == m1.info.b[0]
+        Xh = synth.make(cfg, n=500, heldout=True).X
+        np.testing.assert_array_equal(m1.predict(Xh), ms.predict(Xh))
