@@ -28,6 +28,10 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SOLVER_WARP = SMO_WARPS - 1;
+// X_W^T row stride in floats: dense reads broadcast one feature per warp (16 is fine); CSR reads
+// 32 random features per warp, so the stride is padded to 20 floats (80 B = 5 x 16 B, coprime
+// with the 8 16-byte bank groups) -- with 16 all lanes fell into two bank groups (16-way conflict).
+constexpr int WSTR_CSR = 20;
 
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p, bool sys)
 {
@@ -212,7 +216,7 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
     for (int64_t p = b; p < e; ++p) {
         int k = __ldg(indices + p);
         float v = __ldg(vals + p);
-        float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
+        float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             acc[0][4 * q + 0] = fmaf(v, wv[q].x, acc[0][4 * q + 0]);
@@ -221,6 +225,53 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
             acc[0][4 * q + 3] = fmaf(v, wv[q].w, acc[0][4 * q + 3]);
         }
     }
+}
+
+// CSR pass with per-warp staging: the 32 rows of a chunk own one contiguous nonzero range
+// [indptr[r0], indptr[r0 + 32]); the warp loads it coalesced into shared memory, then every
+// lane walks its own row from there (no dependent global loads on the FMA chain).  Ranges
+// larger than the buffer fall back to direct loads.
+constexpr int CSR_CAP = 1600;  // nonzeros per warp stage (c5: 32 rows x ~40 nnz)
+__device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indptr,
+                                                const int32_t* __restrict__ indices,
+                                                const float* __restrict__ vals, int64_t li0_warp,
+                                                int64_t row_end, int lane, uint16_t* st_idx,
+                                                float* st_val, const float* sXW,
+                                                float (&acc)[1][SVM_WS])
+{
+    zero_acc<1>(acc);
+    const int64_t li = li0_warp + lane;
+    const int64_t rlast = min(li0_warp + 32, row_end);
+    if (li0_warp >= row_end) return;
+    const int64_t z0 = __ldg(indptr + li0_warp), z1 = __ldg(indptr + rlast);
+    const bool active = li < row_end;
+    int64_t b = 0, e = 0;
+    if (active) { b = __ldg(indptr + li); e = __ldg(indptr + li + 1); }
+    if (z1 - z0 > CSR_CAP) {  // rare: direct path
+        dots_csr(indptr, indices, vals, li, active, sXW, acc);
+        return;
+    }
+    for (int64_t p = z0 + lane; p < z1; p += 32) {
+        st_idx[p - z0] = (uint16_t)__ldg(indices + p);
+        st_val[p - z0] = __ldg(vals + p);
+    }
+    __syncwarp();
+    if (active) {
+        const float4* w4 = reinterpret_cast<const float4*>(sXW);
+        for (int64_t p = b; p < e; ++p) {
+            const int k = st_idx[p - z0];
+            const float v = st_val[p - z0];
+            const float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                acc[0][4 * q + 0] = fmaf(v, wv[q].x, acc[0][4 * q + 0]);
+                acc[0][4 * q + 1] = fmaf(v, wv[q].y, acc[0][4 * q + 1]);
+                acc[0][4 * q + 2] = fmaf(v, wv[q].z, acc[0][4 * q + 2]);
+                acc[0][4 * q + 3] = fmaf(v, wv[q].w, acc[0][4 * q + 3]);
+            }
+        }
+    }
+    __syncwarp();
 }
 
 // Shared state of one persistent CTA (static part; X_W, the staged keys, the score arrays and
@@ -542,13 +593,16 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int dp = (d + 3) & ~3;
     const int R = (int)a.rows_per_cta;
     float* sXW = reinterpret_cast<float*>(dyn_smem);                        // [d][16] fp32
-    double* sXWd = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);      // [16][dp] fp64
-    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWd + (size_t)SVM_WS * dp); // [L][8]
+    constexpr int WS = CSR ? WSTR_CSR : SVM_WS;                               // sXW row stride
+    double* sXWd = reinterpret_cast<double*>(sXW + (size_t)d * WS);           // [16][dp] fp64 (dense)
+    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWd + (CSR ? 0 : (size_t)SVM_WS * dp)); // [L][8]
     uint64_t* sKL = sKU + (size_t)L * 8;                                     // [L][8]
     float* sX = reinterpret_cast<float*>(sKL + (size_t)L * 8);               // [d][R] (XS)
     // dot-product buffer: [16][dbuf_rows] fp32, column r holds x_i . x_{W_r} for the CTA's first
     // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
-    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? 0 : (size_t)SMO_THREADS * PF_X * RPT));
+    float* csr_val = sX + (size_t)warp * CSR_CAP;                                   // CSR only
+    uint16_t* csr_idx = reinterpret_cast<uint16_t*>(sX + (size_t)SMO_WARPS * CSR_CAP) + (size_t)warp * CSR_CAP;
+    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * PF_X * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
     const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
@@ -815,12 +869,13 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         // ---- a2 setup: X_W rows (fp32 [d][16] for the pass, fp64 [16][dp] for K_WW), their
         // norms and the W payloads; one warp per row, no integer division -------------------
         const int nw = sh.nw, nr = sh.nr;
-        for (int i = tid; i < d * SVM_WS; i += SMO_THREADS)
-            if ((i & 15) >= nr || CSR) sXW[i] = 0.0f;
         if constexpr (CSR) {
-            for (int i = tid; i < nr * dp; i += SMO_THREADS) sXWd[i] = 0.0;
-            __syncthreads();
+            for (int i = tid; i < d * WS; i += SMO_THREADS) sXW[i] = 0.0f;
+        } else {
+            for (int i = tid; i < d * SVM_WS; i += SMO_THREADS)
+                if ((i & 15) >= nr) sXW[i] = 0.0f;
         }
+        if constexpr (CSR) __syncthreads();
         if (warp == SMO_WARPS - 1 && lane < nw) {  // payloads of W (tagged words)
             const int p = lane;
             const int q = sh.w_src[p] % XW_PER_SLOT;
@@ -849,12 +904,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 }
             } else {
                 const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
-                for (int64_t p = b + lane; p < e; p += 32) {
-                    const int k = a.peer_indices[o][p];
-                    const float v = a.peer_vals[o][p];
-                    sXW[k * SVM_WS + r] = v;
-                    sXWd[r * dp + k] = (double)v;
-                }
+                for (int64_t p = b + lane; p < e; p += 32)
+                    sXW[a.peer_indices[o][p] * WS + r] = a.peer_vals[o][p];
             }
             if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];
         }
@@ -872,7 +923,16 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
                 const int sidx = r + rem;
                 double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-                if (sidx != r || a.kp.kernel != 2) {
+                if constexpr (CSR) {   // from the fp32 [d][16] tile (no fp64 copy for CSR)
+                    const int k0 = part * klen, k1 = min(k0 + klen, d);
+                    if (sidx != r || a.kp.kernel != 2) {
+                        for (int k = k0; k < k1; ++k) {
+                            const double u = (double)sXW[k * WS + r], v = (double)sXW[k * WS + sidx];
+                            if (a.kp.kernel == 2) { const double t0 = u - v; acc0 = fma(t0, t0, acc0); }
+                            else acc0 = fma(u, v, acc0);
+                        }
+                    }
+                } else if (sidx != r || a.kp.kernel != 2) {
                     const double2* xr = reinterpret_cast<const double2*>(sXWd + r * dp);
                     const double2* xs = reinterpret_cast<const double2*>(sXWd + sidx * dp);
                     const int k0 = part * klen, k1 = min(k0 + klen, dp);
@@ -941,7 +1001,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 if (ch >= nbuf) break;
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
-                if constexpr (CSR) dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
+                if constexpr (CSR) dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
                 else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
                 else dots_dense_async<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, xring, acc);
                 const int lr = (int)(li0 - cta_begin);
@@ -1019,7 +1079,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     }
                 }
             } else if constexpr (CSR) {
-                dots_csr(a.indptr, a.indices, a.vals, li0, li0 < cta_end, sXW, acc);
+                dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
             } else if (XS || !a.x_ring) {
                 dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
             } else {
@@ -1050,7 +1110,8 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
     float* sXW = reinterpret_cast<float*>(dyn_smem);
     __shared__ float xn[SVM_WS];
     const int d = (int)a.d;
-    for (int i = threadIdx.x; i < d * SVM_WS; i += blockDim.x) sXW[i] = 0.0f;
+    constexpr int WS = CSR ? WSTR_CSR : SVM_WS;
+    for (int i = threadIdx.x; i < d * WS; i += blockDim.x) sXW[i] = 0.0f;
     __syncthreads();
     if constexpr (!CSR) {
         for (int i = threadIdx.x; i < d * SVM_WS; i += blockDim.x) {
@@ -1061,7 +1122,7 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
         for (int r = 0; r < nr; ++r) {
             int64_t b = a.peer_indptr[0][rows[r]], e = a.peer_indptr[0][rows[r] + 1];
             for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x)
-                sXW[a.peer_indices[0][p] * SVM_WS + r] = a.peer_vals[0][p];
+                sXW[a.peer_indices[0][p] * WS + r] = a.peer_vals[0][p];
         }
     }
     if (threadIdx.x < SVM_WS) xn[threadIdx.x] = threadIdx.x < nr ? a.xnorm[rows[threadIdx.x]] : 0.0f;
@@ -1078,6 +1139,8 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
 }  // namespace
 
 int smo_ring_bytes(int rpt) { return SMO_THREADS * PF_X * 4 * rpt; }
+int smo_csr_stage_bytes() { return SMO_WARPS * CSR_CAP * 6; }
+int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS)); }
 
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)
 {
@@ -1109,7 +1172,7 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st)
 {
-    int smem = (int)(a.d * 64);
+    int smem = (int)(a.d * 4 * (a.XT == nullptr ? WSTR_CSR : SVM_WS));
     int grid = (int)((a.n_local + 255) / 256);
     if (a.XT == nullptr) {
         cudaFuncSetAttribute(kernel_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

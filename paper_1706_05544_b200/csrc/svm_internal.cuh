@@ -166,5 +166,7 @@ void svm_note_launches(int k);
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
 int smo_ring_bytes(int rpt);
+int smo_csr_stage_bytes();
+int smo_csr_w_extra_bytes(int64_t d);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);
