@@ -1,5 +1,2 @@
-export SVMB200_PROFILE=1
-timeout 900 python scripts/prof_train.py c5:200000 300 2>&1 | tail -3
-timeout 900 python scripts/prof_train.py c5 100 2>&1 | tail -3
-unset SVMB200_PROFILE
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x -s > gpurun_out/pytest_full.log 2>&1; echo full_rc=$?; tail -5 gpurun_out/pytest_full.log
+timeout 300 python scripts/probe.py c4 > gpurun_out/probe_c4.log 2>&1; tail -4 gpurun_out/probe_c4.log
