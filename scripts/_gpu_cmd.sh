@@ -1,2 +1,6 @@
-timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x -s > gpurun_out/pytest_full.log 2>&1; echo full_rc=$?; tail -5 gpurun_out/pytest_full.log
-timeout 300 python scripts/probe.py c4 > gpurun_out/probe_c4.log 2>&1; tail -4 gpurun_out/probe_c4.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_all.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest_gpu_all.log
+timeout 600 python bench.py > gpurun_out/bench_r01.log 2>&1; echo bench_rc=$?; tail -1 gpurun_out/bench_r01.log | cut -c1-600
+timeout 900 python bench.py --config c4 --steps 3 --warmup 3 --cpu-seconds 10 > gpurun_out/bench_r01_c4.log 2>&1; echo bench4_rc=$?; tail -1 gpurun_out/bench_r01_c4.log | cut -c1-400
+timeout 600 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_short.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2_r01.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launches.log 2>&1; echo ncu1_rc=$?
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:smo_persistent -c 1 -o gpurun_out/smo_c2_r01 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
