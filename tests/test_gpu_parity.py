@@ -360,3 +360,86 @@ def test_sharded_api_world1_matches_single_gpu():
         assert ms.info.b[0] == m1.info.b[0]
         Xh = synth.make(cfg, n=500, heldout=True).X
         np.testing.assert_array_equal(m1.predict(Xh), ms.predict(Xh))
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_iteration_cap_is_not_an_error():
+    """reaching max_iter returns the model with converged = 0 (not an error)."""
+    ds = synth.make("c1", n=1000)
+    m = pkg.train(ds.X, ds.y, gamma=1.0 / ds.d, max_iter=5, certify=0)
+    assert m.info.converged == 0 and m.info.iterations == 5
+    om_prob = ora.Problem(ora.C_CLASSIFICATION, ds.y, ds.n)
+    r = ora.train_dual(ds.X, om_prob, ora.kspec("rbf", 1.0 / ds.d, d=ds.d), max_iter=5)
+    assert r["iterations"] == 5 and not r["converged"]
+
+
+@pytest.mark.parametrize("q", [2, 6])
+def test_small_working_sets(q):
+    """|W| = q (S:41-43 allow any even size): same solution quality as the oracle with the same q."""
+    ds = synth.make("c1", n=800)
+    m = pkg.train(ds.X, ds.y, gamma=1.0 / ds.d, working_set=q)
+    prob = ora.Problem(ora.C_CLASSIFICATION, ds.y, ds.n)
+    r = ora.train_dual(ds.X, prob, ora.kspec("rbf", 1.0 / ds.d, d=ds.d), q=q)
+    assert m.info.converged == 1
+    assert abs(m.info.dual_objective - r["dual"]) <= 1e-4 * abs(r["dual"])
+    s = pkg.Solver(ds.X, ds.y, gamma=1.0 / ds.d, working_set=q)
+    st = s.run(1)
+    W = ora.select(prob, np.zeros(prob.m), prob.p.copy(), 1.0, q)
+    np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+
+
+def test_sigmoid_one_step_and_train():
+    """The sigmoid kernel (not PSD) through one step and a short training."""
+    ds = synth.make("c1", n=600)
+    gamma, coef0 = 1.0 / ds.d, -0.5
+    ks = ora.kspec("sigmoid", gamma, coef0=coef0, d=ds.d)
+    prob = ora.Problem(ora.C_CLASSIFICATION, ds.y, ds.n)
+    W, dA, a1, G1 = ora.step(ds.X, prob, ks, np.zeros(prob.m), prob.p.copy(), 1.0)
+    s = pkg.Solver(ds.X, ds.y, kernel="sigmoid", gamma=gamma, coef0=coef0)
+    st = s.run(1)
+    np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+    _, Gg = s.get_state()
+    Gref = ora.gradient_update(ds.X, prob, ks, W, np.array(st.last_dalpha[:st.last_nw]), prob.p)
+    assert (np.abs(Gg - Gref) <= 1e-5 * np.maximum(1.0, np.abs(Gref))).all()
+
+
+def test_svr_on_csr_matches_dense():
+    """eps-SVR through the CSR pass equals the dense pass (Eq. 1 doubled problem on sparse X)."""
+    ds = synth.make("c2", n=1500)
+    X = ds.X.copy()
+    X[np.abs(X) < 1.0] = 0.0
+    ip = np.concatenate([[0], np.cumsum((X != 0).sum(1))]).astype(np.int64)
+    md = pkg.train(X, ds.y, svm_type="eps-regression", gamma=1.0 / ds.d)
+    mc = pkg.train_csr(ip, np.nonzero(X)[1].astype(np.int32), X[X != 0], ds.y, ds.d,
+                       svm_type="eps-regression", gamma=1.0 / ds.d)
+    assert abs(md.info.dual_objective - mc.info.dual_objective) <= 1e-5 * abs(md.info.dual_objective)
+    om = ora.train(X, ds.y, svm_type=ora.EPS_REGRESSION, gamma=1.0 / ds.d)
+    assert abs(mc.info.dual_objective - om.results[0]["dual"]) <= 1e-4 * abs(om.results[0]["dual"])
+
+
+def test_layouts_and_host_device_inputs():
+    """Column-major (R layout) and host vs device inputs give the identical model."""
+    import torch
+    ds = synth.make("c1", n=700)
+    m_row = pkg.train(ds.X, ds.y, gamma=1.0 / ds.d)
+    m_col = pkg.train(ds.X.T.copy(), ds.y, layout=1, gamma=1.0 / ds.d)   # d x n = column-major X
+    m_dev = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d)
+    for m in (m_col, m_dev):
+        np.testing.assert_array_equal(m.support()[1], m_row.support()[1])
+    Xh = synth.make("c1", n=300, heldout=True).X
+    np.testing.assert_array_equal(m_row.predict(Xh), m_col.predict(Xh.T.copy(), layout=1))
+    out_dev = m_row.predict(torch.from_numpy(Xh).cuda())
+    np.testing.assert_array_equal(out_dev.cpu().numpy(), m_row.predict(Xh))
+
+
+@pytest.mark.parametrize("n", [2, 3, 17])
+def test_tiny_problems(n):
+    """Tiny n (most CTAs own no rows; candidate lists shorter than |W|/2): matches the oracle."""
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 3)).astype(np.float32)
+    y = np.where(np.arange(n) % 2 == 0, 1.0, -1.0).astype(np.float32)
+    m = pkg.train(X, y, gamma=0.5, tolerance=1e-6)
+    r = ora.train(X, y, gamma=0.5, tol=1e-6)
+    assert abs(m.info.dual_objective - r.results[0]["dual"]) <= 1e-6 * max(1.0, abs(r.results[0]["dual"]))
+    np.testing.assert_allclose(m.predict(X, decision=True)[1][:, 0], r.decision_function(X)[:, 0],
+                               atol=1e-4)
