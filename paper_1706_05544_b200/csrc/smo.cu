@@ -293,7 +293,7 @@ struct SmoShared {
     int32_t w_y[SVM_WS];
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
     float xn[SVM_WS];                    // |x_r|^2 of the distinct rows
-    int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps;
+    int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
     double m_up, M_low;
 };
 
@@ -847,6 +847,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 sh.stop = (sh.m_up - sh.M_low <= a.tol) || (t >= a.max_iter) || nw == 0;
                 sh.next_chunk = 0;
                 sh.next_chunk2 = 0;
+                sh.sub_done = 0;
             }
         }
         __syncthreads();
@@ -995,8 +996,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         // ---- phase A: dot products x_i . X_W of the buffered chunks into shared memory --------
         auto phase_a = [&]() {
             for (;;) {
-                int ch = 0;
-                if (lane == 0) ch = atomicAdd(&sh.next_chunk, 1);
+                // chunks are buffered only while the subproblem runs: once it is solved the rest
+                // are cheaper fused with their epilogue in phase B (no tail of buffered work)
+                int ch = nbuf;
+                if (lane == 0 && !*reinterpret_cast<volatile int32_t*>(&sh.sub_done))
+                    ch = atomicAdd(&sh.next_chunk, 1);
                 ch = __shfl_sync(FULL, ch, 0);
                 if (ch >= nbuf) break;
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
@@ -1018,6 +1022,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
             // arbiter favours high ids), overlapped with phase A on the other warps ------------
             const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
+            if (lane == 0) *reinterpret_cast<volatile int32_t*>(&sh.sub_done) = 1;
             __syncwarp();
             if (lane < nw) sh.w_dalpha[lane] = sh.w_anew[lane] - sh.w_alpha[lane];
             __syncwarp();
@@ -1051,19 +1056,27 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
             mark(4);
         }
+        // overlap == 2 (default): the warps sharing the solver's SM sub-partition (warp % 4 == 3) leave
+        // its issue slots to the subproblem and join phase A when it is solved
+        if (a.overlap == 2 && (warp & 3) == (SOLVER_WARP & 3)) named_bar_sync(1, 32 * (SMO_WARPS / 4));
         phase_a();   // the solver warp joins phase A once its subproblem is done
         __syncthreads();
         mark(5);
         wmark(-1);
         // ---- phase B / a3: epilogue of every chunk (buffered dots, or computed now) ----------
+        // chunks [0, nA) have buffered dots; the streamed ones [nA, nchunks) are handed out
+        // first so that their X reads start together and no streamed chunk forms the tail
+        const int nA = sh.next_chunk < nbuf ? sh.next_chunk : nbuf;
+        const int nS = nchunks - nA;
         for (;;) {
-            int ch = 0;
-            if (lane == 0) ch = atomicAdd(&sh.next_chunk2, 1);
-            ch = __shfl_sync(FULL, ch, 0);
-            if (ch >= nchunks) break;
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&sh.next_chunk2, 1);
+            t = __shfl_sync(FULL, t, 0);
+            if (t >= nchunks) break;
+            const int ch = t < nS ? nA + t : t - nS;
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             float acc[RPT][SVM_WS];
-            if (ch < nbuf) {
+            if (ch < nA) {
                 const int lr = (int)(li0 - cta_begin);
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {

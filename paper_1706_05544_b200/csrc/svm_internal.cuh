@@ -155,7 +155,7 @@ struct SmoArgs {
     uint64_t timeout_ns;
     SmoInfo* info;
     int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
-    int32_t overlap;          // (unused, kept for ABI-internal compatibility)
+    int32_t overlap;          // 2: solver's sub-partition warps defer phase A; 1: all warps
     int32_t dbuf_rows;        // rows whose 16 dot products are buffered in shared memory
     int32_t x_ring;           // streamed X through a per-lane cp.async ring (RPT >= 2)
 };
