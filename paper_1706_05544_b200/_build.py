@@ -22,6 +22,8 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
 if os.environ.get("SVMB200_PROFILE_BUILD"):  # per-phase clock64 instrumentation of smo.cu
     FLAGS = FLAGS + ["-DSMO_PROFILE"]
+if os.environ.get("SVMB200_EXTRA_FLAGS"):  # debugging builds (e.g. -DSMO_POISON=0xffffffffu)
+    FLAGS = FLAGS + os.environ["SVMB200_EXTRA_FLAGS"].split()
 
 
 def _nvcc() -> str:

@@ -495,7 +495,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         a.x_ring = (!D.csr && a.rpt >= 2) ? 1 : 0;
         if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
         smem = smo_smem_bytes(D.d, a.world, D.nblk, 0) +
-               (D.csr ? smo_csr_stage_bytes() - (int)(128 * ((D.d + 3) & ~3)) + smo_csr_w_extra_bytes(D.d)
+               (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
     }
     if (smem > 220 * 1024)

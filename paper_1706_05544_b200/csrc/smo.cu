@@ -413,12 +413,23 @@ __device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[N
     if (doL) wll = nl;
 }
 
+// Explicit shared-memory 64-bit load for the list merges.  With plain indexed loads
+// (keys[l * 8 + hd + 1]) nvcc 12.9 / sm_100a returned the element one past the intended one for
+// some shared-memory carve-outs (found by a partition-invariance test: L = 40 lists, the merge
+// skipped one list entry); the explicit ld.shared reads exactly the addressed word.
+__device__ __forceinline__ uint64_t lds_u64(const uint64_t* p)
+{
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+
 // Merge SMO_WARPS sorted warp lists into the CTA top-8 (one warp).
 __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* out, int lane)
 {
     int idx = 0;
-    uint64_t head = lane < SMO_WARPS ? lists[lane][0] : 0;
-    uint64_t next = lane < SMO_WARPS ? lists[lane][1] : 0;
+    uint64_t head = lane < SMO_WARPS ? lds_u64(&lists[lane][0]) : 0;
+    uint64_t next = lane < SMO_WARPS ? lds_u64(&lists[lane][1]) : 0;
 #pragma unroll 1
     for (int r = 0; r < 8; ++r) {
         uint64_t best = warp_max_u64(head);
@@ -430,7 +441,7 @@ __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* 
         if (head == best && lane < SMO_WARPS) {
             ++idx;
             head = next;
-            next = idx + 1 < 8 ? lists[lane][idx + 1] : 0;
+            next = idx + 1 < 8 ? lds_u64(&lists[lane][idx + 1]) : 0;
         }
     }
 }
@@ -447,8 +458,8 @@ __device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) {
         int l = lane + 32 * k;
-        cur[k] = l < L ? keys[l * 8] : 0;
-        nxt[k] = l < L ? keys[l * 8 + 1] : 0;
+        cur[k] = l < L ? lds_u64(keys + l * 8) : 0;
+        nxt[k] = l < L ? lds_u64(keys + l * 8 + 1) : 0;
         hd[k] = 0;
     }
 #pragma unroll 1
@@ -470,7 +481,7 @@ __device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64
                     src[r] = l * 8 + hd[k];
                     ++hd[k];
                     cur[k] = nxt[k];
-                    nxt[k] = hd[k] + 1 < 8 ? keys[l * 8 + hd[k] + 1] : 0;
+                    nxt[k] = hd[k] + 1 < 8 ? lds_u64(keys + l * 8 + hd[k] + 1) : 0;
                 }
             }
         }
@@ -486,7 +497,7 @@ __device__ __noinline__ void global_merge_smem(const uint64_t* keys, uint8_t* he
     uint64_t lb = 0;
     int ll = -1;
     for (int l = lane; l < L; l += 32)
-        if (keys[l * 8] > lb) { lb = keys[l * 8]; ll = l; }
+        { const uint64_t kk = lds_u64(keys + l * 8); if (kk > lb) { lb = kk; ll = l; } }
     for (int r = 0; r < 8; ++r) {
         uint64_t best = warp_max_u64(lb);
         if (best == 0) {
@@ -502,7 +513,7 @@ __device__ __noinline__ void global_merge_smem(const uint64_t* keys, uint8_t* he
             ll = -1;
             for (int l = lane; l < L; l += 32) {
                 const int hh = head[l];
-                const uint64_t k = hh < 8 ? keys[l * 8 + hh] : 0;
+                const uint64_t k = hh < 8 ? lds_u64(keys + l * 8 + hh) : 0;
                 if (k > lb) { lb = k; ll = l; }
             }
         }
@@ -594,8 +605,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int R = (int)a.rows_per_cta;
     float* sXW = reinterpret_cast<float*>(dyn_smem);                        // [d][16] fp32
     constexpr int WS = CSR ? WSTR_CSR : SVM_WS;                               // sXW row stride
-    double* sXWd = reinterpret_cast<double*>(sXW + (size_t)d * WS);           // [16][dp] fp64 (dense)
-    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXWd + (CSR ? 0 : (size_t)SVM_WS * dp)); // [L][8]
+    uint64_t* sKU = reinterpret_cast<uint64_t*>(sXW + (size_t)((d * WS + 3) & ~3));  // [L][8]
     uint64_t* sKL = sKU + (size_t)L * 8;                                     // [L][8]
     float* sX = reinterpret_cast<float*>(sKL + (size_t)L * 8);               // [d][R] (XS)
     // dot-product buffer: [16][dbuf_rows] fp32, column r holds x_i . x_{W_r} for the CTA's first
@@ -615,6 +625,14 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const bool reporter = blockIdx.x == 0;  // CTA 0 of every rank reports for its rank
     uint64_t* rxw = a.peer_xw[a.rank];       // this rank's receive buffer
 
+#ifdef SMO_POISON
+    {
+        uint32_t dsz;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+        for (uint32_t i = tid; i < dsz / 4; i += SMO_THREADS) reinterpret_cast<uint32_t*>(dyn_smem)[i] = SMO_POISON;
+        __syncthreads();
+    }
+#endif
     // stage this CTA's X^T slice into shared memory once (resident across iterations)
     if constexpr (XS) {
         for (int k = warp; k < d; k += SMO_WARPS)
@@ -867,7 +885,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 #endif
             return;
         }
-        // ---- a2 setup: X_W rows (fp32 [d][16] for the pass, fp64 [16][dp] for K_WW), their
+        // ---- a2 setup: X_W rows (fp32 [d][16], for the pass and for K_WW), their
         // norms and the W payloads; one warp per row, no integer division -------------------
         const int nw = sh.nw, nr = sh.nr;
         if constexpr (CSR) {
@@ -898,11 +916,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             const int64_t lr = row - a.rank_row0[o];
             if constexpr (!CSR) {
                 const float* src = a.peer_XR[o] + lr * a.d;
-                for (int k = lane; k < dp; k += 32) {
-                    const float v = k < d ? __ldg(src + k) : 0.0f;
-                    if (k < d) sXW[k * SVM_WS + r] = v;
-                    sXWd[r * dp + k] = (double)v;
-                }
+                for (int k = lane; k < d; k += 32) sXW[k * SVM_WS + r] = __ldg(src + k);
             } else {
                 const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
                 for (int64_t p = b + lane; p < e; p += 32)
@@ -924,40 +938,30 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
                 const int sidx = r + rem;
                 double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-                if constexpr (CSR) {   // from the fp32 [d][16] tile (no fp64 copy for CSR)
-                    const int k0 = part * klen, k1 = min(k0 + klen, d);
-                    if (sidx != r || a.kp.kernel != 2) {
-                        for (int k = k0; k < k1; ++k) {
-                            const double u = (double)sXW[k * WS + r], v = (double)sXW[k * WS + sidx];
-                            if (a.kp.kernel == 2) { const double t0 = u - v; acc0 = fma(t0, t0, acc0); }
-                            else acc0 = fma(u, v, acc0);
-                        }
-                    }
-                } else if (sidx != r || a.kp.kernel != 2) {
-                    const double2* xr = reinterpret_cast<const double2*>(sXWd + r * dp);
-                    const double2* xs = reinterpret_cast<const double2*>(sXWd + sidx * dp);
+                // from the fp32 [d][WS] tile (the fp32 inputs promoted exactly): four interleaved
+                // fp64 accumulators over k, features >= d contribute exact zeros
+                if (sidx != r || a.kp.kernel != 2) {
                     const int k0 = part * klen, k1 = min(k0 + klen, dp);
+                    const float* xr = sXW + r;
+                    const float* xs = sXW + sidx;
+                    auto ld = [&](const float* x, int k) { return k < d ? (double)x[k * WS] : 0.0; };
                     if (a.kp.kernel == 2) {
-#pragma unroll 4
+#pragma unroll 1
                         for (int k = k0; k < k1; k += 4) {
-                            const double2 u0 = xr[k >> 1], v0 = xs[k >> 1];
-                            const double2 u1 = xr[(k >> 1) + 1], v1 = xs[(k >> 1) + 1];
-                            const double t0 = u0.x - v0.x, t1 = u0.y - v0.y;
-                            const double t2 = u1.x - v1.x, t3 = u1.y - v1.y;
+                            const double t0 = ld(xr, k) - ld(xs, k), t1 = ld(xr, k + 1) - ld(xs, k + 1);
+                            const double t2 = ld(xr, k + 2) - ld(xs, k + 2), t3 = ld(xr, k + 3) - ld(xs, k + 3);
                             acc0 = fma(t0, t0, acc0);
                             acc1 = fma(t1, t1, acc1);
                             acc2 = fma(t2, t2, acc2);
                             acc3 = fma(t3, t3, acc3);
                         }
                     } else {
-#pragma unroll 4
+#pragma unroll 1
                         for (int k = k0; k < k1; k += 4) {
-                            const double2 u0 = xr[k >> 1], v0 = xs[k >> 1];
-                            const double2 u1 = xr[(k >> 1) + 1], v1 = xs[(k >> 1) + 1];
-                            acc0 = fma(u0.x, v0.x, acc0);
-                            acc1 = fma(u0.y, v0.y, acc1);
-                            acc2 = fma(u1.x, v1.x, acc2);
-                            acc3 = fma(u1.y, v1.y, acc3);
+                            acc0 = fma(ld(xr, k), ld(xs, k), acc0);
+                            acc1 = fma(ld(xr, k + 1), ld(xs, k + 1), acc1);
+                            acc2 = fma(ld(xr, k + 2), ld(xs, k + 2), acc2);
+                            acc3 = fma(ld(xr, k + 3), ld(xs, k + 3), acc3);
                         }
                     }
                 }
@@ -1158,8 +1162,7 @@ int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS))
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)
 {
     int64_t L = (int64_t)world * nblk;
-    int64_t dp = (d + 3) & ~3;
-    return (int)(d * 64 + 128 * dp + L * 8 * 8 * 2 + 4 * d * x_rows);  // + 64 B per buffered row
+    return (int)(((d * 16 + 3) & ~3) * 4 + L * 8 * 8 * 2 + 4 * d * x_rows);  // + 64 B per buffered row
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)

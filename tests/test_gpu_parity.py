@@ -313,7 +313,7 @@ def test_partition_invariance_bit_identical():
     import os
     ds = synth.make("c2", n=4000)
     res = []
-    for nblk in ("3", "16", "40"):
+    for nblk in ("3", "16", "40", "41"):   # 40, 41: 100 rows per CTA (caught a merge miscompile)
         os.environ["SVMB200_NBLK"] = nblk
         try:
             s = pkg.Solver(ds.X, ds.y, svm_type="eps-regression", gamma=1.0 / ds.d)
