@@ -492,7 +492,10 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     if (!D.csr && smem <= smem_cap && !getenv("SVMB200_NO_XSMEM")) {
         a.x_in_smem = 1;  // this CTA's X slice stays resident in shared memory
     } else {
-        a.x_ring = (!D.csr && a.rpt >= 2) ? 1 : 0;
+        // wide rows streamed from HBM: one row per lane and features split into slices, so that
+        // enough (chunk, slice) items keep every warp's loads in flight
+        if (!D.csr && D.d >= 256 && !getenv("SVMB200_RPT")) a.rpt = 1;
+        a.x_ring = (!D.csr && (a.rpt >= 2 || D.d >= 256)) ? 1 : 0;
         if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
         smem = smo_smem_bytes(D.d, a.world, D.nblk, 0) +
                (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
@@ -503,12 +506,24 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
                     (long long)D.d, a.world * D.nblk);
     {   // buffer the dot products of as many rows as fit (64 B per row), whole chunks only
         const int64_t chunk = 32 * a.rpt;
-        int64_t rows = (210 * 1024 - smem) / 64;
-        rows = std::min<int64_t>(rows, (D.rows_per_cta + chunk - 1) / chunk * chunk);
+        const int64_t all_rows = (D.rows_per_cta + chunk - 1) / chunk * chunk;
+        const int64_t avail = 210 * 1024 - smem;
+        int64_t rows = avail / 64;
+        rows = std::min<int64_t>(rows, all_rows);
         rows = rows / chunk * chunk;
         if (getenv("SVMB200_NO_DBUF")) rows = 0;
+        a.nslice = 1;
+        if (!a.x_in_smem && !D.csr && D.d >= 256 && rows == all_rows) {
+            // feature slices: as many as the partial buffers allow, >= 64 features each, aiming
+            // at >= 4 items per warp
+            const int64_t nch = all_rows / chunk;
+            int64_t ns = std::min<int64_t>({avail / (64 * all_rows), D.d / 64, 8,
+                                            (4 * SMO_WARPS + nch - 1) / nch});
+            if (const char* e = getenv("SVMB200_NSLICE")) ns = std::min<int64_t>(ns, atoi(e));
+            a.nslice = (int32_t)std::max<int64_t>(ns, 1);
+        }
         a.dbuf_rows = (int32_t)std::max<int64_t>(rows, 0);
-        smem += (int)(64 * a.dbuf_rows);
+        smem += (int)(64 * a.dbuf_rows * a.nslice);
     }
     if (pos_elems > 65535)
         return fail(SVM_EINVAL, "%lld dual variables per CTA exceed the 16-bit candidate position",

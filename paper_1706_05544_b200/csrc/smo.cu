@@ -139,7 +139,8 @@ __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64
 // filled by cp.async (one commit group per feature), so PF_X features of its rows are in flight
 // without holding registers -- with 64 accumulators per thread ptxas keeps only ~2 plain loads
 // in flight, which left the streamed pass latency-bound.
-constexpr int PF_X = 8;
+template <int RPT>
+__host__ __device__ constexpr int pf_x() { return RPT == 1 ? 16 : 8; }  // ~1-2 KB of X in flight per warp
 template <int RPT>
 __device__ __forceinline__ void cp_async_x(uint32_t dst, const float* src)
 {
@@ -162,6 +163,7 @@ __device__ __forceinline__ void dots_dense_async(const float* __restrict__ xcol,
     zero_acc<RPT>(acc);
     if (!active) return;
     constexpr uint32_t SLOT = 32u * 4u * RPT;  // bytes per slot across the warp
+    constexpr int PF_X = pf_x<RPT>();
     const float4* w4 = reinterpret_cast<const float4*>(sXW);
 #pragma unroll
     for (int f = 0; f < PF_X; ++f) {
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
     float* csr_val = sX + (size_t)warp * CSR_CAP;                                   // CSR only
     uint16_t* csr_idx = reinterpret_cast<uint16_t*>(sX + (size_t)SMO_WARPS * CSR_CAP) + (size_t)warp * CSR_CAP;
-    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * PF_X * RPT));
+    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
     const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     const int64_t xld = XS ? R : a.n_pad;
     // per-lane cp.async ring for streamed X (in the place of the resident slice)
     const uint32_t xring = (uint32_t)__cvta_generic_to_shared(sX) +
-                           (uint32_t)(warp * PF_X * 32 * 4 * RPT + lane * 4 * RPT);
+                           (uint32_t)(warp * pf_x<RPT>() * 32 * 4 * RPT + lane * 4 * RPT);
 
     // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
     auto finish_lists = [&](uint64_t wlu, uint64_t wll) {
@@ -916,7 +918,19 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             const int64_t lr = row - a.rank_row0[o];
             if constexpr (!CSR) {
                 const float* src = a.peer_XR[o] + lr * a.d;
-                for (int k = lane; k < d; k += 32) sXW[k * SVM_WS + r] = __ldg(src + k);
+                for (int k0 = 0; k0 < d; k0 += 8 * 32) {  // 8 loads in flight per lane
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = k0 + u * 32 + lane;
+                        v[u] = k < d ? __ldg(src + k) : 0.0f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = k0 + u * 32 + lane;
+                        if (k < d) sXW[k * SVM_WS + r] = v[u];
+                    }
+                }
             } else {
                 const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
                 for (int64_t p = b + lane; p < e; p += 32)
@@ -997,25 +1011,31 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 
         uint64_t wlu = 0, wll = 0;  // this warp's running top-8 lists (exact, per chunk)
         const int nbuf = dbuf_rows / rows_per_chunk < nchunks ? dbuf_rows / rows_per_chunk : nchunks;
+        // feature slicing (wide d, streamed X): every (chunk, slice) item is buffered in phase A
+        const int nsl = a.nslice > 1 ? a.nslice : 1;
+        const int ks = nsl > 1 ? (d + nsl - 1) / nsl : d;
+        const int nitems = nsl > 1 ? nchunks * nsl : nbuf;
         // ---- phase A: dot products x_i . X_W of the buffered chunks into shared memory --------
         auto phase_a = [&]() {
             for (;;) {
                 // chunks are buffered only while the subproblem runs: once it is solved the rest
                 // are cheaper fused with their epilogue in phase B (no tail of buffered work)
-                int ch = nbuf;
-                if (lane == 0 && !*reinterpret_cast<volatile int32_t*>(&sh.sub_done))
-                    ch = atomicAdd(&sh.next_chunk, 1);
-                ch = __shfl_sync(FULL, ch, 0);
-                if (ch >= nbuf) break;
+                int it = nitems;
+                if (lane == 0 && (nsl > 1 || !*reinterpret_cast<volatile int32_t*>(&sh.sub_done)))
+                    it = atomicAdd(&sh.next_chunk, 1);
+                it = __shfl_sync(FULL, it, 0);
+                if (it >= nitems) break;
+                const int ch = nsl > 1 ? it / nsl : it, sl = nsl > 1 ? it - ch * nsl : 0;
+                const int k0 = sl * ks, kn = min(d, k0 + ks) - k0;
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
-                else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
-                else dots_dense_async<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, xring, acc);
+                else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, acc);
+                else dots_dense_async<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, xring, acc);
                 const int lr = (int)(li0 - cta_begin);
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {
-                    float* dst = sDot + (size_t)r * dbuf_rows + lr;
+                    float* dst = sDot + (size_t)(sl * SVM_WS + r) * dbuf_rows + lr;
                     if constexpr (RPT == 4) *reinterpret_cast<float4*>(dst) = make_float4(acc[0][r], acc[1][r], acc[2][r], acc[3][r]);
                     else if constexpr (RPT == 2) *reinterpret_cast<float2*>(dst) = make_float2(acc[0][r], acc[1][r]);
                     else *dst = acc[0][r];
@@ -1070,7 +1090,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         // ---- phase B / a3: epilogue of every chunk (buffered dots, or computed now) ----------
         // chunks [0, nA) have buffered dots; the streamed ones [nA, nchunks) are handed out
         // first so that their X reads start together and no streamed chunk forms the tail
-        const int nA = sh.next_chunk < nbuf ? sh.next_chunk : nbuf;
+        const int nA = nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf);
         const int nS = nchunks - nA;
         for (;;) {
             int t = 0;
@@ -1094,6 +1114,13 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     } else {
                         acc[0][r] = *src;
                     }
+                }
+                for (int q = 1; q < nsl; ++q) {   // slice partials, added in slice order
+#pragma unroll
+                    for (int r = 0; r < SVM_WS; ++r)
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j)
+                            acc[j][r] += sDot[(size_t)(q * SVM_WS + r) * dbuf_rows + lr + j];
                 }
             } else if constexpr (CSR) {
                 dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
@@ -1155,7 +1182,7 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
 
 }  // namespace
 
-int smo_ring_bytes(int rpt) { return SMO_THREADS * PF_X * 4 * rpt; }
+int smo_ring_bytes(int rpt) { return SMO_THREADS * 4 * rpt * (rpt == 1 ? pf_x<1>() : rpt == 2 ? pf_x<2>() : pf_x<4>()); }
 int smo_csr_stage_bytes() { return SMO_WARPS * CSR_CAP * 6; }
 int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS)); }
 

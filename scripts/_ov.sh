@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -q -x -m gpu 2>&1 | tail -2
-python scripts/prof_train.py c2 0; python scripts/prof_train.py c4 8000; python scripts/prof_c3.py
+for nb in 148 128 112 100; do echo "NBLK=$nb"; SVMB200_NBLK=$nb python scripts/prof_train.py c2 0; done

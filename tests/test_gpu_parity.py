@@ -443,3 +443,26 @@ def test_tiny_problems(n):
     assert abs(m.info.dual_objective - r.results[0]["dual"]) <= 1e-6 * max(1.0, abs(r.results[0]["dual"]))
     np.testing.assert_allclose(m.predict(X, decision=True)[1][:, 0], r.decision_function(X)[:, 0],
                                atol=1e-4)
+
+
+@pytest.mark.parametrize("nslice", ["1", "auto"])
+def test_wide_rows_streamed_sliced(nslice):
+    """d = 784 (c3's MNIST shape): X streamed from HBM, features split into slices whose partial
+    dot products are summed in slice order; same solution as the oracle either way."""
+    import os
+    ds = synth.make("c3", n=1500)
+    y = np.where(ds.y == ds.y[0], 1.0, -1.0).astype(np.float32)
+    if nslice != "auto":
+        os.environ["SVMB200_NSLICE"] = nslice
+    try:
+        m = pkg.train(ds.X, y, gamma=1.0 / ds.d)
+    finally:
+        os.environ.pop("SVMB200_NSLICE", None)
+    om = ora.train(ds.X, y, gamma=1.0 / ds.d)
+    r = om.results[0]
+    assert m.info.converged == 1
+    assert abs(m.info.dual_objective - r["dual"]) <= 1e-4 * abs(r["dual"])
+    Xh = synth.make("c3", n=300, heldout=True).X
+    f_gpu = m.predict(Xh, decision=True)[1][:, 0]
+    f_ora = om.decision_function(Xh)[:, 0]
+    assert np.abs(f_gpu - f_ora).max() <= 1e-3
