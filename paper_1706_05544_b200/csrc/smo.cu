@@ -366,53 +366,71 @@ __device__ __forceinline__ void sort_desc(uint64_t (&k)[NK])
 }
 
 // Merge one chunk's candidate keys (NK per lane) into the warp's running top-8 lists (lane l < 8
-// holds the l-th best; 0 = empty), up and low together.  Each lane sorts its keys once; every
-// extraction round takes the 64-bit warp max of the lanes' heads (own list entry vs sorted
-// chunk keys) and the winning lane pops its head -- no rescans.  A side with no key above the
-// current 8th is skipped.  Keys are unique, so the result is exact.
+// holds the l-th best, descending; 0 = empty), up and low together.  Only keys above the current
+// 8th can enter: their warp-wide count (capped at 8) bounds the rounds.  Each lane sorts its keys
+// once; a round takes the 64-bit warp max of the lanes' heads and inserts it into the list at
+// rank popc(ballot(list > key)) (entries below shift down one lane); the winning lane pops its
+// head.  Keys are unique, so the result is exact.
 template <int NK>
 __device__ __forceinline__ void merge_chunk(uint64_t (&ku)[NK], uint64_t (&kl)[NK], uint64_t& wlu,
                                             uint64_t& wll, int lane)
 {
     const uint64_t thu = __shfl_sync(FULL, wlu, 7), thl = __shfl_sync(FULL, wll, 7);
-    bool au = false, alo = false;
+    uint32_t cu = 0, cl = 0;
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
-        au |= ku[k] > thu;
-        alo |= kl[k] > thl;
+        cu += ku[k] > thu ? 1u : 0u;
+        cl += kl[k] > thl ? 1u : 0u;
     }
-    const bool doU = __any_sync(FULL, au), doL = __any_sync(FULL, alo);
-    if (!doU && !doL) return;
-    if (doU) sort_desc<NK>(ku);
-    if (doL) sort_desc<NK>(kl);
-    uint64_t ou = lane < 8 ? wlu : 0ull, ol = lane < 8 ? wll : 0ull;
-    uint64_t nu = 0ull, nl = 0ull;
+    int ru = (int)min(__reduce_add_sync(FULL, cu), 8u);
+    int rl = (int)min(__reduce_add_sync(FULL, cl), 8u);
+    if (ru == 0 && rl == 0) return;
+    if (ru) sort_desc<NK>(ku);
+    if (rl) sort_desc<NK>(kl);
+    const int rounds = ru > rl ? ru : rl;
 #pragma unroll 1
-    for (int r = 0; r < 8; ++r) {
-        const uint64_t hu = doU ? (ku[0] > ou ? ku[0] : ou) : 0ull;
-        const uint64_t hl = doL ? (kl[0] > ol ? kl[0] : ol) : 0ull;
+    for (int r = 0; r < rounds; ++r) {
+        const bool du = r < ru, dl = r < rl;   // warp-uniform
+        const uint64_t hu = du ? ku[0] : 0ull, hl = dl ? kl[0] : 0ull;
         const uint64_t bu = warp_max_u64(hu);
         const uint64_t bl = warp_max_u64(hl);
-        if (lane == r) { nu = bu; nl = bl; }
-        if (bu != 0ull && hu == bu) {
-            if (ou == bu) ou = 0ull;
-            else {
+        const uint64_t pu = __shfl_up_sync(FULL, wlu, 1), pl = __shfl_up_sync(FULL, wll, 1);
+        const int posu = __popc(__ballot_sync(FULL, lane < 8 && wlu > bu));
+        const int posl = __popc(__ballot_sync(FULL, lane < 8 && wll > bl));
+        if (du && bu != 0ull && posu < 8) {
+            if (lane == posu) wlu = bu;
+            else if (lane > posu && lane < 8) wlu = pu;
+            if (hu == bu) {
 #pragma unroll
                 for (int q = 0; q + 1 < NK; ++q) ku[q] = ku[q + 1];
                 ku[NK - 1] = 0ull;
             }
-        }
-        if (bl != 0ull && hl == bl) {
-            if (ol == bl) ol = 0ull;
-            else {
+        } else ru = 0;      // nothing left above the 8th on this side
+        if (dl && bl != 0ull && posl < 8) {
+            if (lane == posl) wll = bl;
+            else if (lane > posl && lane < 8) wll = pl;
+            if (hl == bl) {
 #pragma unroll
                 for (int q = 0; q + 1 < NK; ++q) kl[q] = kl[q + 1];
                 kl[NK - 1] = 0ull;
             }
-        }
+        } else rl = 0;
     }
-    if (doU) wlu = nu;
-    if (doL) wll = nl;
+}
+
+// One copy per row (C-SVC): only the even key slots are used, so merge RPT keys per lane.
+template <int RPT>
+__device__ __forceinline__ void merge_chunk_rows(uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT],
+                                                 uint64_t& wlu, uint64_t& wll, int lane, int ncopy)
+{
+    if (ncopy == 1) {
+        uint64_t cu[RPT], cl[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) { cu[j] = ku[2 * j]; cl[j] = kl[2 * j]; }
+        merge_chunk<RPT>(cu, cl, wlu, wll, lane);
+    } else {
+        merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
+    }
 }
 
 // Explicit shared-memory 64-bit load for the list merges.  With plain indexed loads
@@ -699,7 +717,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             uint64_t ku[2 * RPT], kl[2 * RPT];
             row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, false, acc, ku, kl);
-            merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
+            merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
         }
         finish_lists(wlu, wll);
     };
@@ -941,6 +959,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
         __syncthreads();
         mark(2);
+        wmark(-1);
         // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
         {
             const int npairs = nr * (nr + 1) / 2;
@@ -982,6 +1001,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 sh.qpart[p * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
             }
             __syncthreads();
+            wmark(6);
             if (tid < npairs) {
                 int r = 0, rem = tid;
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
@@ -993,6 +1013,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 sh.kr[sidx * SVM_WS + r] = kv;
             }
             __syncthreads();
+            wmark(7);
             if (tid < SVM_WS * SVM_WS) {
                 const int pa = tid >> 4, pb = tid & 15;
                 double kab = 0.0, ie = 0.0;
@@ -1133,7 +1154,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             uint64_t ku[2 * RPT], kl[2 * RPT];
             row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, true, acc, ku, kl);
             wmark(2);
-            merge_chunk<2 * RPT>(ku, kl, wlu, wll, lane);
+            merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             wmark(3);
         }
         wmark(4);

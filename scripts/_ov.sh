@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for nb in 148 128 112 100; do echo "NBLK=$nb"; SVMB200_NBLK=$nb python scripts/prof_train.py c2 0; done
+python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -2
+python scripts/e2e_margins.py
+python scripts/prof_train.py c2 0; python scripts/prof_train.py c4 8000; python scripts/prof_c3.py
