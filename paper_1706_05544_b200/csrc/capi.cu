@@ -501,6 +501,21 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
                (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
     }
+    if (!a.x_in_smem && !D.csr && D.d >= 256 && a.rpt == 1 && D.rows_per_cta <= 14 * 32 &&
+        !getenv("SVMB200_NO_WIDE")) {
+        // wide streamed rows: CTA-wide bulk-copy pipeline (8 stages of wide_kc features x Rs
+        // rows, Rs = 8 mod 32) feeding one-row-per-lane dot products held in registers
+        const int64_t ncw = (D.rows_per_cta + 31) / 32, Rs = ncw * 32 + 8;
+        const int base = smo_smem_bytes(D.d, a.world, D.nblk, 0);
+        int64_t kc = std::min<int64_t>(16, (210 * 1024 - base) / (8 * 4 * Rs));
+        if (kc < 4) kc = 0;
+        if (kc > 0) {
+            a.wide = 1;
+            a.wide_kc = (int32_t)kc;
+            a.x_ring = 0;
+            smem = base + (int)(8 * 4 * kc * Rs);
+        }
+    }
     if (smem > 220 * 1024)
         return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d lists)", smem,
                     (long long)D.d, a.world * D.nblk);
@@ -511,7 +526,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         int64_t rows = avail / 64;
         rows = std::min<int64_t>(rows, all_rows);
         rows = rows / chunk * chunk;
-        if (getenv("SVMB200_NO_DBUF")) rows = 0;
+        if (getenv("SVMB200_NO_DBUF") || a.wide) rows = 0;
         a.nslice = 1;
         if (!a.x_in_smem && !D.csr && D.d >= 256 && rows == all_rows) {
             // feature slices: as many as the partial buffers allow, >= 64 features each, aiming

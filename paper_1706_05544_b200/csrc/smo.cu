@@ -99,6 +99,32 @@ __device__ __forceinline__ void zero_acc(float (&acc)[RPT][SVM_WS])
 // Dense kernel-row dot products acc[j][r] = x_{li+j} . x_{W_r} for RPT consecutive rows.  X^T is
 // feature-major with row stride `ld` (global [d][n_pad], or the CTA's slice staged in shared
 // memory); X_W^T is [d][16] in shared memory, read with 4 broadcast LDS.128 per feature.
+// acc[0..15] += x * w[0..15] as eight packed FFMA2 (sm_100): each lane of the pair rounds exactly
+// like fmaf, so the result is bit-identical to sixteen scalar FMAs at half the issue slots.
+__device__ __forceinline__ void fma_row16_scalar(float x, const float4 (&wv)[4], float* acc)
+{
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        acc[4 * q + 0] = fmaf(x, wv[q].x, acc[4 * q + 0]);
+        acc[4 * q + 1] = fmaf(x, wv[q].y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(x, wv[q].z, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(x, wv[q].w, acc[4 * q + 3]);
+    }
+}
+__device__ __forceinline__ void fma_row16(float x, const float4 (&wv)[4], float* acc)
+{
+    const float2 xx = make_float2(x, x);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float2 lo = __ffma2_rn(xx, make_float2(wv[q].x, wv[q].y), make_float2(acc[4 * q], acc[4 * q + 1]));
+        const float2 hi = __ffma2_rn(xx, make_float2(wv[q].z, wv[q].w), make_float2(acc[4 * q + 2], acc[4 * q + 3]));
+        acc[4 * q] = lo.x;
+        acc[4 * q + 1] = lo.y;
+        acc[4 * q + 2] = hi.x;
+        acc[4 * q + 3] = hi.y;
+    }
+}
+
 template <int RPT>
 __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64_t ld, int d,
                                            bool active, const float* sXW,
@@ -124,13 +150,8 @@ __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64
         float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc[j][4 * q + 0] = fmaf(x[j], wv[q].x, acc[j][4 * q + 0]);
-                acc[j][4 * q + 1] = fmaf(x[j], wv[q].y, acc[j][4 * q + 1]);
-                acc[j][4 * q + 2] = fmaf(x[j], wv[q].z, acc[j][4 * q + 2]);
-                acc[j][4 * q + 3] = fmaf(x[j], wv[q].w, acc[j][4 * q + 3]);
-            }
+            if constexpr (RPT == 4) fma_row16_scalar(x[j], wv, acc[j]);   // pairs would spill
+            else fma_row16(x[j], wv, acc[j]);
         }
     }
 }
@@ -190,13 +211,8 @@ __device__ __forceinline__ void dots_dense_async(const float* __restrict__ xcol,
         float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc[j][4 * q + 0] = fmaf(x[j], wv[q].x, acc[j][4 * q + 0]);
-                acc[j][4 * q + 1] = fmaf(x[j], wv[q].y, acc[j][4 * q + 1]);
-                acc[j][4 * q + 2] = fmaf(x[j], wv[q].z, acc[j][4 * q + 2]);
-                acc[j][4 * q + 3] = fmaf(x[j], wv[q].w, acc[j][4 * q + 3]);
-            }
+            if constexpr (RPT == 4) fma_row16_scalar(x[j], wv, acc[j]);   // pairs would spill
+            else fma_row16(x[j], wv, acc[j]);
         }
         // refill the slot just consumed with feature k + PF_X
         if (k + PF_X < d) cp_async_x<RPT>(sa, xcol + (int64_t)(k + PF_X) * ld);
@@ -219,13 +235,7 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
         int k = __ldg(indices + p);
         float v = __ldg(vals + p);
         float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            acc[0][4 * q + 0] = fmaf(v, wv[q].x, acc[0][4 * q + 0]);
-            acc[0][4 * q + 1] = fmaf(v, wv[q].y, acc[0][4 * q + 1]);
-            acc[0][4 * q + 2] = fmaf(v, wv[q].z, acc[0][4 * q + 2]);
-            acc[0][4 * q + 3] = fmaf(v, wv[q].w, acc[0][4 * q + 3]);
-        }
+        fma_row16(v, wv, acc[0]);
     }
 }
 
@@ -264,13 +274,7 @@ __device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indp
             const int k = st_idx[p - z0];
             const float v = st_val[p - z0];
             const float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                acc[0][4 * q + 0] = fmaf(v, wv[q].x, acc[0][4 * q + 0]);
-                acc[0][4 * q + 1] = fmaf(v, wv[q].y, acc[0][4 * q + 1]);
-                acc[0][4 * q + 2] = fmaf(v, wv[q].z, acc[0][4 * q + 2]);
-                acc[0][4 * q + 3] = fmaf(v, wv[q].w, acc[0][4 * q + 3]);
-            }
+            fma_row16(v, wv, acc[0]);
         }
     }
     __syncwarp();
@@ -296,6 +300,7 @@ struct SmoShared {
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
     float xn[SVM_WS];                    // |x_r|^2 of the distinct rows
     int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
+    alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode pipeline barriers
     double m_up, M_low;
 };
 
@@ -613,6 +618,52 @@ __device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C,
     return step;
 }
 
+// ---- wide-mode pipeline primitives (mbarrier + bulk async copy, sm_90+ PTX) -----------------
+constexpr int WIDE_STAGES = 8;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ uint64_t gtimer_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity)
+{
+    uint32_t ok = 0;
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+        if (ok) return;
+        if (++spins == 1024) {   // watchdog: a lost stage must fail the launch, not hang the GPU
+            spins = 0;
+            const uint64_t now = gtimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();
+        }
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 template <bool CSR, int RPT, bool XS, bool RBFK>
 __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a)
 {
@@ -664,6 +715,40 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     // per-lane cp.async ring for streamed X (in the place of the resident slice)
     const uint32_t xring = (uint32_t)__cvta_generic_to_shared(sX) +
                            (uint32_t)(warp * pf_x<RPT>() * 32 * 4 * RPT + lane * 4 * RPT);
+
+    // ---- wide mode (streamed dense rows, large d): CTA-wide bulk-copy pipeline --------------
+    // Stage T of the run holds features [kc (T % nst), +kc) of the CTA's R rows ([kc][R] fp32,
+    // one contiguous R * 4 B copy per feature) in slot T % 8; the producer (lane 0 of warp ncw)
+    // runs 8 stages ahead of the consumer warps, across iteration boundaries (X does not depend
+    // on W), so the next iteration's first stages load during this one's epilogue and exchange.
+    constexpr bool WIDE_OK = !CSR && !XS && RPT == 1;   // compiled out elsewhere (registers)
+    const bool wide = WIDE_OK && a.wide != 0;
+    const int wkc = a.wide_kc > 0 ? a.wide_kc : 8;
+    const int nst = (d + wkc - 1) / wkc;
+    const int ncw = (R + 31) / 32;                        // consumer warps, 32 rows each
+    const int Rs = ncw * 32 + 8;                          // stage row stride: = 8 mod 32 floats
+    float* wring = sX;                                    // [8][wkc][Rs]
+    auto wide_issue = [&](uint64_t T) {
+        const int s = (int)(T % WIDE_STAGES);
+        const int k0 = (int)(T % (uint64_t)nst) * wkc, kn = min(wkc, d - k0);
+        mbar_arrive_tx(&sh.mb_full[s], (uint32_t)(kn * R * 4));
+        float* dst = wring + (size_t)s * wkc * Rs;
+        for (int q = 0; q < kn; ++q)
+            bulk_g2s(dst + (size_t)q * Rs, a.XT + (int64_t)(k0 + q) * a.n_pad + cta_begin,
+                     (uint32_t)(R * 4), &sh.mb_full[s]);
+    };
+    if (wide) {
+        if (tid == 0) {
+            for (int s = 0; s < WIDE_STAGES; ++s) {
+                mbar_init(&sh.mb_full[s], 1);
+                mbar_init(&sh.mb_empty[s], (uint32_t)ncw);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (warp == ncw && lane == 0)
+            for (int T = 0; T < WIDE_STAGES; ++T) wide_issue((uint64_t)T);
+    }
 
     // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
     auto finish_lists = [&](uint64_t wlu, uint64_t wll) {
@@ -809,6 +894,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         mark(0);
         if (sh.timeout) {
             if (reporter && tid == 0) a.info->error = 1;
+            if (wide && warp == ncw && lane == 0)   // no bulk copy may outlive the CTA
+                for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
+                    mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
             return;
         }
         // ---- a1 (2/2): global merge (warp 0: I_up top-8, warp 1: I_low top-8) ----------------
@@ -891,6 +979,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         __syncthreads();
         mark(1);
         if (sh.stop) {
+            if (wide && warp == ncw && lane == 0)   // no bulk copy may outlive the CTA
+                for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
+                    mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
             if (reporter && tid == 0) {
                 a.info->iterations = t;
                 a.info->m_up = sh.m_up;
@@ -1101,6 +1192,49 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
             mark(4);
         }
+        if (wide) {
+            // ---- a3 in wide mode: consumer warps stream every feature stage through registers,
+            // then (after the subproblem) the epilogue of their own rows -------------------------
+            float acc[RPT][SVM_WS];
+            const int lr = warp * 32 + lane;   // this lane's local row
+            if (warp < ncw) {
+                zero_acc<RPT>(acc);
+                const uint64_t Tb = (uint64_t)t * nst;
+                wmark(-1);
+                for (int j = 0; j < nst; ++j) {
+                    const uint64_t T = Tb + j;
+                    const int s = (int)(T % WIDE_STAGES);
+                    mbar_wait(&sh.mb_full[s], (uint32_t)((T / WIDE_STAGES) & 1));
+                    wmark(0);
+                    const float* st = wring + (size_t)s * wkc * Rs + lr;
+                    const int k0 = j * wkc, kn = min(wkc, d - k0);
+                    const float4* w4 = reinterpret_cast<const float4*>(sXW + k0 * SVM_WS);
+#pragma unroll 4
+                    for (int q = 0; q < kn; ++q) {
+                        const float4 wv[4] = {w4[4 * q], w4[4 * q + 1], w4[4 * q + 2], w4[4 * q + 3]};
+                        fma_row16(st[(size_t)q * Rs], wv, acc[0]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sh.mb_empty[s]);
+                    wmark(1);
+                }
+            } else if (warp == ncw && lane == 0) {
+                const uint64_t Tb = (uint64_t)t * nst + WIDE_STAGES;
+                for (int j = 0; j < nst; ++j) {
+                    const uint64_t T = Tb + j;
+                    mbar_wait(&sh.mb_empty[T % WIDE_STAGES], (uint32_t)(((T / WIDE_STAGES) - 1) & 1));
+                    wide_issue(T);
+                }
+            }
+            __syncthreads();
+            mark(5);
+            wmark(-1);
+            if (warp < ncw) {
+                uint64_t ku[2 * RPT], kl[2 * RPT];
+                row_epilogue<RPT, RBFK>(a, sh, cta_begin + lr, cta_end, true, acc, ku, kl);
+                merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
+            }
+        } else {
         // overlap == 2 (default): the warps sharing the solver's SM sub-partition (warp % 4 == 3) leave
         // its issue slots to the subproblem and join phase A when it is solved
         if (a.overlap == 2 && (warp & 3) == (SOLVER_WARP & 3)) named_bar_sync(1, 32 * (SMO_WARPS / 4));
@@ -1157,6 +1291,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             wmark(3);
         }
+        }   // !wide
         wmark(4);
         finish_lists(wlu, wll);
         mark(6);

@@ -157,6 +157,9 @@ struct SmoArgs {
     int32_t x_in_smem;        // 1: this CTA's slice of X^T is staged once into shared memory
     int32_t overlap;          // 2: solver's sub-partition warps defer phase A; 1: all warps
     int32_t dbuf_rows;        // rows whose 16 dot products are buffered in shared memory
+    int32_t wide;             // 1: CTA-wide bulk-copy pipeline for wide streamed rows (one row
+                              //    block per consumer warp, dots in registers across all features)
+    int32_t wide_kc;          //    features per pipeline stage (8 stages)
     int32_t nslice;           // > 1: phase A splits the features of each chunk into nslice items
                               //      (partials [nslice][16][dbuf_rows], summed in slice order)
     int32_t x_ring;           // streamed X through a per-lane cp.async ring (RPT >= 2)
