@@ -37,7 +37,15 @@ sys.path.insert(0, ROOT)
 METRIC = "train time to KKT tol & fused kernel-row GB/s vs HBM peak; predict rows/s"
 # iterations to KKT tol of each workload on this path (B200 runs of this round; the oracle runs
 # the same algorithm in fp64): used only to project the oracle's bounded sample to the metric.
-ITERS_TO_TOL = {"c1": 296, "c2": 19291, "c4": 70000}
+ROOF_NOTES = {
+    "c1": "2,000 rows on 8 CTAs: launch/serial latency bound; see DESIGN.md",
+    "c2": "X is SMEM-resident for c2 (135 KB per CTA): the per-iteration chain (exchange, merge, "
+          "fp64 subproblem) bounds it, not HBM; see DESIGN.md",
+    "c3": "wide mode: X (188 MB > L2) streamed once per iteration through a cp.async.bulk + "
+          "mbarrier ring; traffic = ncu DRAM bytes per iteration x iterations; see DESIGN.md",
+    "c4": "X (108 MB) streamed from HBM/L2 through per-lane cp.async rings; see DESIGN.md",
+}
+ITERS_TO_TOL = {"c1": 296, "c2": 19291, "c3": 10616, "c4": 70000}
 WORKLOADS = {
     "c1": "binary C-SVC, RBF, two Gaussian blobs, n=2,000 d=20 dense",
     "c2": "eps-SVR, RBF, Friedman #1, n=50,000 d=100 dense (m=100,000 duals)",
@@ -278,14 +286,17 @@ def main():
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        if "dram_bytes_per_launch" in tj:
+            traffic = tj["dram_bytes_per_launch"]
+        elif "dram_bytes_per_iter" in tj:   # streamed X: traffic scales with the iterations
+            traffic = tj["dram_bytes_per_iter"] * info.iterations
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "algorithmic_bytes_per_launch": bpi * info.iterations,
                 "kernel": "smo_persistent (a1+a2+a3 fused, one cooperative launch per training)",
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
-                "note": "X is SMEM-resident for c2 (135 KB per CTA): the per-iteration chain "
-                        "(exchange, merge, fp64 subproblem) bounds it, not HBM; see DESIGN.md"}
+                "note": ROOF_NOTES.get(args.config, "")}
     # ---- e2e: pinned host buffers through the C ABI ------------------------------------------
     e2e = None
     if not args.no_e2e:
