@@ -11,6 +11,7 @@
 #include "layout.cuh"
 
 #include <math.h>
+#include <cstdlib>
 
 namespace {
 
@@ -182,6 +183,163 @@ __global__ void k_finalize(const double* __restrict__ F, int64_t nq, int n_out,
     else out[q] = (float)labels[arg];
 }
 
+// ---- tcgen05 3xTF32 variant (d <= 128): D[128 queries x 64 SVs] in TMEM ----------------------
+// Operands K-major in shared memory, SWIZZLE_NONE canonical layout: core matrix = 8 rows x 4
+// consecutive k (16 B per row, 128 B), at ((row / 8) * KC + k / 4) * 128 B with KC = dp / 4; the
+// descriptor's LBO (next k chunk) = 128 B, SBO (next 8-row group) = KC * 128 B.  kind::tf32 reads
+// the top 19 bits of each fp32 operand (truncation, measured with scripts/tc_probe.cu), so each
+// operand is split x = hi + lo with hi = rna_tf32(x), lo = x - hi (exact, |lo| <= 2^-11 |x|) and
+// x.w = lo.lo + lo.hi + hi.lo + hi.hi: four MMAs per k-step, fp32 accumulation in TMEM (the
+// truncation of lo costs ~2^-21 relative per product).  One query per thread = one TMEM lane, so the
+// epilogue (kernel value, coefficient contraction) needs no cross-thread reduction.
+constexpr int TQ = 128, TS = 64;
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t sbo)
+{
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128u >> 4) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// x = hi + lo with hi = rna_tf32(x) (|lo| <= 2^-11 |x|, exact in fp32)
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo)
+{
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
+    lo = x - hi;
+}
+__device__ __forceinline__ int kmaj_off(int r, int k, int KC) { return ((r >> 3) * KC + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3); }
+
+template <int NOUT>
+__global__ void __launch_bounds__(TQ, 1)
+    k_decision_tc(const float* __restrict__ XqT, const float* __restrict__ qnorm, int64_t nq,
+                  int64_t nq_pad, const float* __restrict__ SVT, const float* __restrict__ svnorm,
+                  int64_t nsv_pad, int d, int dp, const double* __restrict__ coef, int n_out,
+                  KParams kp, int tiles_per_split, double* __restrict__ Fpart)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* Ah = reinterpret_cast<float*>(smem_raw);
+    float* Al = Ah + TQ * dp;
+    float* Bh = Al + TQ * dp;
+    float* Bl = Bh + TS * dp;
+    float* sSn = Bl + TS * dp;
+    float* sCoef = sSn + TS;                                   // [NOUT][TS]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sCoef + NOUT * TS);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(mbar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int KC = dp >> 2;
+    const int64_t q0 = (int64_t)blockIdx.x * TQ;
+    const int64_t n_tiles = nsv_pad / TS;
+    const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
+    const int64_t t_end = min(t_begin + tiles_per_split, n_tiles);
+
+    // the CTA's 128 queries, resident for all SV tiles (hi and lo parts)
+    for (int e = tid; e < dp * TQ; e += TQ) {
+        const int k = e / TQ, r = e - k * TQ;
+        const float x = k < d ? XqT[(int64_t)k * nq_pad + q0 + r] : 0.0f;
+        float hi, lo;
+        tf32_split(x, hi, lo);
+        Ah[kmaj_off(r, k, KC)] = hi;
+        Al[kmaj_off(r, k, KC)] = lo;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(TS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(mbar)), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_holder;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TS >> 3) << 17) |
+                           ((uint32_t)(TQ >> 4) << 24);   // F32 accum, TF32 A/B, K-major, M128 N64
+    const float qn = qnorm[q0 + tid];
+    double facc[NOUT];
+#pragma unroll
+    for (int p = 0; p < NOUT; ++p) facc[p] = 0.0;
+    uint32_t phase = 0;
+    for (int64_t t = t_begin; t < t_end; ++t) {
+        const int64_t s0 = t * TS;
+        for (int e = tid; e < dp * TS; e += TQ) {
+            const int k = e / TS, r = e - k * TS;
+            const float x = k < d ? SVT[(int64_t)k * nsv_pad + s0 + r] : 0.0f;
+            float hi, lo;
+            tf32_split(x, hi, lo);
+            Bh[kmaj_off(r, k, KC)] = hi;
+            Bl[kmaj_off(r, k, KC)] = lo;
+        }
+        if (tid < TS) sSn[tid] = svnorm[s0 + tid];
+        for (int i = tid; i < n_out * TS; i += TQ) {
+            const int p = i / TS, sI = i - p * TS;
+            sCoef[p * TS + sI] = (float)coef[(int64_t)p * nsv_pad + s0 + sI];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 0) {
+            const uint32_t sbo = (uint32_t)KC * 128u;
+            const uint32_t ah = su32(Ah), al = su32(Al), bh = su32(Bh), bl = su32(Bl);
+            for (int ks = 0; ks < (dp >> 3); ++ks)
+#pragma unroll
+                for (int ps = 0; ps < 4; ++ps) {   // lo.lo, lo.hi, hi.lo, then hi.hi
+                    const uint64_t da = umma_desc_kmajor((ps <= 1 ? al : ah) + ks * 256, sbo);
+                    const uint64_t db = umma_desc_kmajor((ps == 0 || ps == 2 ? bl : bh) + ks * 256, sbo);
+                    const uint32_t acc = (ks > 0 || ps > 0) ? 1u : 0u;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                                 ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mbar)) : "memory");
+        }
+        {
+            uint32_t ok = 0, spins = 0;
+            uint64_t t0 = 0;
+            for (;;) {
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(ok) : "r"(su32(mbar)), "r"(phase) : "memory");
+                if (ok) break;
+                if (++spins == 1024) {   // watchdog: a lost commit must fail the launch, not hang the GPU
+                    spins = 0;
+                    uint64_t now;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    if (t0 == 0) t0 = now;
+                    else if (now - t0 > 5000000000ull) __trap();
+                }
+            }
+            phase ^= 1u;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t v[TS];
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+#define TC_LD16(o) asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+    : "=r"(v[o+0]), "=r"(v[o+1]), "=r"(v[o+2]), "=r"(v[o+3]), "=r"(v[o+4]), "=r"(v[o+5]), "=r"(v[o+6]), "=r"(v[o+7]), \
+      "=r"(v[o+8]), "=r"(v[o+9]), "=r"(v[o+10]), "=r"(v[o+11]), "=r"(v[o+12]), "=r"(v[o+13]), "=r"(v[o+14]), "=r"(v[o+15]) : "r"(ta + o))
+        TC_LD16(0); TC_LD16(16); TC_LD16(32); TC_LD16(48);
+#undef TC_LD16
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int p = 0; p < NOUT; ++p) {
+            if (p < n_out) {
+                float part = 0.0f;
+#pragma unroll
+                for (int sI = 0; sI < TS; ++sI)
+                    part = fmaf(sCoef[p * TS + sI], kernel_from_dot(kp, __uint_as_float(v[sI]), qn, sSn[sI]), part);
+                facc[p] += (double)part;
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();   // B, the norms / coefficients and D are reused by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (q0 + tid < nq)
+        for (int p = 0; p < n_out; ++p) Fpart[((int64_t)blockIdx.y * nq + q0 + tid) * n_out + p] = facc[p];
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TS));
+}
+
 constexpr int decision_smem(int nout)
 {
     return 2 * BK * (BQ + BS) * 4 + BQ * (BS + 1) * 4 + nout * BS * 4 + (BQ + BS) * 4;
@@ -199,7 +357,9 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
 {
     (void)nsv;
     if (nq <= 0) return cudaSuccess;
-    int64_t q_tiles = nq_pad / BQ, s_tiles = nsv_pad / BS;
+    // tcgen05 3xTF32 path for d <= 128 (query tile resident in shared memory)
+    const bool tc = d <= 128 && n_out <= 16 && !getenv("SVMB200_NO_TC") && nq_pad % TQ == 0 && nsv_pad % TS == 0;
+    int64_t q_tiles = nq_pad / (tc ? TQ : BQ), s_tiles = nsv_pad / (tc ? TS : BS);
     if (s_tiles == 0) return cudaMemsetAsync(F, 0, sizeof(double) * nq * n_out, st);
     int64_t want = std::max<int64_t>(1, (4 * 148 + q_tiles - 1) / q_tiles);
     int splits = (int)std::min<int64_t>(want, s_tiles);
@@ -219,6 +379,27 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
         part = g_fpart;
     }
     dim3 grid((unsigned)q_tiles, (unsigned)splits);
+    if (tc) {
+        const int dp = (int)((d + 7) / 8 * 8);
+        auto tc_smem = [&](int nout) { return (int)((2 * TQ * dp + 2 * TS * dp + TS + nout * TS) * 4 + 16); };
+        cudaError_t e;
+        svm_note_launches(1);
+        if (n_out == 1) {
+            cudaFuncSetAttribute(k_decision_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(1));
+            k_decision_tc<1><<<grid, TQ, tc_smem(1), st>>>(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv_pad, (int)d, dp,
+                                                        coef, n_out, kp, tps, part);
+        } else {
+            cudaFuncSetAttribute(k_decision_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(16));
+            k_decision_tc<16><<<grid, TQ, tc_smem(16), st>>>(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv_pad, (int)d, dp,
+                                                          coef, n_out, kp, tps, part);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess || splits == 1) return e;
+        int64_t count = nq * n_out;
+        svm_note_launches(1);
+        k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, splits, count, F);
+        return cudaGetLastError();
+    }
     const int smem1 = decision_smem(1), smem16 = decision_smem(16);
     cudaFuncSetAttribute(k_decision<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
     cudaFuncSetAttribute(k_decision<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
