@@ -689,8 +689,15 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
         qnorm = qn.as<float>();
         ld = nq_pad;
     }
+    DBuf SVtc;
+    const float* svtc = nullptr;
+    if (const int64_t dp = pred_tc_dp(D.d)) {
+        TRY(SVtc.alloc(sizeof(float) * 2 * nsv_pad * dp));
+        CK(pred_sv_tiles(SVT.as<float>(), nsv_pad, D.d, SVtc.as<float>(), st));
+        svtc = SVtc.as<float>();
+    }
     CK(pred_decision(qT, qnorm, D.n, ld, SVT.as<float>(), svn.as<float>(), nsv, nsv_pad, D.d,
-                     coef_sv.as<double>(), 1, kp, F.as<double>(), st));
+                     coef_sv.as<double>(), 1, kp, F.as<double>(), st, svtc));
     return SVM_OK;
 }
 
@@ -791,9 +798,20 @@ struct svm_model {
     KParams kp;
     double first_label = 0;
     DBuf SVT, svnorm, coef, b, labels;  // coef fp64 [n_out][nsv_pad]
+    DBuf SVtc;                          // tcgen05 SV tiles (built on the first predict, d <= 128)
     std::vector<int64_t> sv_index;
     std::vector<double> coef_host;      // [n_out][nsv]
 };
+
+// tcgen05 predict operands: the SVs as [tile][hi | lo][64 * dp] K-major core tiles (d <= 128)
+static int build_sv_tiles(svm_model* M, cudaStream_t st)
+{
+    const int64_t dp = pred_tc_dp(M->d);
+    if (dp == 0 || M->nsv_pad == 0) return SVM_OK;
+    TRY(M->SVtc.alloc(sizeof(float) * 2 * M->nsv_pad * dp));
+    CK(pred_sv_tiles(M->SVT.as<float>(), M->nsv_pad, M->d, M->SVtc.as<float>(), st));
+    return SVM_OK;
+}
 
 static int assemble_model(const Data& D, std::vector<Problem>& probs, const svm_params* prm,
                           svm_model* M, const std::vector<double>& bs, cudaStream_t st)
@@ -811,6 +829,7 @@ static int assemble_model(const Data& D, std::vector<Problem>& probs, const svm_
     M->nsv_pad = std::max<int64_t>(64, (nsv + 63) / 64 * 64);
     M->d = D.d;
     TRY(gather_rows_T(D, idx, nsv, M->nsv_pad, M->SVT, M->svnorm, st));
+    TRY(build_sv_tiles(M, st));
     TRY(M->coef.alloc(sizeof(double) * M->nsv_pad * np));
     for (int p = 0; p < np; ++p)
         CK(lay_gather_coef(coefs[p].as<double>(), idx.as<int64_t>(), nsv, M->nsv_pad,
@@ -1041,7 +1060,7 @@ static int predict_common(const svm_model* M, int64_t nq, const float* Xq_dense,
         CK(lay_norms_XT(QT.as<float>(), m, M->d, cpad, qn.as<float>(), st));
         CK(pred_decision(QT.as<float>(), qn.as<float>(), m, cpad, M->SVT.as<float>(),
                          M->svnorm.as<float>(), M->nsv, M->nsv_pad, M->d, M->coef.as<double>(),
-                         M->n_out, M->kp, F.as<double>(), st));
+                         M->n_out, M->kp, F.as<double>(), st, M->SVtc.p ? M->SVtc.as<float>() : nullptr));
         CK(pred_finalize(F.as<double>(), m, M->n_out, M->b.as<double>(), M->mode,
                          M->labels.as<double>(), M->first_label, ddec.as<float>(),
                          dout.as<float>(), st));
@@ -1657,6 +1676,8 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     M->nsv = nsv;
     M->nsv_pad = nsv_pad;
     M->d = D.d;
+    rc = build_sv_tiles(M, S->st);
+    if (rc != SVM_OK) { delete M; return rc; }
     M->mode = S->mode;
     M->n_out = S->nprob;
     M->kp = probs[0].kp;

@@ -73,7 +73,11 @@ cudaError_t lay_gather_global_sv(const SvPeers& P, int64_t nsv, int64_t nsv_pad,
 cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
                           const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad,
                           int64_t d, const double* coef, int n_out, const KParams& kp,
-                          double* F, cudaStream_t st);
+                          double* F, cudaStream_t st, const float* SVtc = nullptr);
+// tcgen05 predict (d <= 128): SV tiles [nsv_pad / 64][hi | lo][64 * dp] in the K-major core
+// layout (dp = pred_tc_dp(d)); 0 when the tensor-core path does not apply
+int64_t pred_tc_dp(int64_t d);
+cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, float* out, cudaStream_t st);
 // G refresh from raw decision sums (certification, a4): G_c(i) = p_c(i) + y_c * F[i]
 cudaError_t pred_refresh_G(const double* F, const float* yv, const uint8_t* status, int64_t n,
                            int64_t n_pad, int ncopy, double eps, float* G, cudaStream_t st);

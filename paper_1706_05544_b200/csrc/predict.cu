@@ -12,6 +12,7 @@
 
 #include <math.h>
 #include <cstdlib>
+#include <algorithm>
 
 namespace {
 
@@ -340,6 +341,200 @@ __global__ void __launch_bounds__(TQ, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TS));
 }
 
+// ---- pipelined tcgen05 variant: SV tiles pre-laid-out in global memory (K-major core layout,
+// [tile][hi | lo][TS * dp]), one cp.async.bulk per tile into a 2-slot ring; warp 8 lane 0 is the
+// producer and MMA issuer, accumulators double-buffered in TMEM (2 x 64 columns) so tile j's MMAs
+// overlap tile j-1's epilogue; 8 epilogue warps (warp w: TMEM lanes 32 (w % 4) .., columns
+// 32 (w / 4) ..) ---------------------------------------------------------------------------------
+__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0, spins = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+        if (ok) return;
+        if (++spins == 1024) {   // watchdog: a lost stage must fail the launch, not hang the GPU
+            spins = 0;
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();
+        }
+    }
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+constexpr int TP_THREADS = 9 * 32;
+template <int NOUT>
+__global__ void __launch_bounds__(TP_THREADS, 1)
+    k_decision_tcp(const float* __restrict__ XqT, const float* __restrict__ qnorm, int64_t nq,
+                   int64_t nq_pad, const float* __restrict__ SVtc, const float* __restrict__ svnorm,
+                   int64_t nsv_pad, int d, int dp, const double* __restrict__ coef, int n_out,
+                   KParams kp, int tiles_per_split, double* __restrict__ Fpart)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    float* Ah = reinterpret_cast<float*>(smem_raw);
+    float* Al = Ah + TQ * dp;
+    float* Bs = Al + TQ * dp;                                   // [2 slots][hi | lo][TS * dp]
+    float* sSn = Bs + 2 * 2 * TS * dp;                          // [2][TS]
+    double* sCf = reinterpret_cast<double*>(sSn + 2 * TS);     // [2][NOUT][TS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sCf + 2 * NOUT * TS);   // bfull[2] accfull[2] accfree[2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 6);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int KC = dp >> 2;
+    const int64_t q0 = (int64_t)blockIdx.x * TQ;
+    const int64_t n_tiles = nsv_pad / TS;
+    const int64_t t_begin = (int64_t)blockIdx.y * tiles_per_split;
+    const int64_t t_end = min(t_begin + tiles_per_split, n_tiles);
+    const int nt = (int)(t_end - t_begin);
+    const uint32_t tile_bytes = (uint32_t)(2 * TS * dp * 4);
+    const uint32_t b_bfull = su32(bars), b_accfull = su32(bars + 2), b_accfree = su32(bars + 4);
+
+    for (int e = tid; e < dp * TQ; e += TP_THREADS) {   // resident query tile (hi, lo)
+        const int k = e / TQ, r = e - k * TQ;
+        const float x = k < d ? XqT[(int64_t)k * nq_pad + q0 + r] : 0.0f;
+        float hi, lo;
+        tf32_split(x, hi, lo);
+        Ah[kmaj_off(r, k, KC)] = hi;
+        Al[kmaj_off(r, k, KC)] = lo;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(2 * TS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_bfull + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accfull + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accfree + 8 * i), "r"(8));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // query tile -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 8) {
+        if (lane == 0 && nt > 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TS >> 3) << 17) |
+                                   ((uint32_t)(TQ >> 4) << 24);
+            const uint32_t sbo = (uint32_t)KC * 128u;
+            auto issue = [&](int j) {   // tile j -> slot j & 1: B (hi | lo), norms, coefficients
+                const int sl = j & 1;
+                const int64_t t = t_begin + j, s0 = t * TS;
+                const uint32_t bar = b_bfull + 8 * sl;
+                const uint32_t bytes = tile_bytes + TS * 4 + (uint32_t)(n_out * TS * 8);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+                bulk_g2s(su32(Bs + (size_t)sl * 2 * TS * dp), SVtc + (size_t)t * 2 * TS * dp, tile_bytes, bar);
+                bulk_g2s(su32(sSn + sl * TS), svnorm + s0, TS * 4, bar);
+                for (int p = 0; p < n_out; ++p)
+                    bulk_g2s(su32(sCf + ((size_t)sl * NOUT + p) * TS), coef + (int64_t)p * nsv_pad + s0, TS * 8, bar);
+            };
+            issue(0);
+            if (nt > 1) issue(1);
+            for (int j = 0; j < nt; ++j) {
+                const int sl = j & 1;
+                mb_wait(b_bfull + 8 * sl, (uint32_t)((j >> 1) & 1));   // (issue(j) waited for tile j - 2's release)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t bh = su32(Bs + (size_t)sl * 2 * TS * dp), bl = bh + TS * dp * 4;
+                const uint32_t ah = su32(Ah), al = su32(Al);
+                const uint32_t dcol = tmem + (uint32_t)(sl * TS);
+                for (int ks = 0; ks < (dp >> 3); ++ks)
+#pragma unroll
+                    for (int ps = 0; ps < 4; ++ps) {   // lo.lo, lo.hi, hi.lo, then hi.hi
+                        const uint64_t da = umma_desc_kmajor((ps <= 1 ? al : ah) + ks * 256, sbo);
+                        const uint64_t db = umma_desc_kmajor((ps == 0 || ps == 2 ? bl : bh) + ks * 256, sbo);
+                        const uint32_t acc = (ks > 0 || ps > 0) ? 1u : 0u;
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                                     ::"r"(dcol), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                    }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_accfull + 8 * sl) : "memory");
+                // the other slot (tile j - 1) is refilled with tile j + 1 once tile j - 1's epilogue,
+                // which runs while tile j's MMAs execute, has released it
+                if (j >= 1 && j + 1 < nt) {
+                    mb_wait(b_accfree + 8 * (sl ^ 1), (uint32_t)(((j - 1) >> 1) & 1));
+                    issue(j + 1);
+                }
+            }
+        }
+    } else {
+        const int quad = warp & 3, half = warp >> 2;
+        const float qn = qnorm[q0 + quad * 32 + lane];
+        double facc[NOUT];
+#pragma unroll
+        for (int p = 0; p < NOUT; ++p) facc[p] = 0.0;
+        for (int j = 0; j < nt; ++j) {
+            const int sl = j & 1;
+            mb_wait(b_accfull + 8 * sl, (uint32_t)((j >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t v[32];
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * TS + half * 32);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                           "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const float* sn = sSn + sl * TS + half * 32;
+#pragma unroll
+            for (int p = 0; p < NOUT; ++p) {
+                if (p < n_out) {
+                    const double* cf = sCf + ((size_t)sl * NOUT + p) * TS + half * 32;
+                    float part = 0.0f;
+#pragma unroll
+                    for (int sI = 0; sI < 32; ++sI)
+                        part = fmaf((float)cf[sI], kernel_from_dot(kp, __uint_as_float(v[sI]), qn, sn[sI]), part);
+                    facc[p] += (double)part;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b_accfree + 8 * sl) : "memory");
+        }
+        // the two column halves of a query are combined in a fixed order (half 0 + half 1)
+        double* red = reinterpret_cast<double*>(Bs);   // B slots are free once every tile is done
+        __syncthreads();
+        if (half == 1)
+            for (int p = 0; p < n_out; ++p) red[(quad * 32 + lane) * NOUT + p] = facc[p];
+        __syncthreads();
+        if (half == 0 && q0 + quad * 32 + lane < nq)
+            for (int p = 0; p < n_out; ++p)
+                Fpart[((int64_t)blockIdx.y * nq + q0 + quad * 32 + lane) * n_out + p] =
+                    facc[p] + red[(quad * 32 + lane) * NOUT + p];
+    }
+    if (warp == 8) { __syncthreads(); __syncthreads(); }   // match the epilogue warps' barriers
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TS));
+}
+
+// SV tiles for k_decision_tcp: [tile][hi | lo][TS * dp] in the K-major core layout
+__global__ void k_sv_tiles(const float* __restrict__ SVT, int64_t nsv_pad, int d, int dp, float* __restrict__ out)
+{
+    const int64_t total = nsv_pad * dp;
+    const int KC = dp >> 2;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / nsv_pad, s = e - k * nsv_pad;
+        const float x = k < d ? SVT[k * nsv_pad + s] : 0.0f;
+        float hi, lo;
+        tf32_split(x, hi, lo);
+        const int64_t t = s / TS;
+        const int r = (int)(s - t * TS);
+        float* base = out + (size_t)t * 2 * TS * dp;
+        base[kmaj_off(r, (int)k, KC)] = hi;
+        base[TS * dp + kmaj_off(r, (int)k, KC)] = lo;
+    }
+}
+
 constexpr int decision_smem(int nout)
 {
     return 2 * BK * (BQ + BS) * 4 + BQ * (BS + 1) * 4 + nout * BS * 4 + (BQ + BS) * 4;
@@ -353,7 +548,7 @@ static size_t g_fpart_bytes = 0;
 cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
                           const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad,
                           int64_t d, const double* coef, int n_out, const KParams& kp, double* F,
-                          cudaStream_t st)
+                          cudaStream_t st, const float* SVtc)
 {
     (void)nsv;
     if (nq <= 0) return cudaSuccess;
@@ -379,6 +574,31 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
         part = g_fpart;
     }
     dim3 grid((unsigned)q_tiles, (unsigned)splits);
+    if (tc && SVtc) {   // pipelined variant (pre-laid-out SV tiles), when its shared memory fits
+        const int dp = (int)pred_tc_dp(d);
+        auto tcp_smem = [&](int nout) {
+            return (int)((2 * TQ * dp + 4 * TS * dp + 2 * TS) * 4 + 2 * nout * TS * 8 + 6 * 8 + 16);
+        };
+        const int nout_t = n_out == 1 ? 1 : 16;
+        if (tcp_smem(nout_t) <= 227 * 1024 && !getenv("SVMB200_NO_TCP")) {
+            svm_note_launches(1);
+            if (n_out == 1) {
+                cudaFuncSetAttribute(k_decision_tcp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcp_smem(1));
+                k_decision_tcp<1><<<grid, TP_THREADS, tcp_smem(1), st>>>(XqT, qnorm, nq, nq_pad, SVtc, svnorm, nsv_pad,
+                                                                        (int)d, dp, coef, n_out, kp, tps, part);
+            } else {
+                cudaFuncSetAttribute(k_decision_tcp<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcp_smem(16));
+                k_decision_tcp<16><<<grid, TP_THREADS, tcp_smem(16), st>>>(XqT, qnorm, nq, nq_pad, SVtc, svnorm, nsv_pad,
+                                                                          (int)d, dp, coef, n_out, kp, tps, part);
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess || splits == 1) return e;
+            int64_t count = nq * n_out;
+            svm_note_launches(1);
+            k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, splits, count, F);
+            return cudaGetLastError();
+        }
+    }
     if (tc) {
         const int dp = (int)((d + 7) / 8 * 8);
         auto tc_smem = [&](int nout) { return (int)((2 * TQ * dp + 2 * TS * dp + TS + nout * TS) * 4 + 16); };
@@ -415,6 +635,23 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     int64_t count = nq * n_out;
     svm_note_launches(1);
     k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, splits, count, F);
+    return cudaGetLastError();
+}
+
+int64_t pred_tc_dp(int64_t d)
+{
+    if (d > 128 || getenv("SVMB200_NO_TC")) return 0;
+    return (d + 7) / 8 * 8;
+}
+
+cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, float* out, cudaStream_t st)
+{
+    const int64_t dp = pred_tc_dp(d);
+    if (dp == 0 || nsv_pad % TS != 0) return cudaErrorInvalidValue;
+    const int64_t total = nsv_pad * dp;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    svm_note_launches(1);
+    k_sv_tiles<<<blocks, 256, 0, st>>>(SVT, nsv_pad, (int)d, (int)dp, out);
     return cudaGetLastError();
 }
 
