@@ -691,9 +691,9 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
     }
     DBuf SVtc;
     const float* svtc = nullptr;
-    if (const int64_t dp = pred_tc_dp(D.d)) {
-        TRY(SVtc.alloc(sizeof(float) * 2 * nsv_pad * dp));
-        CK(pred_sv_tiles(SVT.as<float>(), nsv_pad, D.d, SVtc.as<float>(), st));
+    if (pred_tc_dp(D.d)) {
+        TRY(SVtc.alloc(sizeof(float) * pred_sv_tiles_floats(nsv_pad, D.d, 1)));
+        CK(pred_sv_tiles(SVT.as<float>(), nsv_pad, D.d, coef_sv.as<double>(), 1, SVtc.as<float>(), st));
         svtc = SVtc.as<float>();
     }
     CK(pred_decision(qT, qnorm, D.n, ld, SVT.as<float>(), svn.as<float>(), nsv, nsv_pad, D.d,
@@ -806,10 +806,10 @@ struct svm_model {
 // tcgen05 predict operands: the SVs as [tile][hi | lo][64 * dp] K-major core tiles (d <= 128)
 static int build_sv_tiles(svm_model* M, cudaStream_t st)
 {
-    const int64_t dp = pred_tc_dp(M->d);
-    if (dp == 0 || M->nsv_pad == 0) return SVM_OK;
-    TRY(M->SVtc.alloc(sizeof(float) * 2 * M->nsv_pad * dp));
-    CK(pred_sv_tiles(M->SVT.as<float>(), M->nsv_pad, M->d, M->SVtc.as<float>(), st));
+    if (pred_tc_dp(M->d) == 0 || M->nsv_pad == 0) return SVM_OK;
+    TRY(M->SVtc.alloc(sizeof(float) * pred_sv_tiles_floats(M->nsv_pad, M->d, M->n_out)));
+    CK(pred_sv_tiles(M->SVT.as<float>(), M->nsv_pad, M->d, M->coef.as<double>(), M->n_out,
+                     M->SVtc.as<float>(), st));
     return SVM_OK;
 }
 
@@ -829,11 +829,12 @@ static int assemble_model(const Data& D, std::vector<Problem>& probs, const svm_
     M->nsv_pad = std::max<int64_t>(64, (nsv + 63) / 64 * 64);
     M->d = D.d;
     TRY(gather_rows_T(D, idx, nsv, M->nsv_pad, M->SVT, M->svnorm, st));
-    TRY(build_sv_tiles(M, st));
     TRY(M->coef.alloc(sizeof(double) * M->nsv_pad * np));
     for (int p = 0; p < np; ++p)
         CK(lay_gather_coef(coefs[p].as<double>(), idx.as<int64_t>(), nsv, M->nsv_pad,
                            M->coef.as<double>() + (int64_t)p * M->nsv_pad, st));
+    M->n_out = np;
+    TRY(build_sv_tiles(M, st));
     TRY(to_device(M->b, bs.data(), np, st));
     M->sv_index.resize(nsv);
     if (nsv) CK(cudaMemcpyAsync(M->sv_index.data(), idx.p, sizeof(int64_t) * nsv,
@@ -1676,10 +1677,10 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     M->nsv = nsv;
     M->nsv_pad = nsv_pad;
     M->d = D.d;
-    rc = build_sv_tiles(M, S->st);
-    if (rc != SVM_OK) { delete M; return rc; }
     M->mode = S->mode;
     M->n_out = S->nprob;
+    rc = build_sv_tiles(M, S->st);
+    if (rc != SVM_OK) { delete M; return rc; }
     M->kp = probs[0].kp;
     M->first_label = S->first;
     rc = to_device(M->b, bs.data(), S->nprob, S->st);

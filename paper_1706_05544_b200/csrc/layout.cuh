@@ -77,7 +77,9 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
 // tcgen05 predict (d <= 128): SV tiles [nsv_pad / 64][hi | lo][64 * dp] in the K-major core
 // layout (dp = pred_tc_dp(d)); 0 when the tensor-core path does not apply
 int64_t pred_tc_dp(int64_t d);
-cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, float* out, cudaStream_t st);
+int64_t pred_sv_tiles_floats(int64_t nsv_pad, int64_t d, int n_out);   // tiles + fp32 coefficients
+cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, const double* coef, int n_out,
+                          float* out, cudaStream_t st);
 // G refresh from raw decision sums (certification, a4): G_c(i) = p_c(i) + y_c * F[i]
 cudaError_t pred_refresh_G(const double* F, const float* yv, const uint8_t* status, int64_t n,
                            int64_t n_pad, int ncopy, double eps, float* G, cudaStream_t st);

@@ -11,6 +11,9 @@
 #include "layout.cuh"
 
 #include <math.h>
+#ifdef TC_PROFILE
+#include <cstdio>
+#endif
 #include <cstdlib>
 #include <algorithm>
 
@@ -369,7 +372,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
-constexpr int TP_THREADS = 9 * 32;
+constexpr int TP_EPI = 16;                 // epilogue warps: TMEM lanes 32 (w % 4), columns 16 (w / 4)
+constexpr int TP_THREADS = (TP_EPI + 1) * 32;
 template <int NOUT>
 __global__ void __launch_bounds__(TP_THREADS, 1)
     k_decision_tcp(const float* __restrict__ XqT, const float* __restrict__ qnorm, int64_t nq,
@@ -381,9 +385,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     float* Ah = reinterpret_cast<float*>(smem_raw);
     float* Al = Ah + TQ * dp;
     float* Bs = Al + TQ * dp;                                   // [2 slots][hi | lo][TS * dp]
-    float* sSn = Bs + 2 * 2 * TS * dp;                          // [2][TS]
-    double* sCf = reinterpret_cast<double*>(sSn + 2 * TS);     // [2][NOUT][TS]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sCf + 2 * NOUT * TS);   // bfull[2] accfull[2] accfree[2]
+    float* sSn = Bs + 2 * 2 * TS * dp;                          // [4][TS] SV norms (ring j & 3)
+    float* sCf = sSn + 4 * TS;                                  // [4][NOUT][TS] fp32 coefficients
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sCf + 4 * NOUT * TS);   // bfull[2] accfull[2] accfree[2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 6);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KC = dp >> 2;
@@ -393,6 +397,8 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     const int64_t t_end = min(t_begin + tiles_per_split, n_tiles);
     const int nt = (int)(t_end - t_begin);
     const uint32_t tile_bytes = (uint32_t)(2 * TS * dp * 4);
+    const float* coef32 = SVtc + (size_t)n_tiles * 2 * TS * dp;   // [n_out][nsv_pad] after the tiles
+    (void)coef;
     const uint32_t b_bfull = su32(bars), b_accfull = su32(bars + 2), b_accfree = su32(bars + 4);
 
     for (int e = tid; e < dp * TQ; e += TP_THREADS) {   // resident query tile (hi, lo)
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_bfull + 8 * i), "r"(1));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accfull + 8 * i), "r"(1));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accfree + 8 * i), "r"(8));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accfree + 8 * i), "r"(TP_EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -421,103 +427,141 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_holder;
 
-    if (warp == 8) {
+    if (warp == TP_EPI) {
         if (lane == 0 && nt > 0) {
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TS >> 3) << 17) |
                                    ((uint32_t)(TQ >> 4) << 24);
             const uint32_t sbo = (uint32_t)KC * 128u;
-            auto issue = [&](int j) {   // tile j -> slot j & 1: B (hi | lo), norms, coefficients
-                const int sl = j & 1;
+            // tile j -> B slot j & 1 and norm / coefficient slot j & 3.  Safe to overwrite: B slot
+            // j & 1 once tile j - 2's MMAs completed (waited below), small slot j & 3 once tile
+            // j - 4's epilogue finished (implied by the wait for tile j - 3's TMEM release)
+            auto issue = [&](int j) {
+                const int sl = j & 1, ss = j & 3;
                 const int64_t t = t_begin + j, s0 = t * TS;
                 const uint32_t bar = b_bfull + 8 * sl;
-                const uint32_t bytes = tile_bytes + TS * 4 + (uint32_t)(n_out * TS * 8);
+                const uint32_t bytes = tile_bytes + TS * 4 + (uint32_t)(n_out * TS * 4);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
                 bulk_g2s(su32(Bs + (size_t)sl * 2 * TS * dp), SVtc + (size_t)t * 2 * TS * dp, tile_bytes, bar);
-                bulk_g2s(su32(sSn + sl * TS), svnorm + s0, TS * 4, bar);
+                bulk_g2s(su32(sSn + ss * TS), svnorm + s0, TS * 4, bar);
                 for (int p = 0; p < n_out; ++p)
-                    bulk_g2s(su32(sCf + ((size_t)sl * NOUT + p) * TS), coef + (int64_t)p * nsv_pad + s0, TS * 8, bar);
+                    bulk_g2s(su32(sCf + ((size_t)ss * NOUT + p) * TS), coef32 + (int64_t)p * nsv_pad + s0, TS * 4, bar);
             };
             issue(0);
             if (nt > 1) issue(1);
+#ifdef TC_PROFILE
+            long long pc[4] = {0, 0, 0, 0}, pt = clock64();
+#define PMARK(i) { long long _n = clock64(); pc[i] += _n - pt; pt = _n; }
+#else
+#define PMARK(i)
+#endif
             for (int j = 0; j < nt; ++j) {
                 const int sl = j & 1;
-                mb_wait(b_bfull + 8 * sl, (uint32_t)((j >> 1) & 1));   // (issue(j) waited for tile j - 2's release)
+                mb_wait(b_bfull + 8 * sl, (uint32_t)((j >> 1) & 1));
+                PMARK(0)
+                if (j >= 2) mb_wait(b_accfree + 8 * sl, (uint32_t)(((j - 2) >> 1) & 1));   // TMEM slot drained
+                PMARK(1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t bh = su32(Bs + (size_t)sl * 2 * TS * dp), bl = bh + TS * dp * 4;
                 const uint32_t ah = su32(Ah), al = su32(Al);
                 const uint32_t dcol = tmem + (uint32_t)(sl * TS);
                 for (int ks = 0; ks < (dp >> 3); ++ks)
 #pragma unroll
-                    for (int ps = 0; ps < 4; ++ps) {   // lo.lo, lo.hi, hi.lo, then hi.hi
+                    for (int ps = 1; ps < 4; ++ps) {   // lo.hi, hi.lo, then hi.hi (lo.lo <= 2^-22: dropped)
                         const uint64_t da = umma_desc_kmajor((ps <= 1 ? al : ah) + ks * 256, sbo);
                         const uint64_t db = umma_desc_kmajor((ps == 0 || ps == 2 ? bl : bh) + ks * 256, sbo);
-                        const uint32_t acc = (ks > 0 || ps > 0) ? 1u : 0u;
+                        const uint32_t acc = (ks > 0 || ps > 1) ? 1u : 0u;
                         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                                      ::"r"(dcol), "l"(da), "l"(db), "r"(idesc), "r"(acc));
                     }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_accfull + 8 * sl) : "memory");
-                // the other slot (tile j - 1) is refilled with tile j + 1 once tile j - 1's epilogue,
-                // which runs while tile j's MMAs execute, has released it
+                PMARK(2)
+                // the other B slot (tile j - 1) is refilled with tile j + 1 as soon as tile j - 1's
+                // MMAs have completed, so the copy overlaps tile j's MMAs and tile j - 1's epilogue
                 if (j >= 1 && j + 1 < nt) {
-                    mb_wait(b_accfree + 8 * (sl ^ 1), (uint32_t)(((j - 1) >> 1) & 1));
+                    mb_wait(b_accfull + 8 * (sl ^ 1), (uint32_t)(((j - 1) >> 1) & 1));
                     issue(j + 1);
                 }
+                PMARK(3)
             }
+#ifdef TC_PROFILE
+            if (blockIdx.x == 0 && blockIdx.y == 0)
+                printf("[tcp] producer per tile (%d tiles): wait B %.0f, wait TMEM free %.0f, issue MMAs %.0f, refill %.0f cycles\n",
+                       nt, (double)pc[0] / nt, (double)pc[1] / nt, (double)pc[2] / nt, (double)pc[3] / nt);
+#endif
         }
     } else {
-        const int quad = warp & 3, half = warp >> 2;
+        const int quad = warp & 3, half = warp >> 2;   // half = column quarter (16 columns)
         const float qn = qnorm[q0 + quad * 32 + lane];
         double facc[NOUT];
 #pragma unroll
         for (int p = 0; p < NOUT; ++p) facc[p] = 0.0;
+#ifdef TC_PROFILE
+        long long ec[3] = {0, 0, 0}, et = clock64();
+#define EMARK(i) { long long _n = clock64(); ec[i] += _n - et; et = _n; }
+#else
+#define EMARK(i)
+#endif
         for (int j = 0; j < nt; ++j) {
             const int sl = j & 1;
+            const int ss = j & 3;
             mb_wait(b_accfull + 8 * sl, (uint32_t)((j >> 1) & 1));
+            EMARK(0)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            uint32_t v[32];
-            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * TS + half * 32);
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            uint32_t v[16];
+            const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * TS + half * 16);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-                           "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-                           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                          : "r"(ta));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const float* sn = sSn + sl * TS + half * 32;
+            EMARK(1)
+            const float* sn = sSn + ss * TS + half * 16;
 #pragma unroll
             for (int p = 0; p < NOUT; ++p) {
                 if (p < n_out) {
-                    const double* cf = sCf + ((size_t)sl * NOUT + p) * TS + half * 32;
+                    const float* cf = sCf + ((size_t)ss * NOUT + p) * TS + half * 16;
                     float part = 0.0f;
 #pragma unroll
-                    for (int sI = 0; sI < 32; ++sI)
-                        part = fmaf((float)cf[sI], kernel_from_dot(kp, __uint_as_float(v[sI]), qn, sn[sI]), part);
+                    for (int sI = 0; sI < 16; ++sI)
+                        part = fmaf(cf[sI], kernel_from_dot(kp, __uint_as_float(v[sI]), qn, sn[sI]), part);
                     facc[p] += (double)part;
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b_accfree + 8 * sl) : "memory");
+            EMARK(2)
         }
-        // the two column halves of a query are combined in a fixed order (half 0 + half 1)
+#ifdef TC_PROFILE
+        if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0)
+            printf("[tcp] epilogue warp 0 per tile: wait acc %.0f, tmem ld %.0f, compute %.0f cycles (facc %g)\n",
+                   (double)ec[0] / nt, (double)ec[1] / nt, (double)ec[2] / nt, facc[0]);
+#endif
+        // the four column quarters of a query are combined in a fixed order (0 + 1 + 2 + 3)
         double* red = reinterpret_cast<double*>(Bs);   // B slots are free once every tile is done
         __syncthreads();
-        if (half == 1)
-            for (int p = 0; p < n_out; ++p) red[(quad * 32 + lane) * NOUT + p] = facc[p];
+        if (half > 0)
+            for (int p = 0; p < n_out; ++p) red[((half - 1) * TQ + quad * 32 + lane) * NOUT + p] = facc[p];
         __syncthreads();
         if (half == 0 && q0 + quad * 32 + lane < nq)
-            for (int p = 0; p < n_out; ++p)
-                Fpart[((int64_t)blockIdx.y * nq + q0 + quad * 32 + lane) * n_out + p] =
-                    facc[p] + red[(quad * 32 + lane) * NOUT + p];
+            for (int p = 0; p < n_out; ++p) {
+                double f = facc[p];
+                for (int h = 0; h < 3; ++h) f += red[(h * TQ + quad * 32 + lane) * NOUT + p];
+                Fpart[((int64_t)blockIdx.y * nq + q0 + quad * 32 + lane) * n_out + p] = f;
+            }
     }
-    if (warp == 8) { __syncthreads(); __syncthreads(); }   // match the epilogue warps' barriers
+    if (warp == TP_EPI) { __syncthreads(); __syncthreads(); }   // match the epilogue warps' barriers
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TS));
 }
 
 // SV tiles for k_decision_tcp: [tile][hi | lo][TS * dp] in the K-major core layout
+__global__ void k_coef32(const double* __restrict__ coef, int64_t count, float* __restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)coef[i];
+}
 __global__ void k_sv_tiles(const float* __restrict__ SVT, int64_t nsv_pad, int d, int dp, float* __restrict__ out)
 {
     const int64_t total = nsv_pad * dp;
@@ -577,10 +621,11 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     if (tc && SVtc) {   // pipelined variant (pre-laid-out SV tiles), when its shared memory fits
         const int dp = (int)pred_tc_dp(d);
         auto tcp_smem = [&](int nout) {
-            return (int)((2 * TQ * dp + 4 * TS * dp + 2 * TS) * 4 + 2 * nout * TS * 8 + 6 * 8 + 16);
+            return (int)((2 * TQ * dp + 4 * TS * dp + 4 * TS) * 4 + 4 * nout * TS * 4 + 6 * 8 + 16);
         };
         const int nout_t = n_out == 1 ? 1 : 16;
-        if (tcp_smem(nout_t) <= 227 * 1024 && !getenv("SVMB200_NO_TCP")) {
+        // (the final reduction reuses the B slots: 3 x 128 x nout doubles must fit 4 x 64 x dp floats)
+        if (tcp_smem(nout_t) <= 227 * 1024 && 3 * TQ * nout_t * 8 <= 4 * TS * dp * 4 && !getenv("SVMB200_NO_TCP")) {
             svm_note_launches(1);
             if (n_out == 1) {
                 cudaFuncSetAttribute(k_decision_tcp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tcp_smem(1));
@@ -644,7 +689,13 @@ int64_t pred_tc_dp(int64_t d)
     return (d + 7) / 8 * 8;
 }
 
-cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, float* out, cudaStream_t st)
+int64_t pred_sv_tiles_floats(int64_t nsv_pad, int64_t d, int n_out)
+{
+    return 2 * nsv_pad * pred_tc_dp(d) + (int64_t)n_out * nsv_pad;
+}
+
+cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, const double* coef, int n_out,
+                          float* out, cudaStream_t st)
 {
     const int64_t dp = pred_tc_dp(d);
     if (dp == 0 || nsv_pad % TS != 0) return cudaErrorInvalidValue;
@@ -652,6 +703,9 @@ cudaError_t pred_sv_tiles(const float* SVT, int64_t nsv_pad, int64_t d, float* o
     const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
     svm_note_launches(1);
     k_sv_tiles<<<blocks, 256, 0, st>>>(SVT, nsv_pad, (int)d, (int)dp, out);
+    const int64_t cc = (int64_t)n_out * nsv_pad;
+    svm_note_launches(1);
+    k_coef32<<<(unsigned)std::min<int64_t>((cc + 255) / 256, 148 * 16), 256, 0, st>>>(coef, cc, out + 2 * total);
     return cudaGetLastError();
 }
 
