@@ -594,7 +594,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         (void)clk;
         const double it = (double)std::max<int64_t>(1, info.iterations);
         fprintf(stderr, "[svmb200]   worker warp 0 (cycles/iter): B-dots %.0f - %.0f B-epilogue %.0f "
-                "B-merge %.0f B-tail %.0f finish %.0f | qww: partial-sync %.0f kernel-sync %.0f\n",
+                "B-merge %.0f B-tail %.0f finish %.0f | level-1 merge: first call %.0f, warm repeat %.0f\n",
                 info.phase_cycles[8] / it, info.phase_cycles[9] / it,
                 info.phase_cycles[10] / it, info.phase_cycles[11] / it, info.phase_cycles[12] / it,
                 info.phase_cycles[13] / it, info.phase_cycles[14] / it, info.phase_cycles[15] / it);

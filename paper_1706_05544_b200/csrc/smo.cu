@@ -287,6 +287,8 @@ struct SmoShared {
     uint64_t cta_up[8], cta_low[8];
     uint64_t win_up[8], win_low[8];      // merged global winners (keys)
     int32_t win_up_src[8], win_low_src[8];
+    uint64_t gm_key[2][8][8];            // two-level merge: [side][part] sorted top-8 of part's lists
+    int32_t gm_src[2][8][8];
     int64_t w_gidx[SVM_WS];              // working set, ascending dual index
     int32_t w_src[SVM_WS];               // exchange word index (slot * 64 + candidate) per position
     int32_t w_slot[SVM_WS];              // distinct-row slot of each position
@@ -445,7 +447,7 @@ __device__ __forceinline__ void merge_chunk_rows(uint64_t (&ku)[2 * RPT], uint64
 __device__ __forceinline__ uint64_t lds_u64(const uint64_t* p)
 {
     uint64_t v;
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
     return v;
 }
 
@@ -509,6 +511,32 @@ __device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64
                     nxt[k] = hd[k] + 1 < 8 ? lds_u64(keys + l * 8 + hd[k] + 1) : 0;
                 }
             }
+        }
+    }
+}
+
+// One warp, one sorted 8-list per lane (heads in registers, the next key prefetched): the top-8
+// of the union in 8 rounds of a 64-bit warp max.  key(l, j) / src(l, j) read list l's j-th entry.
+template <class KeyF, class SrcF>
+__device__ __forceinline__ void lane_list_merge(int nl, KeyF key, SrcF srcf, uint64_t* out,
+                                                int32_t* src, int lane)
+{
+    int hd = 0;
+    uint64_t cur = lane < nl ? key(lane, 0) : 0ull;
+    uint64_t nxt = lane < nl ? key(lane, 1) : 0ull;
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r) {
+        const uint64_t best = warp_max_u64(cur);
+        if (best == 0ull) {
+            if (lane < 8 && lane >= r) { out[lane] = 0ull; src[lane] = -1; }
+            break;
+        }
+        if (cur == best) {   // unique owner (keys are unique)
+            out[r] = best;
+            src[r] = srcf(lane, hd);
+            ++hd;
+            cur = nxt;
+            nxt = hd + 1 < 8 ? key(lane, hd + 1) : 0ull;
         }
     }
 }
@@ -900,13 +928,46 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             return;
         }
         // ---- a1 (2/2): global merge (warp 0: I_up top-8, warp 1: I_low top-8) ----------------
-        if (warp < 2) {
+        wmark(-1);
+        if (L <= 8 * 32) {
+            // two levels: 8 warps per side merge <= 32 lists each (one per lane), then one warp per
+            // side merges the 8 partial top-8 lists (src = list * 8 + position throughout)
+            {
+                const int side = warp >> 3, part = warp & 7;
+                const uint64_t* keys = side == 0 ? sKU : sKL;
+                const int per = (L + 7) >> 3, l0 = part * per;
+                const int nl = max(0, min(per, L - l0));
+#ifdef SMO_PROFILE
+                const long long c0 = clock64();
+#endif
+                lane_list_merge(nl, [&](int i, int j) { return lds_u64(keys + (l0 + i) * 8 + j); },
+                                [&](int i, int j) { return (l0 + i) * 8 + j; },
+                                sh.gm_key[side][part], sh.gm_src[side][part], lane);
+#ifdef SMO_PROFILE
+                {   // I-cache probe: the same merge again (warm instructions), into scratch
+                    uint64_t sk[8]; int32_t ss[8];
+                    const int v0 = *reinterpret_cast<volatile int*>(&sh.nw);
+                    const long long c1 = clock64() + (v0 & 0);
+                    lane_list_merge(nl, [&](int i, int j) { return lds_u64(keys + (l0 + i) * 8 + j); },
+                                    [&](int i, int j) { return (l0 + i) * 8 + j; }, sk, ss, lane);
+                    const int v1 = *reinterpret_cast<volatile int*>(&sh.nw);
+                    const long long c2 = clock64() + (v1 & 0) + (long long)(sk[0] & 0);
+                    if (warp == 0) { wprof[6] += c1 - c0; wprof[7] += c2 - c1; }
+                }
+#endif
+            }
+            __syncthreads();
+            if (warp < 2) {
+                uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
+                int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
+                lane_list_merge(8, [&](int i, int j) { return lds_u64(&sh.gm_key[warp][i][j]); },
+                                [&](int i, int j) { return sh.gm_src[warp][i][j]; }, out, srcs, lane);
+            }
+        } else if (warp < 2) {
             const uint64_t* keys = warp == 0 ? sKU : sKL;
             uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
             int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
-            if (L <= 160) global_merge<5>(keys, L, out, srcs, lane);
-            else global_merge_smem(keys, reinterpret_cast<uint8_t*>(sh.qpart) + warp * 2048, L,
-                                   out, srcs, lane);
+            global_merge_smem(keys, reinterpret_cast<uint8_t*>(sh.qpart) + warp * 2048, L, out, srcs, lane);
         }
         __syncthreads();
         if (warp == 0) {
