@@ -762,10 +762,19 @@ static int certify(const Data& D, Problem& P, double* viol, cudaStream_t st)
 }
 
 // The full solve of one problem: loop to tolerance, then certification + resume (a4).
+static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
+                          cudaStream_t st);
 static int solve_problem(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
                          cudaStream_t st)
 {
     TRY(run_loop(D, P, E, P.max_iter, st, nullptr));
+    return certify_resume(D, P, E, prm, st);
+}
+
+// Certification (a4, reading R16) and resumption of the persistent loop after a loop stopped.
+static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
+                          cudaStream_t st)
+{
     for (int round = 0; round < 4; ++round) {
         if (!P.converged || prm->certify == 0) break;
         if (prm->certify < 0) {  // auto: only when one pass over n x n_SV is affordable
@@ -893,6 +902,112 @@ static int label_problems(const svm_params* prm, const std::vector<float>& y,
     return SVM_OK;
 }
 
+// Batched one-vs-rest: all binary problems of one dense X iterate together, one
+// X pass per iteration on tcgen05 (k_ovr_pass) and one CTA per problem for selection + subproblem
+// (k_ovr_solve).  Every problem follows the single-problem iteration of P:53; *handled = false
+// when the configuration is not covered (the problems are then solved one after another).
+static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_params* prm,
+                         cudaStream_t st, bool* handled)
+{
+    *handled = false;
+    const int P = (int)probs.size();
+    if (D.csr || P < 2 || P > OVR_MAXP || probs[0].ncopy != 1 || probs[0].q != SVM_WS ||
+        getenv("SVMB200_NO_BATCH"))
+        return SVM_OK;
+    OvrArgs a;
+    memset(&a, 0, sizeof a);
+    a.XT = D.XT.as<float>();
+    a.XR = D.XR;
+    a.xnorm = D.norms.as<float>();
+    a.n = D.n;
+    a.n_pad = D.n_pad;
+    a.d = D.d;
+    a.P = P;
+    for (int p = 0; p < P; ++p) {
+        a.alpha[p] = probs[p].alpha.as<double>();
+        a.G[p] = probs[p].G.as<float>();
+        a.status[p] = probs[p].status.as<uint8_t>();
+    }
+    const Problem& P0 = probs[0];
+    a.C = P0.C;
+    a.tol = P0.tol_loop;
+    a.inner_tol = std::max(0.1 * P0.tol, 1e-10);   // DESIGN.md reading R2
+    a.inner_max = 64 * P0.q;
+    a.max_iter = P0.max_iter;
+    a.kp = P0.kp;
+    a.NU = 16 * P;
+    a.kch = 32;
+    a.nkc = (int)((D.d + a.kch - 1) / a.kch);
+    a.nct = (int)((D.n + 127) / 128);
+    if (ovr_pass_smem(a) > 227 * 1024 || D.d * SVM_WS * 4 > 200 * 1024) return SVM_OK;
+    DBuf Utc, unorm, ucoef, cand, done, iters, mup, mlow, inner;
+    TRY(Utc.alloc(sizeof(float) * (size_t)a.nkc * 2 * a.NU * a.kch));
+    TRY(unorm.alloc(sizeof(float) * a.NU));
+    TRY(ucoef.alloc(sizeof(float) * a.NU));
+    TRY(cand.alloc(sizeof(uint64_t) * (size_t)P * 2 * a.nct * 8));
+    TRY(done.alloc(sizeof(int32_t) * P));
+    TRY(iters.alloc(sizeof(int64_t) * P));
+    TRY(mup.alloc(sizeof(double) * P));
+    TRY(mlow.alloc(sizeof(double) * P));
+    TRY(inner.alloc(sizeof(int64_t) * P));
+    for (DBuf* b : {&Utc, &unorm, &ucoef, &done, &iters, &inner}) CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
+    a.Utc = Utc.as<float>();
+    a.unorm = unorm.as<float>();
+    a.ucoef = ucoef.as<float>();
+    a.cand = cand.as<uint64_t>();
+    a.done = done.as<int32_t>();
+    a.iters = iters.as<int64_t>();
+    a.mup = mup.as<double>();
+    a.mlow = mlow.as<double>();
+    a.inner_total = inner.as<int64_t>();
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    CK(launch_ovr_pass(a, st));   // candidates of the initial state (all coefficients 0)
+    std::vector<int32_t> dh(P);
+    for (int64_t it = 0; it <= a.max_iter; ++it) {
+        CK(launch_ovr_solve(a, st));
+        CK(launch_ovr_pass(a, st));
+        if ((it & 15) == 15) {
+            CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            bool all = true;
+            for (int p = 0; p < P; ++p) all = all && dh[p];
+            if (all) break;
+        }
+    }
+    CK(launch_ovr_solve(a, st));   // stop tests of the final state
+    CK(cudaEventRecord(e1, st));
+    std::vector<int64_t> ih(P);
+    std::vector<double> uh(P), lh(P);
+    CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ih.data(), a.iters, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(uh.data(), a.mup, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lh.data(), a.mlow, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int p = 0; p < P; ++p) {
+        Problem& Pp = probs[p];
+        Pp.iterations = ih[p];
+        Pp.m_up = dh[p] ? uh[p] : 0.0;
+        Pp.M_low = dh[p] ? lh[p] : 0.0;
+        Pp.converged = dh[p] && (uh[p] - lh[p] <= Pp.tol_loop);
+        Pp.loop_ms += ms / P;
+    }
+    if (getenv("SVMB200_PROFILE")) {
+        int64_t mx = 0, sum = 0;
+        for (int p = 0; p < P; ++p) { mx = std::max(mx, ih[p]); sum += ih[p]; }
+        fprintf(stderr, "[svmb200] batched OvR: %d problems, %lld iterations (max), %lld in total, %.1f ms, %.1f us per batched iteration\n",
+                P, (long long)mx, (long long)sum, ms, 1e3 * ms / std::max<int64_t>(1, mx));
+    }
+    *handled = true;
+    return SVM_OK;
+}
+
 static int train_common(Data& D, const float* y, const svm_params* prm, svm_model** out,
                         double t_start, cudaStream_t st)
 {
@@ -911,10 +1026,13 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0;
     int64_t iters = 0;
     bool conv = true, cert = true;
+    for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
+    bool batched = false;
+    TRY(solve_batched(D, probs, prm, st, &batched));
     for (size_t p = 0; p < ys.size(); ++p) {
         Problem& P = probs[p];
-        TRY(problem_init(P, D, ys[p].data(), prm, st));
-        TRY(solve_problem(D, P, E, prm, st));
+        if (batched) TRY(certify_resume(D, P, E, prm, st));
+        else TRY(solve_problem(D, P, E, prm, st));
         Reduced r;
         TRY(reduce_state(D, P, &r, st));
         // bias (sign-corrected; reading R6)

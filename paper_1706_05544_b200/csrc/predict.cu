@@ -197,21 +197,6 @@ __global__ void k_finalize(const double* __restrict__ F, int64_t nq, int n_out,
 // truncation of lo costs ~2^-21 relative per product).  One query per thread = one TMEM lane, so the
 // epilogue (kernel value, coefficient contraction) needs no cross-thread reduction.
 constexpr int TQ = 128, TS = 64;
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t sbo)
-{
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128u >> 4) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
-}
-// x = hi + lo with hi = rna_tf32(x) (|lo| <= 2^-11 |x|, exact in fp32)
-__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo)
-{
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-    hi = __uint_as_float(h);
-    lo = x - hi;
-}
-__device__ __forceinline__ int kmaj_off(int r, int k, int KC) { return ((r >> 3) * KC + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3); }
 
 template <int NOUT>
 __global__ void __launch_bounds__(TQ, 1)

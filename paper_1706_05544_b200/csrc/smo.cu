@@ -1397,6 +1397,354 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
     for (int r = 0; r < nr; ++r) K[li * nr + r] = kernel_from_dot(a.kp, acc[0][r], xi, xn[r]);
 }
 
+
+// ================================================================ batched one-vs-rest (8(f) #1)
+// One iteration = k_ovr_solve (one CTA per problem: merge its candidates -> W, stop test, K_WW,
+// subproblem, alpha / status of W, coefficients and its 16 columns of the U operand) followed by
+// k_ovr_pass (one CTA per 128 training rows: D = X_rows X_U^T on tcgen05 3xTF32 into TMEM, then per
+// problem the kernel values of its 16 columns, the G update and the tile's top-8 candidates).
+// Each problem follows exactly the single-problem iteration of P:53 (same selection, subproblem and
+// update rules); only the X pass is shared.
+constexpr int OVR_THREADS = 512;
+
+__device__ __forceinline__ void ovr_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0, spins = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+        if (ok) return;
+        if (++spins == 1024) {   // watchdog: a lost stage must fail the launch, not hang the GPU
+            spins = 0;
+            const uint64_t now = gtimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_pass(const OvrArgs a)
+{
+    extern __shared__ __align__(1024) unsigned char ovr_smem[];
+    const int kch = a.kch, NU = a.NU, KC = kch >> 2;
+    float* Ah = reinterpret_cast<float*>(ovr_smem);             // [128 x kch] K-major core layout
+    float* Al = Ah + 128 * kch;
+    float* Bs = Al + 128 * kch;                                  // [hi | lo][NU x kch]
+    float* sCoef = Bs + 2 * NU * kch;                            // [NU]
+    float* sNorm = sCoef + NU;                                   // [NU]
+    uint64_t* wl = reinterpret_cast<uint64_t*>(sNorm + NU);      // [P][2][4][8] warp lists
+    uint64_t* bars = wl + OVR_MAXP * 2 * 4 * 8;                  // bfull, mdone
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * 128;
+    const uint32_t b_full = su32(bars), b_done = su32(bars + 1);
+    for (int i = tid; i < NU; i += OVR_THREADS) { sCoef[i] = a.ucoef[i]; sNorm[i] = a.unorm[i]; }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_full), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_done), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_holder;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NU >> 3) << 17) | (8u << 24);
+    const uint32_t sbo = (uint32_t)KC * 128u;
+    const uint32_t bbytes = (uint32_t)(2 * NU * kch * 4);
+    for (int kc = 0; kc < a.nkc; ++kc) {
+        // A: this tile's rows x chunk features, split hi / lo
+        for (int e = tid; e < 128 * kch; e += OVR_THREADS) {
+            const int k = e >> 7, r = e & 127;
+            const int64_t f = (int64_t)kc * kch + k, row = r0 + r;
+            const float x = (f < a.d && row < a.n) ? a.XT[f * a.n_pad + row] : 0.0f;
+            float hi, lo;
+            tf32_split(x, hi, lo);
+            Ah[kmaj_off(r, k, KC)] = hi;
+            Al[kmaj_off(r, k, KC)] = lo;
+        }
+        if (tid == 0) {   // B: the union rows' chunk (hi | lo), one bulk copy
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b_full), "r"(bbytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(Bs)), "l"(a.Utc + (size_t)kc * 2 * NU * kch), "r"(bbytes), "r"(b_full) : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 0) {
+            ovr_wait(b_full, (uint32_t)(kc & 1));
+            const uint32_t ah = su32(Ah), al = su32(Al), bh = su32(Bs), bl = bh + (uint32_t)(NU * kch * 4);
+            for (int ks = 0; ks < (kch >> 3); ++ks)
+#pragma unroll
+                for (int ps = 1; ps < 4; ++ps) {   // lo.hi, hi.lo, hi.hi
+                    const uint64_t da = umma_desc_kmajor((ps <= 1 ? al : ah) + ks * 256, sbo);
+                    const uint64_t db = umma_desc_kmajor((ps == 2 ? bl : bh) + ks * 256, sbo);
+                    const uint32_t acc = (kc > 0 || ks > 0 || ps > 1) ? 1u : 0u;
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                                 ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_done) : "memory");
+        }
+        ovr_wait(b_done, (uint32_t)(kc & 1));   // A and B are rewritten by the next chunk
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // ---- epilogue: warp w = rows 32 (w % 4) .., problems w / 4, w / 4 + 4, ... --------------
+    const int q = warp & 3;
+    const int64_t i = r0 + q * 32 + lane;
+    const bool valid = i < a.n;
+    const float xn = valid ? a.xnorm[i] : 0.0f;
+    for (int p = warp >> 2; p < a.P; p += 4) {
+        uint32_t v[16];
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(p * 16);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                     : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint64_t ku = 0ull, kl = 0ull;
+        if (valid) {
+            float S = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+                S = fmaf(sCoef[p * 16 + r], kernel_from_dot(a.kp, __uint_as_float(v[r]), xn, sNorm[p * 16 + r]), S);
+            const uint32_t st = a.status[p][i];
+            const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
+            float g = a.G[p][i];
+            g = fmaf(yv, S, g);
+            a.G[p][i] = g;
+            const float sc = -yv * g;
+            const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)i);
+            if (st_in_up(st)) ku = ((uint64_t)ord_f32(sc) << 32) | lo;
+            if (st_in_low(st)) kl = ((uint64_t)ord_f32(-sc) << 32) | lo;
+        }
+        uint64_t wlu = 0ull, wll = 0ull;
+        uint64_t ka[1] = {ku}, kb[1] = {kl};
+        merge_chunk<1>(ka, kb, wlu, wll, lane);
+        if (lane < 8) {
+            wl[((p * 2 + 0) * 4 + q) * 8 + lane] = wlu;
+            wl[((p * 2 + 1) * 4 + q) * 8 + lane] = wll;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    // tile top-8 per problem and side: warp w merges the 4 quadrant lists of (p, side) = (w / 2, w % 2)
+    for (int ps = warp; ps < 2 * a.P; ps += OVR_THREADS / 32) {
+        const int p = ps >> 1, side = ps & 1;
+        uint64_t out[8];
+        int32_t srcd[8];
+        const uint64_t* L4 = wl + (size_t)((p * 2 + side) * 4) * 8;
+        uint64_t* dst = a.cand + (((size_t)p * 2 + side) * a.nct + blockIdx.x) * 8;
+        __shared__ uint64_t mo[OVR_THREADS / 32][8];
+        __shared__ int32_t ms[OVR_THREADS / 32][8];
+        lane_list_merge(4, [&](int l, int j) { return lds_u64(L4 + l * 8 + j); },
+                        [&](int l, int j) { return l * 8 + j; }, mo[warp], ms[warp], lane);
+        __syncwarp();
+        (void)out; (void)srcd;
+        if (lane < 8) dst[lane] = mo[warp][lane];
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+__global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
+{
+    extern __shared__ __align__(16) unsigned char ovr_smem[];
+    float* sXW = reinterpret_cast<float*>(ovr_smem);   // [d][16]
+    __shared__ SmoShared sh;
+    __shared__ uint64_t gm[16][8];
+    __shared__ int32_t gms[16][8];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int p = blockIdx.x;
+    const int d = (int)a.d;
+    if (a.done[p]) {
+        if (tid < 16) a.ucoef[p * 16 + tid] = 0.0f;
+        return;
+    }
+    // ---- a1: merge the row tiles' top-8 lists (two levels, 16 warps x 32 lists) per side ----
+    for (int side = 0; side < 2; ++side) {
+        const uint64_t* cl = a.cand + ((size_t)p * 2 + side) * a.nct * 8;
+        for (int base = 0; base < a.nct; base += 16 * 32) {   // more than 512 tiles: fold rounds
+            const int l0 = base + warp * 32;
+            const int nl = max(0, min(32, a.nct - l0));
+            uint64_t mo[8];
+            int32_t ms[8];
+            (void)mo; (void)ms;
+            lane_list_merge(nl, [&](int l, int j) { return cl[(size_t)(l0 + l) * 8 + j]; },
+                            [&](int l, int j) { return (l0 + l) * 8 + j; }, gm[warp], gms[warp], lane);
+            __syncthreads();
+            if (warp == 0) {
+                uint64_t* out = side == 0 ? sh.win_up : sh.win_low;
+                int32_t* srcs = side == 0 ? sh.win_up_src : sh.win_low_src;
+                // merge the 16 partial lists together with the result of the previous fold round
+                __shared__ uint64_t prev[8];
+                if (base > 0 && lane < 8) prev[lane] = out[lane];
+                __syncwarp();
+                const int nlist = base > 0 ? 17 : 16;
+                lane_list_merge(nlist, [&](int l, int j) { return l < 16 ? lds_u64(&gm[l][j]) : lds_u64(&prev[j]); },
+                                [&](int l, int j) { return l; }, out, srcs, lane);
+            }
+            __syncthreads();
+        }
+    }
+    // ---- W: sorted union of the 8 + 8 winners, deduplicated (one copy per row: C-SVC) ---------
+    if (warp == 0) {
+        uint64_t key = 0;
+        if (lane < 8) key = sh.win_up[lane];
+        else if (lane < 16) key = sh.win_low[lane - 8];
+        const uint64_t g = key ? key_index(key) : ~0ull;
+        bool valid = key != 0;
+        uint64_t gj[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) gj[j] = __shfl_sync(FULL, g, j);
+        if (lane >= 8 && lane < 16) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) valid = valid && gj[j] != g;
+        }
+        valid = valid && lane < 16;
+        const uint32_t vm = __ballot_sync(FULL, valid);
+        int rank = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) rank += (((vm >> j) & 1u) && gj[j] < g) ? 1 : 0;
+        const int nw = __popc(vm);
+        if (valid) {
+            sh.w_gidx[rank] = (int64_t)g;
+            sh.w_slot[rank] = rank;
+            sh.r_row[rank] = (int64_t)g;
+        }
+        if (lane == 0) {
+            sh.nw = nw;
+            sh.nr = nw;
+            const uint64_t ku0 = sh.win_up[0], kl0 = sh.win_low[0];
+            sh.m_up = ku0 ? (double)unord_f32((uint32_t)(ku0 >> 32)) : -INFINITY;
+            sh.M_low = kl0 ? -(double)unord_f32((uint32_t)(kl0 >> 32)) : INFINITY;
+            sh.stop = (sh.m_up - sh.M_low <= a.tol) || (a.iters[p] >= a.max_iter) || nw == 0;
+        }
+    }
+    __syncthreads();
+    if (sh.stop) {
+        if (tid == 0) {
+            a.done[p] = 1;
+            a.mup[p] = sh.m_up;
+            a.mlow[p] = sh.M_low;
+        }
+        if (tid < 16) a.ucoef[p * 16 + tid] = 0.0f;
+        return;
+    }
+    const int nw = sh.nw, nr = sh.nr;
+    // payloads of W, X_W rows (fp32 [d][16], columns >= nr zero), norms
+    if (tid < nw) {
+        const int64_t g = sh.w_gidx[tid];
+        sh.w_alpha[tid] = a.alpha[p][g];
+        sh.w_G[tid] = (double)a.G[p][g];
+        sh.w_y[tid] = (a.status[p][g] & ST_YPOS) ? 1 : -1;
+    }
+    for (int i = tid; i < d * SVM_WS; i += OVR_THREADS)
+        if ((i & 15) >= nr) sXW[i] = 0.0f;
+    if (warp < nr) {
+        const int64_t row = sh.r_row[warp];
+        const float* src = a.XR + row * a.d;
+        for (int k = lane; k < d; k += 32) sXW[k * SVM_WS + warp] = __ldg(src + k);
+        if (lane == 0) sh.xn[warp] = a.xnorm[row];
+    }
+    if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
+    __syncthreads();
+    // ---- K_WW in fp64 from the fp32 tile (pairs k-split, four interleaved accumulators) -------
+    {
+        const int npairs = nr * (nr + 1) / 2;
+        const int kp = max(1, min(4, OVR_THREADS / max(npairs, 1)));
+        const int dp = (d + 3) & ~3;
+        const int klen = ((d + kp - 1) / kp + 3) & ~3;
+        if (tid < npairs * kp) {
+            const int pr = tid / kp, part = tid - pr * kp;
+            int r = 0, rem = pr;
+            while (rem >= nr - r) { rem -= nr - r; ++r; }
+            const int sidx = r + rem;
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            if (sidx != r || a.kp.kernel != 2) {
+                const int k0 = part * klen, k1 = min(k0 + klen, dp);
+                auto ld = [&](int c, int k) { return k < d ? (double)sXW[k * SVM_WS + c] : 0.0; };
+                for (int k = k0; k < k1; k += 4) {
+                    if (a.kp.kernel == 2) {
+                        const double t0 = ld(r, k) - ld(sidx, k), t1 = ld(r, k + 1) - ld(sidx, k + 1);
+                        const double t2 = ld(r, k + 2) - ld(sidx, k + 2), t3 = ld(r, k + 3) - ld(sidx, k + 3);
+                        acc0 = fma(t0, t0, acc0); acc1 = fma(t1, t1, acc1);
+                        acc2 = fma(t2, t2, acc2); acc3 = fma(t3, t3, acc3);
+                    } else {
+                        acc0 = fma(ld(r, k), ld(sidx, k), acc0); acc1 = fma(ld(r, k + 1), ld(sidx, k + 1), acc1);
+                        acc2 = fma(ld(r, k + 2), ld(sidx, k + 2), acc2); acc3 = fma(ld(r, k + 3), ld(sidx, k + 3), acc3);
+                    }
+                }
+            }
+            sh.qpart[pr * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
+        }
+        __syncthreads();
+        if (tid < npairs) {
+            int r = 0, rem = tid;
+            while (rem >= nr - r) { rem -= nr - r; ++r; }
+            const int sidx = r + rem;
+            double v = 0.0;
+            for (int part = 0; part < kp; ++part) v += sh.qpart[tid * 4 + part];
+            const double kv = kernel_fp64_from(v, a.kp);
+            sh.kr[r * SVM_WS + sidx] = kv;
+            sh.kr[sidx * SVM_WS + r] = kv;
+        }
+        __syncthreads();
+        if (tid < SVM_WS * SVM_WS) {
+            const int pa = tid >> 4, pb = tid & 15;
+            double kab = 0.0, ie = 0.0;
+            if (pa < nw && pb < nw) {
+                kab = sh.kr[pa * SVM_WS + pb];
+                const double eta = sh.kr[pa * SVM_WS + pa] + sh.kr[pb * SVM_WS + pb] - 2.0 * kab;
+                ie = 1.0 / (eta < 1e-12 ? 1e-12 : eta);
+            }
+            sh.kpos[tid] = kab;
+            sh.inv_eta[tid] = ie;
+        }
+        __syncthreads();
+    }
+    // ---- a2: the subproblem (one warp), then alpha / status of W and the coefficients --------
+    if (warp == 0) {
+        const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
+        __syncwarp();
+        if (lane < SVM_WS) {
+            float c = 0.0f;
+            if (lane < nw) {
+                const double da = sh.w_anew[lane] - sh.w_alpha[lane];
+                c = (float)((double)sh.w_y[lane] * da);
+                const int64_t g = sh.w_gidx[lane];
+                a.alpha[p][g] = sh.w_anew[lane];
+                a.status[p][g] = make_status(sh.w_y[lane], sh.w_anew[lane], a.C);
+            }
+            a.ucoef[p * 16 + lane] = c;
+            a.unorm[p * 16 + lane] = sh.xn[lane];
+        }
+        if (lane == 0) {
+            a.iters[p] += 1;
+            a.inner_total[p] += steps;
+        }
+    }
+    // ---- this problem's 16 columns of the U operand, all K-chunks (hi | lo) --------------------
+    {
+        const int kch = a.kch, KC = kch >> 2, NU = a.NU;
+        const int total = a.nkc * kch * 16;
+        for (int e = tid; e < total; e += OVR_THREADS) {
+            const int f = e >> 4, r = e & 15;
+            const int kc = f / kch, k = f - kc * kch;
+            const float x = f < d ? sXW[f * SVM_WS + r] : 0.0f;
+            float hi, lo;
+            tf32_split(x, hi, lo);
+            float* base = a.Utc + (size_t)kc * 2 * NU * kch;
+            base[kmaj_off(p * 16 + r, k, KC)] = hi;
+            base[NU * kch + kmaj_off(p * 16 + r, k, KC)] = lo;
+        }
+    }
+}
 }  // namespace
 
 int smo_ring_bytes(int rpt) { return SMO_THREADS * 4 * rpt * (rpt == 1 ? pf_x<1>() : rpt == 2 ? pf_x<2>() : pf_x<4>()); }
@@ -1443,5 +1791,30 @@ cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, fl
         svm_note_launches(1);
         kernel_rows_kernel<false><<<grid, 256, smem, st>>>(a, rows, nr, K);
     }
+    return cudaGetLastError();
+}
+
+int ovr_pass_smem(const OvrArgs& a)
+{
+    return (int)((2 * 128 * a.kch + 2 * a.NU * a.kch + 2 * a.NU) * 4 + OVR_MAXP * 2 * 4 * 8 * 8 + 2 * 8 + 16);
+}
+
+cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st)
+{
+    const int smem = ovr_pass_smem(a);
+    cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    svm_note_launches(1);
+    k_ovr_pass<<<a.nct, OVR_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st)
+{
+    const int smem = (int)(a.d * SVM_WS * 4);
+    cudaError_t e = cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    svm_note_launches(1);
+    k_ovr_solve<<<a.P, OVR_THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }

@@ -165,6 +165,40 @@ struct SmoArgs {
     int32_t x_ring;           // streamed X through a per-lane cp.async ring (RPT >= 2)
 };
 
+// Batched one-vs-rest: P <= 16 binary problems on the same dense X, one X pass per
+// iteration for all of them.  The union U of the problems' working sets (16 slots per problem,
+// column p * 16 + slot) is the B operand of a tcgen05 3xTF32 product D[rows x NU] = X_rows X_U^T.
+constexpr int OVR_MAXP = 16;
+struct OvrArgs {
+    const float* XT;           // [d][n_pad] feature-major
+    const float* XR;           // [n][d] row-major (working-set row gathers)
+    const float* xnorm;        // [n_pad]
+    int64_t n, n_pad, d;
+    int P;                     // problems
+    double* alpha[OVR_MAXP];   // per problem [n_pad]
+    float* G[OVR_MAXP];
+    uint8_t* status[OVR_MAXP];
+    double C, tol, inner_tol;
+    int inner_max;
+    int64_t max_iter;
+    KParams kp;
+    int NU;                    // 16 * P (MMA N)
+    int kch, nkc;              // features per K-chunk (multiple of 8), number of chunks
+    float* Utc;                // [nkc][hi | lo][NU * kch] K-major core tiles (KC = kch / 4)
+    float* unorm;              // [NU] |x_u|^2 (0 for empty slots)
+    float* ucoef;              // [NU] c_r of slot r of problem p (0 = no update)
+    uint64_t* cand;            // [P][2 sides][nct][8] per-row-tile top-8 keys
+    int nct;                   // row tiles of 128 (pass CTAs)
+    int32_t* done;             // [P] 1 once problem p stopped
+    int64_t* iters;            // [P]
+    double* mup;               // [P] m_up, M_low at the stop
+    double* mlow;
+    int64_t* inner_total;      // [P]
+};
+int ovr_pass_smem(const OvrArgs& a);
+cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st);
+cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st);
+
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
 void svm_note_launches(int k);
 
@@ -175,3 +209,25 @@ int smo_csr_stage_bytes();
 int smo_csr_w_extra_bytes(int64_t d);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);
+// ---- tcgen05 TF32 operands (predict.cu, the batched one-vs-rest pass in smo.cu) -------------
+// K-major SWIZZLE_NONE canonical layout: core matrix = 8 rows x 4 consecutive k (16 B per row),
+// at ((row / 8) * KC + k / 4) * 128 B with KC = (k extent) / 4; LBO (next k chunk) = 128 B,
+// SBO (next 8-row group) = KC * 128 B.  kind::tf32 reads the top 19 bits of each fp32 operand,
+// so operands are split x = hi + lo, hi = rna_tf32(x), lo = x - hi (exact, |lo| <= 2^-11 |x|).
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t sbo)
+{
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128u >> 4) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// x = hi + lo with hi = rna_tf32(x) (|lo| <= 2^-11 |x|, exact in fp32)
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo)
+{
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
+    lo = x - hi;
+}
+__device__ __forceinline__ int kmaj_off(int r, int k, int KC) { return ((r >> 3) * KC + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3); }
+
+
