@@ -52,7 +52,9 @@ class svm_model_info(ctypes.Structure):
                 ("violation", ctypes.c_double), ("converged", ctypes.c_int32),
                 ("certified", ctypes.c_int32), ("dual_objective", ctypes.c_double),
                 ("train_ms", ctypes.c_double), ("loop_ms", ctypes.c_double),
-                ("setup_ms", ctypes.c_double), ("certify_ms", ctypes.c_double)]
+                ("setup_ms", ctypes.c_double), ("certify_ms", ctypes.c_double),
+                ("passes", ctypes.c_int64), ("pass_ms", ctypes.c_double),
+                ("batched", ctypes.c_int32)]
 
 
 class svm_solver_stats(ctypes.Structure):

@@ -375,6 +375,8 @@ struct Problem {
     bool converged = false, certified = false;
     double tol_loop = 0;   // the loop's stop threshold: tol, lowered after a failed certification (R16)
     double loop_ms = 0, cert_ms = 0;
+    int64_t passes = 0;    // X passes of the dominant pass kernel (batched one-vs-rest: k_ovr_pass)
+    double pass_ms = 0;    // their device time (CUDA event pairs around each launch)
     SmoInfo last_info;
 };
 
@@ -936,12 +938,15 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     a.max_iter = P0.max_iter;
     a.kp = P0.kp;
     a.NU = 16 * P;
-    a.kch = 32;
+    a.kch = OVR_KCH;
     a.nkc = (int)((D.d + a.kch - 1) / a.kch);
     a.nct = (int)((D.n + 127) / 128);
-    if (ovr_pass_smem(a) > 227 * 1024 || D.d * SVM_WS * 4 > 200 * 1024) return SVM_OK;
-    DBuf Utc, unorm, ucoef, cand, done, iters, mup, mlow, inner;
-    TRY(Utc.alloc(sizeof(float) * (size_t)a.nkc * 2 * a.NU * a.kch));
+    // k_ovr_solve stages X_W in fp32 and fp64: d (64 + 128) B + 96 B of shared memory
+    if (ovr_pass_smem(a) > 227 * 1024 || D.d * SVM_WS * 12 + SVM_WS * 6 * 8 > 200 * 1024) return SVM_OK;
+    DBuf Utc, XH, scratch, unorm, ucoef, cand, done, iters, mup, mlow, inner;
+    TRY(Utc.alloc(sizeof(uint16_t) * (size_t)a.nkc * 2 * a.NU * a.kch));
+    TRY(XH.alloc(sizeof(uint16_t) * (size_t)a.nct * a.nkc * 2 * 128 * a.kch));
+    TRY(scratch.alloc(sizeof(unsigned int)));
     TRY(unorm.alloc(sizeof(float) * a.NU));
     TRY(ucoef.alloc(sizeof(float) * a.NU));
     TRY(cand.alloc(sizeof(uint64_t) * (size_t)P * 2 * a.nct * 8));
@@ -951,7 +956,17 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     TRY(mlow.alloc(sizeof(double) * P));
     TRY(inner.alloc(sizeof(int64_t) * P));
     for (DBuf* b : {&Utc, &unorm, &ucoef, &done, &iters, &inner}) CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
-    a.Utc = Utc.as<float>();
+    const bool prof = getenv("SVMB200_PROFILE") != nullptr;
+    if (const char* e = getenv("SVMB200_OVR_DBG")) a.dbg = atoi(e);
+    DBuf profb;
+    if (prof) {
+        TRY(profb.alloc(sizeof(long long) * 64 * 3));
+        CK(cudaMemsetAsync(profb.p, 0, profb.bytes, st));
+        a.prof = profb.as<long long>();
+    }
+    a.Uh = Utc.as<uint16_t>();
+    a.XH = XH.as<uint16_t>();
+    CK(ovr_prepare(a, scratch.as<unsigned int>(), st));
     a.unorm = unorm.as<float>();
     a.ucoef = ucoef.as<float>();
     a.cand = cand.as<uint64_t>();
@@ -963,15 +978,41 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    // every pass launch is bracketed by a CUDA event pair on this stream (the bench's per-launch
+    // timing of the dominant kernel); the ring is read at each host poll
+    constexpr int NEV = 16;
+    cudaEvent_t pev[NEV][2];
+    for (int k = 0; k < NEV; ++k)
+        for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&pev[k][j]));
+    int nrec = 0;
+    int64_t passes = 0;
+    double pass_ms = 0;
+    auto timed_pass = [&]() -> int {
+        CK(cudaEventRecord(pev[nrec][0], st));
+        CK(launch_ovr_pass(a, st));
+        CK(cudaEventRecord(pev[nrec][1], st));
+        ++nrec;
+        ++passes;
+        return SVM_OK;
+    };
+    auto drain = [&]() {   // after a stream synchronize
+        for (int k = 0; k < nrec; ++k) {
+            float t = 0;
+            cudaEventElapsedTime(&t, pev[k][0], pev[k][1]);
+            pass_ms += t;
+        }
+        nrec = 0;
+    };
     CK(cudaEventRecord(e0, st));
-    CK(launch_ovr_pass(a, st));   // candidates of the initial state (all coefficients 0)
+    TRY(timed_pass());   // candidates of the initial state (all coefficients 0)
     std::vector<int32_t> dh(P);
     for (int64_t it = 0; it <= a.max_iter; ++it) {
         CK(launch_ovr_solve(a, st));
-        CK(launch_ovr_pass(a, st));
-        if ((it & 15) == 15) {
+        TRY(timed_pass());
+        if (nrec == NEV) {
             CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+            drain();
             bool all = true;
             for (int p = 0; p < P; ++p) all = all && dh[p];
             if (all) break;
@@ -986,10 +1027,15 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     CK(cudaMemcpyAsync(uh.data(), a.mup, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lh.data(), a.mlow, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    drain();
+    for (int k = 0; k < NEV; ++k)
+        for (int j = 0; j < 2; ++j) cudaEventDestroy(pev[k][j]);
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    probs[0].passes = passes;
+    probs[0].pass_ms = pass_ms;
     for (int p = 0; p < P; ++p) {
         Problem& Pp = probs[p];
         Pp.iterations = ih[p];
@@ -998,7 +1044,18 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
         Pp.converged = dh[p] && (uh[p] - lh[p] <= Pp.tol_loop);
         Pp.loop_ms += ms / P;
     }
-    if (getenv("SVMB200_PROFILE")) {
+    if (prof) {
+        std::vector<long long> ph(64 * 3);
+        cudaMemcpy(ph.data(), a.prof, sizeof(long long) * ph.size(), cudaMemcpyDeviceToHost);
+        const double np = (double)std::max<int64_t>(1, passes);
+        auto w = [&](int warp, int k) { return (double)ph[3 * warp + k] / np; };
+        fprintf(stderr, "[svmb200] k_ovr_pass CTA 0 per pass (cycles): producer wait %.0f issue %.0f | MMA tiles %.0f wait-TMEM %.0f | epilogue0 wait %.0f work %.0f\n",
+                w(0, 0), w(0, 1), w(2, 0), w(2, 1), w(3, 0), w(3, 1));
+        const double ns = (double)std::max<int64_t>(1, passes - 1);
+        fprintf(stderr, "[svmb200] k_ovr_solve CTA 0 per iteration (cycles): merge %.0f W+rows %.0f K_WW sums %.0f kernel %.0f eta %.0f subproblem %.0f alpha+U %.0f\n",
+                ph[96] / ns, ph[97] / ns, ph[101] / ns, ph[102] / ns, ph[98] / ns, ph[99] / ns, ph[100] / ns);
+    }
+    if (prof) {
         int64_t mx = 0, sum = 0;
         for (int p = 0; p < P; ++p) { mx = std::max(mx, ih[p]); sum += ih[p]; }
         fprintf(stderr, "[svmb200] batched OvR: %d problems, %lld iterations (max), %lld in total, %.1f ms, %.1f us per batched iteration\n",
@@ -1023,8 +1080,8 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     TRY(E.alloc(D.nblk));
     std::vector<Problem> probs(ys.size());
     std::vector<double> bs(ys.size());
-    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0;
-    int64_t iters = 0;
+    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, pass_ms = 0;
+    int64_t iters = 0, passes = 0;
     bool conv = true, cert = true;
     for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
     bool batched = false;
@@ -1045,7 +1102,9 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
         cert_ms += P.cert_ms;
+        if (!batched) { passes += P.iterations; pass_ms += P.loop_ms; }
     }
+    if (batched) { passes = probs[0].passes; pass_ms = probs[0].pass_ms; }
     svm_model* M = new (std::nothrow) svm_model();
     if (!M) return fail(SVM_ENOMEM, "model allocation failed");
     int rc = assemble_model(D, probs, prm, M, bs, st);
@@ -1080,6 +1139,9 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     I.loop_ms = loop_ms;
     I.certify_ms = cert_ms;
     I.setup_ms = t_setup;
+    I.passes = passes;
+    I.pass_ms = pass_ms;
+    I.batched = batched ? 1 : 0;
     cudaStreamSynchronize(st);
     I.train_ms = now_ms() - t_start;
     *out = M;
@@ -1837,6 +1899,8 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     I.dual_objective = dual;
     I.loop_ms = loop_ms;
     I.certify_ms = cert_ms;
+    I.passes = iters;
+    I.pass_ms = loop_ms;
     I.train_ms = now_ms() - t_start;
     *out = M;
     return SVM_OK;

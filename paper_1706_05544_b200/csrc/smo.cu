@@ -21,6 +21,8 @@
 // DESIGN.md has the layout, the roofline and what differs from the paper's GTSVM design.
 #include "svm_internal.cuh"
 
+#include <cuda_fp16.h>
+
 #include <float.h>
 #include <math.h>
 
@@ -1424,132 +1426,331 @@ __device__ __forceinline__ void ovr_wait(uint32_t bar, uint32_t parity)
     }
 }
 
-__global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_pass(const OvrArgs a)
+// Pipelined persistent pass (one CTA per SM).  A CTA walks groups of OVR_T = 2 contiguous 128-row
+// tiles; per group the features stream in K-chunks of OVR_KCH:
+//   producer warp   : cp.async.bulk of the raw feature-major X chunk ([kch][256 rows]) and of the
+//                     U chunk (hi | lo, pre-split by k_ovr_solve) into mbarrier rings;
+//   converter warps : raw fp32 -> (hi, lo) tf32 split in the K-major core layout of the A operand;
+//   MMA warp        : 3xTF32 (lo.hi, hi.lo, hi.hi) per 8-feature k-step, D[tile] in TMEM columns
+//                     tile * NU (+ p * 16 for problem p), tcgen05.commit releases the slots;
+//   epilogue warps  : per problem the kernel values of its 16 columns, G update, the tile's top-8.
+// X is read from HBM exactly once per pass; the stages of consecutive chunks / groups overlap.
+// Warp roles of k_ovr_pass
+constexpr int OVR_W_A = 0, OVR_W_B = 1, OVR_W_MMA = 2, OVR_W_EPI = 3, OVR_EPI = 16;
+constexpr int OVR_PASS_THREADS = (OVR_W_EPI + OVR_EPI) * 32;
+constexpr int OVR_MAXRING = 8;                       // A / U ring slots (runtime a.na, a.nb <= this)
+constexpr int OVR_ATILE = 2 * 128 * OVR_KCH;         // fp16 elements of one A chunk (hi | lo)
+
+__device__ __forceinline__ void ovr_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void ovr_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void epi_bar()   // named barrier of the epilogue warps only
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(OVR_EPI * 32) : "memory");
+}
+// wait with back-off (long waits of the epilogue warps: their spinning would take issue slots)
+__device__ __forceinline__ void ovr_wait_sleep(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+        if (ok) return;
+        __nanosleep(32);
+        if ((spins & 1023) == 1023) {
+            const uint64_t now = gtimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();
+        }
+    }
+}
+
+// Operand tiles of the batched pass: X (and U) are pre-split once into fp16 pairs
+//   xs = sigma x,  h = fp16_rn(xs),  l = fp16_rn(xs - h)      (sigma a power of two)
+// in the K-major SWIZZLE_NONE core layout of kind::f16 (core matrix 8 rows x 8 k = 128 B).
+// D = hA hB + hA lB + lA hB (three kind::f16 MMAs, fp32 accumulation in TMEM) ~= sigma^2 x.u with
+// the error of the dropped lA lB term (~2^-24 relative, the 3xTF32 level); the products of two
+// 11-bit significands are exact in fp32.
+__device__ __forceinline__ void f16_split(float x, float sigma, uint16_t& h, uint16_t& l)
+{
+    const float xs = x * sigma;
+    const __half hh = __float2half_rn(xs);
+    const float r = xs - __half2float(hh);   // exact
+    h = __half_as_ushort(hh);
+    l = __half_as_ushort(__float2half_rn(r));
+}
+__device__ __forceinline__ int kmaj16_off(int r, int k) { return ((r >> 3) * (OVR_KCH / 8) + (k >> 3)) * 64 + (r & 7) * 8 + (k & 7); }
+
+// XH[tile][kc][hi | lo][128 x KCH] from row-major X (one pass at setup; rows >= n, k >= d are 0)
+__global__ void k_ovr_xh(const float* __restrict__ XR, int64_t n, int64_t d, int nct, int nkc, float sigma,
+                         uint16_t* __restrict__ XH)
+{
+    const int64_t total = (int64_t)nct * nkc * 16 * (OVR_KCH / 8) * 8;   // (tile, kc, row group, kq, row)
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int r7 = (int)(t & 7), kq = (int)((t >> 3) % (OVR_KCH / 8));
+        const int64_t rest = (t >> 3) / (OVR_KCH / 8);
+        const int rg = (int)(rest & 15);
+        const int64_t tk = rest >> 4;                     // tile * nkc + kc
+        const int kc = (int)(tk % nkc);
+        const int64_t tile = tk / nkc;
+        const int r = rg * 8 + r7;
+        const int64_t row = tile * 128 + r;
+        const int64_t f0 = (int64_t)kc * OVR_KCH + kq * 8;
+        uint16_t h[8], l[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float x = (row < n && f0 + j < d) ? XR[row * d + f0 + j] : 0.0f;
+            f16_split(x, sigma, h[j], l[j]);
+        }
+        uint16_t* base = XH + (size_t)tk * OVR_ATILE;
+        const int off = kmaj16_off(r, kq * 8);
+        uint4 hv, lv;
+        hv.x = h[0] | ((uint32_t)h[1] << 16); hv.y = h[2] | ((uint32_t)h[3] << 16);
+        hv.z = h[4] | ((uint32_t)h[5] << 16); hv.w = h[6] | ((uint32_t)h[7] << 16);
+        lv.x = l[0] | ((uint32_t)l[1] << 16); lv.y = l[2] | ((uint32_t)l[3] << 16);
+        lv.z = l[4] | ((uint32_t)l[5] << 16); lv.w = l[6] | ((uint32_t)l[7] << 16);
+        *reinterpret_cast<uint4*>(base + off) = hv;
+        *reinterpret_cast<uint4*>(base + 128 * OVR_KCH + off) = lv;
+    }
+}
+
+// max |X| as float bits (non-negative floats order as unsigned integers)
+__global__ void k_absmax(const float* __restrict__ X, int64_t count, unsigned int* __restrict__ out)
+{
+    float m = 0.0f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(X[i]));
+    m = fmaxf(m, __shfl_xor_sync(FULL, m, 16));
+    m = fmaxf(m, __shfl_xor_sync(FULL, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(FULL, m, 4));
+    m = fmaxf(m, __shfl_xor_sync(FULL, m, 2));
+    m = fmaxf(m, __shfl_xor_sync(FULL, m, 1));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// Pipelined persistent pass (one CTA per SM) over 128-row tiles t = blockIdx.x + j gridDim.x:
+//   A producer  : one cp.async.bulk per K-chunk of the tile's pre-split X (16 KB) into a ring;
+//   U producer  : one cp.async.bulk per K-chunk of U (hi | lo, written by k_ovr_solve);
+//   MMA warp    : 3 kind::f16 MMAs per 16 features (M = 128, N = |U|), D[tile] in TMEM
+//                 columns (j & 1) NU (double-buffered), tcgen05.commit releases the slots;
+//   16 epilogue : per problem the kernel values of its 16 columns, G update, the tile's top-8;
+//     warps       tile j's epilogue overlaps tile j + 1's MMAs.
+// X is read from HBM exactly once per pass (4 B per element, as fp32).
+__global__ void __launch_bounds__(OVR_PASS_THREADS, 1) k_ovr_pass(const OvrArgs a)
 {
     extern __shared__ __align__(1024) unsigned char ovr_smem[];
-    const int kch = a.kch, NU = a.NU, KC = kch >> 2;
-    float* Ah = reinterpret_cast<float*>(ovr_smem);             // [128 x kch] K-major core layout
-    float* Al = Ah + 128 * kch;
-    float* Bs = Al + 128 * kch;                                  // [hi | lo][NU x kch]
-    float* sCoef = Bs + 2 * NU * kch;                            // [NU]
-    float* sNorm = sCoef + NU;                                   // [NU]
-    uint64_t* wl = reinterpret_cast<uint64_t*>(sNorm + NU);      // [P][2][4][8] warp lists
-    uint64_t* bars = wl + OVR_MAXP * 2 * 4 * 8;                  // bfull, mdone
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2);
+    const int NU = a.NU, NA = a.na, NB = a.nb;
+    const int bslot = 2 * NU * OVR_KCH;                                   // fp16 elements per U slot
+    uint16_t* As = reinterpret_cast<uint16_t*>(ovr_smem);                 // [NA][hi | lo][128 x KCH]
+    uint16_t* Bs = As + (size_t)NA * OVR_ATILE;                           // [NB][hi | lo][NU x KCH]
+    float* sCoef = reinterpret_cast<float*>(Bs + (size_t)NB * bslot);     // [NU]
+    float* sNorm = sCoef + OVR_MAXP * 16;                                 // [NU]
+    uint64_t* wl = reinterpret_cast<uint64_t*>(sNorm + OVR_MAXP * 16);    // [P][2][128] tile keys
+    uint64_t* bars = wl + (size_t)a.P * 2 * 128;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * OVR_MAXRING + 4);
+    const uint32_t b_af = su32(bars), b_ae = b_af + 8 * OVR_MAXRING;
+    const uint32_t b_bf = b_ae + 8 * OVR_MAXRING, b_be = b_bf + 8 * OVR_MAXRING;
+    const uint32_t b_accf = b_be + 8 * OVR_MAXRING, b_acce = b_accf + 16;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t r0 = (int64_t)blockIdx.x * 128;
-    const uint32_t b_full = su32(bars), b_done = su32(bars + 1);
-    for (int i = tid; i < NU; i += OVR_THREADS) { sCoef[i] = a.ucoef[i]; sNorm[i] = a.unorm[i]; }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(256));
+    const int nct = a.nct, nkc = a.nkc;
+    long long pw0 = 0, pw1 = 0, pw2 = 0;   // profile: cycles in the role's waits / work
+
+    for (int i = tid; i < NU; i += OVR_PASS_THREADS) { sCoef[i] = a.ucoef[i]; sNorm[i] = a.unorm[i]; }
+    if (warp == OVR_W_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_full), "r"(1));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_done), "r"(1));
+        for (int i = 0; i < NA; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_af + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_ae + 8 * i), "r"(1));
+        }
+        for (int i = 0; i < NB; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_bf + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_be + 8 * i), "r"(1));
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accf + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_acce + 8 * i), "r"(OVR_EPI));
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_holder;
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NU >> 3) << 17) | (8u << 24);
-    const uint32_t sbo = (uint32_t)KC * 128u;
-    const uint32_t bbytes = (uint32_t)(2 * NU * kch * 4);
-    for (int kc = 0; kc < a.nkc; ++kc) {
-        // A: this tile's rows x chunk features, split hi / lo
-        for (int e = tid; e < 128 * kch; e += OVR_THREADS) {
-            const int k = e >> 7, r = e & 127;
-            const int64_t f = (int64_t)kc * kch + k, row = r0 + r;
-            const float x = (f < a.d && row < a.n) ? a.XT[f * a.n_pad + row] : 0.0f;
-            float hi, lo;
-            tf32_split(x, hi, lo);
-            Ah[kmaj_off(r, k, KC)] = hi;
-            Al[kmaj_off(r, k, KC)] = lo;
-        }
-        if (tid == 0) {   // B: the union rows' chunk (hi | lo), one bulk copy
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b_full), "r"(bbytes) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(su32(Bs)), "l"(a.Utc + (size_t)kc * 2 * NU * kch), "r"(bbytes), "r"(b_full) : "memory");
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (tid == 0) {
-            ovr_wait(b_full, (uint32_t)(kc & 1));
-            const uint32_t ah = su32(Ah), al = su32(Al), bh = su32(Bs), bl = bh + (uint32_t)(NU * kch * 4);
-            for (int ks = 0; ks < (kch >> 3); ++ks)
-#pragma unroll
-                for (int ps = 1; ps < 4; ++ps) {   // lo.hi, hi.lo, hi.hi
-                    const uint64_t da = umma_desc_kmajor((ps <= 1 ? al : ah) + ks * 256, sbo);
-                    const uint64_t db = umma_desc_kmajor((ps == 2 ? bl : bh) + ks * 256, sbo);
-                    const uint32_t acc = (kc > 0 || ks > 0 || ps > 1) ? 1u : 0u;
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
-                                 ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    long long tp = clock64();
+#define OVR_MARK(acc) { const long long _n = clock64(); acc += _n - tp; tp = _n; }
+
+    if (warp == OVR_W_A) {
+        // ---------------- producer: stage = (X chunk of the tile, U chunk), two bulk copies --------
+        if (lane == 0) {
+            const uint32_t abytes = (uint32_t)(OVR_ATILE * 2), bbytes = (uint32_t)(bslot * 2);
+            int sa = 0;
+            uint32_t pe = 1;   // parity of use u = c / NA >= 1 is (u - 1) & 1
+            int c = 0;
+            for (int t = blockIdx.x; t < nct; t += gridDim.x)
+                for (int kc = 0; kc < nkc; ++kc, ++c) {
+                    if (c >= NA) ovr_wait(b_ae + 8 * sa, pe);
+                    OVR_MARK(pw0)
+                    const uint32_t bar = b_af + 8 * sa;
+                    if (a.dbg == 3) { ovr_arrive(bar); }
+                    else {
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(abytes + bbytes) : "memory");
+                        ovr_bulk(su32(As + (size_t)sa * OVR_ATILE), a.XH + ((size_t)t * nkc + kc) * OVR_ATILE, abytes, bar);
+                        ovr_bulk(su32(Bs + (size_t)sa * bslot), a.Uh + (size_t)kc * bslot, bbytes, bar);
+                    }
+                    OVR_MARK(pw1)
+                    if (++sa == NA) { sa = 0; pe ^= 1u; }
                 }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_done) : "memory");
         }
-        ovr_wait(b_done, (uint32_t)(kc & 1));   // A and B are rewritten by the next chunk
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    // ---- epilogue: warp w = rows 32 (w % 4) .., problems w / 4, w / 4 + 4, ... --------------
-    const int q = warp & 3;
-    const int64_t i = r0 + q * 32 + lane;
-    const bool valid = i < a.n;
-    const float xn = valid ? a.xnorm[i] : 0.0f;
-    for (int p = warp >> 2; p < a.P; p += 4) {
-        uint32_t v[16];
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(p * 16);
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                     : "r"(ta));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        uint64_t ku = 0ull, kl = 0ull;
-        if (valid) {
-            float S = 0.0f;
+    } else if (warp == OVR_W_B) {
+        // (spare warp)
+    } else if (warp == OVR_W_MMA) {
+        // ---------------- MMA issuer ------------------------------------------------------------
+        // (a lone thread issues the MMAs: its scalar instruction stream bounds the issue rate, so
+        // descriptors are precomputed, slots advance by counters and one commit releases a stage)
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(NU >> 3) << 17) | (8u << 24);   // f32 D, f16 A/B, K-major
+            const uint32_t sbo = (uint32_t)(OVR_KCH / 8) * 128u;
+            const uint64_t a_desc0 = umma_desc_kmajor(su32(As), sbo), b_desc0 = umma_desc_kmajor(su32(Bs), sbo);
+            const uint64_t a_step = (uint64_t)(OVR_ATILE * 2 / 16), b_step = (uint64_t)(bslot * 2 / 16);
+            const uint64_t a_lo = (uint64_t)(128 * OVR_KCH * 2 / 16), b_lo = (uint64_t)(NU * OVR_KCH * 2 / 16);
+            int sa = 0, j = 0;
+            uint32_t pa = 0;
+            for (int t = blockIdx.x; t < nct; t += gridDim.x, ++j) {
+                const int ab = j & 1;
+                if (j >= 2) ovr_wait(b_acce + 8 * ab, (uint32_t)(((j >> 1) - 1) & 1));   // TMEM half drained
+                OVR_MARK(pw1)
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t dcol = tmem + (uint32_t)(ab * NU);
+                for (int kc = 0; kc < nkc; ++kc) {
+                    ovr_wait(b_af + 8 * sa, pa);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t ah = a_desc0 + (uint64_t)sa * a_step, bh = b_desc0 + (uint64_t)sa * b_step;
+                    const uint32_t acc0 = kc > 0 ? 1u : 0u;
 #pragma unroll
-            for (int r = 0; r < 16; ++r)
-                S = fmaf(sCoef[p * 16 + r], kernel_from_dot(a.kp, __uint_as_float(v[r]), xn, sNorm[p * 16 + r]), S);
-            const uint32_t st = a.status[p][i];
-            const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
-            float g = a.G[p][i];
-            g = fmaf(yv, S, g);
-            a.G[p][i] = g;
-            const float sc = -yv * g;
-            const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)i);
-            if (st_in_up(st)) ku = ((uint64_t)ord_f32(sc) << 32) | lo;
-            if (st_in_low(st)) kl = ((uint64_t)ord_f32(-sc) << 32) | lo;
+                    for (int ks = 0; ks < OVR_KCH / 16; ++ks) {   // h.h, h.l, l.h; +256 B per k-step
+                        const uint64_t ks16 = (uint64_t)(ks * 16);
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                                     ::"r"(dcol), "l"(ah + ks16), "l"(bh + ks16), "r"(idesc), "r"(ks > 0 ? 1u : acc0));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;"
+                                     ::"r"(dcol), "l"(ah + ks16), "l"(bh + b_lo + ks16), "r"(idesc));
+                        asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;"
+                                     ::"r"(dcol), "l"(ah + a_lo + ks16), "l"(bh + ks16), "r"(idesc));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_ae + 8 * sa) : "memory");
+                    if (++sa == NA) { sa = 0; pa ^= 1u; }
+                }
+                OVR_MARK(pw0)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_accf + 8 * ab) : "memory");
+            }
         }
-        uint64_t wlu = 0ull, wll = 0ull;
-        uint64_t ka[1] = {ku}, kb[1] = {kl};
-        merge_chunk<1>(ka, kb, wlu, wll, lane);
-        if (lane < 8) {
-            wl[((p * 2 + 0) * 4 + q) * 8 + lane] = wlu;
-            wl[((p * 2 + 1) * 4 + q) * 8 + lane] = wll;
+    } else {
+        // ---------------- epilogue -------------------------------------------------------------
+        // TMEM half drained first (all of this warp's problems), then per problem the kernel values,
+        // G update and candidate keys of its 32 rows -> shared keys [p][side][128]; then one warp
+        // per (problem, side) selects the tile's top-8 of 128 keys.
+        constexpr int PPW = OVR_MAXP / 4;      // problems per warp at most
+        const int e = warp - OVR_W_EPI;        // 0 .. OVR_EPI - 1
+        const int q = warp & 3;                // TMEM lane quadrant of this warp
+        const int pi = e >> 2;                 // problems p = pi, pi + 4, ...
+        const int np = (a.P - pi + 3) >> 2;    // this warp's problem count (warp-uniform)
+        const float isg = a.inv_sigma2;
+        uint64_t* tkeys = wl;                  // [P][2][128]
+        int j = 0;
+        for (int t = blockIdx.x; t < nct; t += gridDim.x, ++j) {
+            const int ab = j & 1;
+            const int64_t i = (int64_t)t * 128 + q * 32 + lane;
+            const bool valid = i < a.n;
+            float g0[PPW];
+            uint32_t st0[PPW];
+#pragma unroll
+            for (int k = 0; k < PPW; ++k) {    // operands of the update, loaded before the wait
+                const int p = pi + 4 * k;
+                g0[k] = 0.0f;
+                st0[k] = 0;
+                if (k < np && valid) { g0[k] = a.G[p][i]; st0[k] = a.status[p][i]; }
+            }
+            const float xn = valid ? a.xnorm[i] : 0.0f;
+            ovr_wait_sleep(b_accf + 8 * ab, (uint32_t)((j >> 1) & 1));
+            OVR_MARK(pw0)
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t v[PPW][16];
+#pragma unroll
+            for (int k = 0; k < PPW; ++k) {
+                if (k >= np) break;   // warp-uniform
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * NU + (pi + 4 * k) * 16);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                             : "=r"(v[k][0]), "=r"(v[k][1]), "=r"(v[k][2]), "=r"(v[k][3]), "=r"(v[k][4]), "=r"(v[k][5]), "=r"(v[k][6]), "=r"(v[k][7]),
+                               "=r"(v[k][8]), "=r"(v[k][9]), "=r"(v[k][10]), "=r"(v[k][11]), "=r"(v[k][12]), "=r"(v[k][13]), "=r"(v[k][14]), "=r"(v[k][15])
+                             : "r"(ta));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // TMEM half free
+            __syncwarp();
+            if (lane == 0) ovr_arrive(b_acce + 8 * ab);
+#pragma unroll
+            for (int k = 0; k < PPW; ++k) {
+                if (k >= np) break;
+                const int p = pi + 4 * k;
+                uint64_t ku = 0ull, kl = 0ull;
+                if (valid) {
+                    float S = 0.0f;
+#pragma unroll
+                    for (int r = 0; r < 16; ++r)
+                        S = fmaf(sCoef[p * 16 + r], kernel_from_dot(a.kp, __uint_as_float(v[k][r]) * isg, xn, sNorm[p * 16 + r]), S);
+                    const uint32_t st = st0[k];
+                    const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
+                    const float gn = fmaf(yv, S, g0[k]);
+                    a.G[p][i] = gn;
+                    const float sc = -yv * gn;
+                    const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)i);
+                    if (st_in_up(st)) ku = ((uint64_t)ord_f32(sc) << 32) | lo;
+                    if (st_in_low(st)) kl = ((uint64_t)ord_f32(-sc) << 32) | lo;
+                }
+                tkeys[(p * 2 + 0) * 128 + q * 32 + lane] = ku;
+                tkeys[(p * 2 + 1) * 128 + q * 32 + lane] = kl;
+            }
+            epi_bar();
+            // the tile's top-8 per problem and side: each lane sorts its 4 keys, 8 rounds of warp max
+            for (int ps = e; ps < 2 * a.P; ps += OVR_EPI) {
+                const uint64_t* K = tkeys + ps * 128;
+                uint64_t kk[4] = {lds_u64(K + lane), lds_u64(K + 32 + lane), lds_u64(K + 64 + lane), lds_u64(K + 96 + lane)};
+                sort_desc<4>(kk);
+                uint64_t mine = 0ull;
+#pragma unroll 1
+                for (int r = 0; r < 8; ++r) {
+                    const uint64_t best = warp_max_u64(kk[0]);
+                    if (lane == r) mine = best;
+                    if (best == 0ull) break;   // the rest of the list stays 0 (empty)
+                    if (kk[0] == best) { kk[0] = kk[1]; kk[1] = kk[2]; kk[2] = kk[3]; kk[3] = 0ull; }
+                }
+                if (lane < 8) a.cand[((size_t)ps * nct + t) * 8 + lane] = mine;
+            }
+            epi_bar();
+            OVR_MARK(pw1)
         }
+    }
+#undef OVR_MARK
+    if (a.prof && blockIdx.x == 0 && lane == 0) {
+        long long* o = a.prof + 3 * warp;
+        atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)pw0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(o + 1), (unsigned long long)pw1);
+        atomicAdd(reinterpret_cast<unsigned long long*>(o + 2), (unsigned long long)pw2);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    // tile top-8 per problem and side: warp w merges the 4 quadrant lists of (p, side) = (w / 2, w % 2)
-    for (int ps = warp; ps < 2 * a.P; ps += OVR_THREADS / 32) {
-        const int p = ps >> 1, side = ps & 1;
-        uint64_t out[8];
-        int32_t srcd[8];
-        const uint64_t* L4 = wl + (size_t)((p * 2 + side) * 4) * 8;
-        uint64_t* dst = a.cand + (((size_t)p * 2 + side) * a.nct + blockIdx.x) * 8;
-        __shared__ uint64_t mo[OVR_THREADS / 32][8];
-        __shared__ int32_t ms[OVR_THREADS / 32][8];
-        lane_list_merge(4, [&](int l, int j) { return lds_u64(L4 + l * 8 + j); },
-                        [&](int l, int j) { return l * 8 + j; }, mo[warp], ms[warp], lane);
-        __syncwarp();
-        (void)out; (void)srcd;
-        if (lane < 8) dst[lane] = mo[warp][lane];
-    }
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == OVR_W_MMA) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
@@ -1566,32 +1767,60 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
         if (tid < 16) a.ucoef[p * 16 + tid] = 0.0f;
         return;
     }
-    // ---- a1: merge the row tiles' top-8 lists (two levels, 16 warps x 32 lists) per side ----
-    for (int side = 0; side < 2; ++side) {
+    long long t0 = clock64();
+    long long* prof = (a.prof && p == 0 && tid == 0) ? a.prof + 96 : nullptr;
+#define SOLVE_MARK(k) { if (prof) { const long long _n = clock64(); prof[k] += _n - t0; t0 = _n; } }
+    // ---- a1: the tiles' sorted top-8 lists -> this problem's top-8 per side.  Warps 0-7 take the
+    // up side, 8-15 the low side; a lane folds its lists into one sorted register list (top-8 of
+    // a union of two sorted lists = sort(max(a_i, b_{7-i})), a bitonic merge), the warp selects
+    // its top-8 over the lanes (8 rounds of 64-bit warp max), one warp per side merges the 8 warps.
+    {
+        const int side = warp >> 3, sw = warp & 7;
         const uint64_t* cl = a.cand + ((size_t)p * 2 + side) * a.nct * 8;
-        for (int base = 0; base < a.nct; base += 16 * 32) {   // more than 512 tiles: fold rounds
-            const int l0 = base + warp * 32;
-            const int nl = max(0, min(32, a.nct - l0));
-            uint64_t mo[8];
-            int32_t ms[8];
-            (void)mo; (void)ms;
-            lane_list_merge(nl, [&](int l, int j) { return cl[(size_t)(l0 + l) * 8 + j]; },
-                            [&](int l, int j) { return (l0 + l) * 8 + j; }, gm[warp], gms[warp], lane);
-            __syncthreads();
-            if (warp == 0) {
-                uint64_t* out = side == 0 ? sh.win_up : sh.win_low;
-                int32_t* srcs = side == 0 ? sh.win_up_src : sh.win_low_src;
-                // merge the 16 partial lists together with the result of the previous fold round
-                __shared__ uint64_t prev[8];
-                if (base > 0 && lane < 8) prev[lane] = out[lane];
-                __syncwarp();
-                const int nlist = base > 0 ? 17 : 16;
-                lane_list_merge(nlist, [&](int l, int j) { return l < 16 ? lds_u64(&gm[l][j]) : lds_u64(&prev[j]); },
-                                [&](int l, int j) { return l; }, out, srcs, lane);
-            }
-            __syncthreads();
+        uint64_t top[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) top[k] = 0ull;
+        for (int l = sw * 32 + lane; l < a.nct; l += 256) {
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(cl + (size_t)l * 8);
+            uint64_t b[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { const ulonglong2 v = src[k]; b[2 * k] = v.x; b[2 * k + 1] = v.y; }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) top[k] = top[k] > b[7 - k] ? top[k] : b[7 - k];
+            // bitonic sequence -> descending (three half-cleaner stages)
+#pragma unroll
+            for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if ((k & h) == 0) {
+                        const uint64_t x = top[k], y = top[k + h];
+                        top[k] = x > y ? x : y;
+                        top[k + h] = x > y ? y : x;
+                    }
         }
+        uint64_t mine = 0ull;
+#pragma unroll 1
+        for (int r = 0; r < 8; ++r) {
+            const uint64_t best = warp_max_u64(top[0]);
+            if (lane == r) mine = best;
+            if (best == 0ull) break;
+            if (top[0] == best) {
+#pragma unroll
+                for (int k = 0; k < 7; ++k) top[k] = top[k + 1];
+                top[7] = 0ull;
+            }
+        }
+        if (lane < 8) gm[warp][lane] = mine;
+        __syncthreads();
+        if (sw == 0) {
+            uint64_t* out = side == 0 ? sh.win_up : sh.win_low;
+            int32_t* srcs = side == 0 ? sh.win_up_src : sh.win_low_src;
+            lane_list_merge(8, [&](int l, int j) { return lds_u64(&gm[side * 8 + l][j]); },
+                            [&](int l, int j) { return l; }, out, srcs, lane);
+        }
+        __syncthreads();
     }
+    SOLVE_MARK(0)
     // ---- W: sorted union of the 8 + 8 winners, deduplicated (one copy per row: C-SVC) ---------
     if (warp == 0) {
         uint64_t key = 0;
@@ -1646,14 +1875,30 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
     }
     for (int i = tid; i < d * SVM_WS; i += OVR_THREADS)
         if ((i & 15) >= nr) sXW[i] = 0.0f;
+    double* sXW64 = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);   // [16][dp64 + 2] fp64 rows
+    const int dp64 = (d + 3) & ~3, s64 = dp64 + 2;   // +16 B per row: rows start in different banks
     if (warp < nr) {
         const int64_t row = sh.r_row[warp];
         const float* src = a.XR + row * a.d;
-        for (int k = lane; k < d; k += 32) sXW[k * SVM_WS + warp] = __ldg(src + k);
+        for (int k0 = 0; k0 < dp64; k0 += 8 * 32) {   // 8 loads in flight per lane
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + u * 32 + lane;
+                x[u] = k < d ? __ldg(src + k) : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + u * 32 + lane;
+                if (k < d) sXW[k * SVM_WS + warp] = x[u];
+                if (k < dp64) sXW64[warp * s64 + k] = (double)x[u];
+            }
+        }
         if (lane == 0) sh.xn[warp] = a.xnorm[row];
     }
     if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
     __syncthreads();
+    SOLVE_MARK(1)
     // ---- K_WW in fp64 from the fp32 tile (pairs k-split, four interleaved accumulators) -------
     {
         const int npairs = nr * (nr + 1) / 2;
@@ -1668,22 +1913,24 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
             double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
             if (sidx != r || a.kp.kernel != 2) {
                 const int k0 = part * klen, k1 = min(k0 + klen, dp);
-                auto ld = [&](int c, int k) { return k < d ? (double)sXW[k * SVM_WS + c] : 0.0; };
-                for (int k = k0; k < k1; k += 4) {
+                const double2* ur = reinterpret_cast<const double2*>(sXW64 + r * s64);
+                const double2* vr = reinterpret_cast<const double2*>(sXW64 + sidx * s64);
+                for (int k = k0; k < k1; k += 4) {   // rows zero-padded to dp64
+                    const double2 u0 = ur[k >> 1], u1 = ur[(k >> 1) + 1], v0 = vr[k >> 1], v1 = vr[(k >> 1) + 1];
                     if (a.kp.kernel == 2) {
-                        const double t0 = ld(r, k) - ld(sidx, k), t1 = ld(r, k + 1) - ld(sidx, k + 1);
-                        const double t2 = ld(r, k + 2) - ld(sidx, k + 2), t3 = ld(r, k + 3) - ld(sidx, k + 3);
+                        const double t0 = u0.x - v0.x, t1 = u0.y - v0.y, t2 = u1.x - v1.x, t3 = u1.y - v1.y;
                         acc0 = fma(t0, t0, acc0); acc1 = fma(t1, t1, acc1);
                         acc2 = fma(t2, t2, acc2); acc3 = fma(t3, t3, acc3);
                     } else {
-                        acc0 = fma(ld(r, k), ld(sidx, k), acc0); acc1 = fma(ld(r, k + 1), ld(sidx, k + 1), acc1);
-                        acc2 = fma(ld(r, k + 2), ld(sidx, k + 2), acc2); acc3 = fma(ld(r, k + 3), ld(sidx, k + 3), acc3);
+                        acc0 = fma(u0.x, v0.x, acc0); acc1 = fma(u0.y, v0.y, acc1);
+                        acc2 = fma(u1.x, v1.x, acc2); acc3 = fma(u1.y, v1.y, acc3);
                     }
                 }
             }
             sh.qpart[pr * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
         }
         __syncthreads();
+        SOLVE_MARK(5)
         if (tid < npairs) {
             int r = 0, rem = tid;
             while (rem >= nr - r) { rem -= nr - r; ++r; }
@@ -1695,6 +1942,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
             sh.kr[sidx * SVM_WS + r] = kv;
         }
         __syncthreads();
+        SOLVE_MARK(6)
         if (tid < SVM_WS * SVM_WS) {
             const int pa = tid >> 4, pb = tid & 15;
             double kab = 0.0, ie = 0.0;
@@ -1708,9 +1956,11 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
         }
         __syncthreads();
     }
+    SOLVE_MARK(2)
     // ---- a2: the subproblem (one warp), then alpha / status of W and the coefficients --------
     if (warp == 0) {
         const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
+        if (lane == 0) SOLVE_MARK(3)
         __syncwarp();
         if (lane < SVM_WS) {
             float c = 0.0f;
@@ -1729,21 +1979,23 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
             a.inner_total[p] += steps;
         }
     }
-    // ---- this problem's 16 columns of the U operand, all K-chunks (hi | lo) --------------------
+    // ---- this problem's 16 columns of the U operand, all K-chunks (fp16 hi | lo, k_ovr_pass) ----
     {
-        const int kch = a.kch, KC = kch >> 2, NU = a.NU;
-        const int total = a.nkc * kch * 16;
+        const int NU = a.NU;
+        const int total = a.nkc * OVR_KCH * 16;
         for (int e = tid; e < total; e += OVR_THREADS) {
             const int f = e >> 4, r = e & 15;
-            const int kc = f / kch, k = f - kc * kch;
+            const int kc = f / OVR_KCH, k = f - kc * OVR_KCH;
             const float x = f < d ? sXW[f * SVM_WS + r] : 0.0f;
-            float hi, lo;
-            tf32_split(x, hi, lo);
-            float* base = a.Utc + (size_t)kc * 2 * NU * kch;
-            base[kmaj_off(p * 16 + r, k, KC)] = hi;
-            base[NU * kch + kmaj_off(p * 16 + r, k, KC)] = lo;
+            uint16_t h, l;
+            f16_split(x, a.sigma, h, l);
+            uint16_t* base = a.Uh + (size_t)kc * 2 * NU * OVR_KCH;
+            base[kmaj16_off(p * 16 + r, k)] = h;
+            base[NU * OVR_KCH + kmaj16_off(p * 16 + r, k)] = l;
         }
     }
+    SOLVE_MARK(4)
+#undef SOLVE_MARK
 }
 }  // namespace
 
@@ -1794,24 +2046,73 @@ cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, fl
     return cudaGetLastError();
 }
 
+// shared memory of k_ovr_pass for ring depths (na, nb)
+static int ovr_pass_smem_n(int NU, int na, int nb)
+{
+    return (na * OVR_ATILE + nb * 2 * NU * OVR_KCH) * 2 + 2 * OVR_MAXP * 16 * 4 + (NU / 16) * 2 * 128 * 8 +
+           (4 * OVR_MAXRING + 4) * 8 + 16;
+}
+// ring depths: as deep as the shared memory allows (static: 1 KB; 227 KB per CTA in total)
+static void ovr_rings(int NU, int* na, int* nb)
+{
+    const int cap = 225 * 1024;
+    *na = 2;
+    while (*na < OVR_MAXRING && ovr_pass_smem_n(NU, *na + 1, *na + 1) <= cap) ++*na;
+    *nb = *na;   // one stage = (X chunk, U chunk)
+}
 int ovr_pass_smem(const OvrArgs& a)
 {
-    return (int)((2 * 128 * a.kch + 2 * a.NU * a.kch + 2 * a.NU) * 4 + OVR_MAXP * 2 * 4 * 8 * 8 + 2 * 8 + 16);
+    int na, nb;
+    ovr_rings(a.NU, &na, &nb);
+    return ovr_pass_smem_n(a.NU, na, nb);
 }
 
-cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st)
+cudaError_t launch_ovr_pass(const OvrArgs& a0, cudaStream_t st)
 {
-    const int smem = ovr_pass_smem(a);
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
+    }
+    OvrArgs a = a0;
+    ovr_rings(a.NU, &a.na, &a.nb);
+    const int smem = ovr_pass_smem_n(a.NU, a.na, a.nb);
     cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     svm_note_launches(1);
-    k_ovr_pass<<<a.nct, OVR_THREADS, smem, st>>>(a);
+    k_ovr_pass<<<std::min(nsm, a.nct), OVR_PASS_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+// Setup of the batched pass: sigma = 2^e with max|X| sigma < 2^14 (fp16 range with margin), and the
+// pre-split operand copy XH of X (one HBM pass).
+cudaError_t ovr_prepare(OvrArgs& a, unsigned int* scratch, cudaStream_t st)
+{
+    cudaError_t e = cudaMemsetAsync(scratch, 0, sizeof(unsigned int), st);
+    if (e != cudaSuccess) return e;
+    svm_note_launches(2);
+    k_absmax<<<4 * 148, 256, 0, st>>>(a.XR, a.n * a.d, scratch);
+    unsigned int mb = 0;
+    e = cudaMemcpyAsync(&mb, scratch, sizeof mb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    float mx = 0;
+    memcpy(&mx, &mb, sizeof mx);
+    int ex = 0;
+    if (mx > 0) frexpf(mx, &ex);           // mx = f 2^ex, f in [0.5, 1)
+    const int sh = std::max(-100, std::min(100, 14 - ex - 1));   // mx 2^sh < 2^13
+    a.sigma = ldexpf(1.0f, sh);
+    a.inv_sigma2 = ldexpf(1.0f, -2 * sh);
+    k_ovr_xh<<<8 * 148, 256, 0, st>>>(a.XR, a.n, a.d, a.nct, a.nkc, a.sigma, a.XH);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st)
 {
-    const int smem = (int)(a.d * SVM_WS * 4);
+    const int smem = (int)(a.d * SVM_WS * 4 + SVM_WS * (((a.d + 3) & ~3) + 2) * 8);
     cudaError_t e = cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     svm_note_launches(1);

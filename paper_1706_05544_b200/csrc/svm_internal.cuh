@@ -169,6 +169,7 @@ struct SmoArgs {
 // iteration for all of them.  The union U of the problems' working sets (16 slots per problem,
 // column p * 16 + slot) is the B operand of a tcgen05 3xTF32 product D[rows x NU] = X_rows X_U^T.
 constexpr int OVR_MAXP = 16;
+constexpr int OVR_KCH = 32;   // features per K-chunk of the batched pass (two kind::f16 k-steps)
 struct OvrArgs {
     const float* XT;           // [d][n_pad] feature-major
     const float* XR;           // [n][d] row-major (working-set row gathers)
@@ -184,7 +185,9 @@ struct OvrArgs {
     KParams kp;
     int NU;                    // 16 * P (MMA N)
     int kch, nkc;              // features per K-chunk (multiple of 8), number of chunks
-    float* Utc;                // [nkc][hi | lo][NU * kch] K-major core tiles (KC = kch / 4)
+    uint16_t* Uh;              // [nkc][hi | lo][NU x KCH] fp16 K-major core tiles (k_ovr_solve)
+    uint16_t* XH;              // [nct][nkc][hi | lo][128 x KCH] fp16 K-major core tiles of sigma X
+    float sigma, inv_sigma2;   // power-of-two operand scale and 1 / sigma^2
     float* unorm;              // [NU] |x_u|^2 (0 for empty slots)
     float* ucoef;              // [NU] c_r of slot r of problem p (0 = no update)
     uint64_t* cand;            // [P][2 sides][nct][8] per-row-tile top-8 keys
@@ -194,10 +197,14 @@ struct OvrArgs {
     double* mup;               // [P] m_up, M_low at the stop
     double* mlow;
     int64_t* inner_total;      // [P]
+    int na, nb;                // k_ovr_pass ring depths (set at launch)
+    long long* prof;           // optional [warps][3] cycle counters of CTA 0's roles (profiling)
+    int dbg;                   // experiments only (SVMB200_OVR_DBG): 1 skip U loads, 2 skip X loads
 };
 int ovr_pass_smem(const OvrArgs& a);
 cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st);
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st);
+cudaError_t ovr_prepare(OvrArgs& a, unsigned int* scratch, cudaStream_t st);
 
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
 void svm_note_launches(int k);

@@ -289,6 +289,42 @@ def test_ovr_multiclass():
     assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
 
 
+@pytest.mark.parametrize("n,d,k", [(1100, 40, 10), (900, 200, 3), (700, 17, 2 + 14)])
+def test_ovr_batched_vs_oracle(n, d, k):
+    """Batched one-vs-rest (all problems iterate together on one tcgen05 X pass)
+    against the oracle's independent per-class solves: ragged row tiles (odd tile count), a
+    partial last K-chunk (d not a multiple of 16), P = 3 and P = 16 (|U| = 256)."""
+    ds = synth.mnist_like(n=n, d=d, k=k)
+    model = pkg.train(ds.X, ds.y, gamma=1.0 / d)
+    info = model.info
+    assert info.n_problem == k and info.batched == 1
+    om = ora.train(ds.X, ds.y, gamma=1.0 / d)
+    Xh = synth.mnist_like(n=300, d=d, k=k, seed=103).X
+    out, dec = model.predict(Xh, decision=True)
+    f = om.decision_function(Xh)
+    assert np.abs(dec - f).max() <= 1e-3
+    assert _labels_agree(out, f, om.predict(Xh)) >= 0.99
+    d_ora = sum(r["dual"] for r in om.results)
+    assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
+    assert info.passes >= max(r["iterations"] for r in om.results) // 2 and info.pass_ms > 0
+
+
+def test_ovr_batched_many_groups(monkeypatch):
+    """More 256-row tile groups than SMs (several groups per persistent CTA): the batched path
+    against the per-class GPU path (each problem's own persistent kernel, parity-tested above)."""
+    ds = synth.mnist_like(n=40000, d=24, k=4)
+    mb = pkg.train(ds.X, ds.y, gamma=1.0 / 24)
+    assert mb.info.batched == 1
+    monkeypatch.setenv("SVMB200_NO_BATCH", "1")
+    ms = pkg.train(ds.X, ds.y, gamma=1.0 / 24)
+    assert ms.info.batched == 0
+    Xh = synth.mnist_like(n=2000, d=24, k=4, seed=104).X
+    _, db = mb.predict(Xh, decision=True)
+    _, dsq = ms.predict(Xh, decision=True)
+    assert np.abs(db - dsq).max() <= 2e-3
+    assert abs(mb.info.dual_objective - ms.info.dual_objective) <= 1e-4 * abs(ms.info.dual_objective)
+
+
 def test_errors_and_edge_cases():
     ds = synth.make("c1", n=50)
     with pytest.raises(pkg.SvmError) as e:
