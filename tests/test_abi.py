@@ -32,11 +32,35 @@ def test_binding_names_match_header():
     assert set(binding.SIGNATURES) == set(header_functions())
 
 
-def test_struct_layouts():
-    # the ctypes mirrors must match the C layout sizes (offsets of the last fields)
-    assert ctypes.sizeof(binding.svm_params) == 88
-    assert binding.svm_model_info.certify_ms.offset + 8 == ctypes.sizeof(binding.svm_model_info)
-    assert ctypes.sizeof(binding.svm_solver_stats) % 8 == 0
+def test_struct_layouts(tmp_path):
+    """The ctypes mirrors match the C layouts of include/svmb200.h: sizes and every field offset,
+    as the host C compiler lays them out."""
+    import shutil
+    import subprocess
+    structs = [binding.svm_params, binding.svm_model_info, binding.svm_solver_stats]
+    if shutil.which("gcc") is None:
+        assert ctypes.sizeof(binding.svm_params) == 88
+        return
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "svmb200.h"', "int main(void) {"]
+    for st in structs:
+        name = st.__name__
+        src.append(f'printf("{name} sizeof %zu\\n", sizeof({name}));')
+        for f, _ in st._fields_:
+            src.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    src.append("return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    inc = os.path.join(ROOT, "include")
+    subprocess.run(["gcc", "-I", inc, "-I", "/usr/local/cuda/include", str(c), "-o", str(exe)],
+                   check=True, capture_output=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for st in structs:
+        name = st.__name__
+        assert got[(name, "sizeof")] == ctypes.sizeof(st), name
+        for f, _ in st._fields_:
+            assert got[(name, f)] == getattr(st, f).offset, (name, f)
 
 
 def test_params_default_and_invalid_arguments():
