@@ -284,11 +284,12 @@ __global__ void k_gather_sv(const float* __restrict__ XT, int64_t n_pad, int64_t
                             int64_t nsv, int64_t nsv_pad, float* __restrict__ SVT,
                             float* __restrict__ svnorm)
 {
+    // grid.y splits the features (a handful of SVs must still fill the machine)
     int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nsv_pad) return;
     int64_t i = s < nsv ? sv_idx[s] : -1;
-    for (int64_t k = 0; k < d; ++k) SVT[k * nsv_pad + s] = i >= 0 ? XT[k * n_pad + i] : 0.0f;
-    svnorm[s] = i >= 0 ? xnorm[i] : 0.0f;
+    for (int64_t k = blockIdx.y; k < d; k += gridDim.y) SVT[k * nsv_pad + s] = i >= 0 ? XT[k * n_pad + i] : 0.0f;
+    if (blockIdx.y == 0) svnorm[s] = i >= 0 ? xnorm[i] : 0.0f;
 }
 
 // CSR rows -> dense feature-major columns [d][ld] starting at column 0 (zero-filled first)
@@ -507,8 +508,9 @@ cudaError_t lay_gather_sv(const float* XT, int64_t n_pad, int64_t d, const float
                           float* svnorm, cudaStream_t st)
 {
     svm_note_launches(1);
-    k_gather_sv<<<nblocks(nsv_pad, 256), 256, 0, st>>>(XT, n_pad, d, xnorm, sv_idx, nsv, nsv_pad,
-                                                        SVT, svnorm);
+    const unsigned gx = (unsigned)nblocks(nsv_pad, 256);
+    const unsigned gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(d, (4 * 148 + gx - 1) / gx));
+    k_gather_sv<<<dim3(gx, gy), 256, 0, st>>>(XT, n_pad, d, xnorm, sv_idx, nsv, nsv_pad, SVT, svnorm);
     return cudaGetLastError();
 }
 cudaError_t lay_csr_to_XT(const int64_t* indptr, const int32_t* idx, const float* vals,

@@ -15,6 +15,7 @@
 #include <cstdio>
 #endif
 #include <cstdlib>
+#include <cstring>
 #include <algorithm>
 
 namespace {
@@ -541,6 +542,245 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TS));
 }
 
+// ---- d > 128: both operands streamed in K-chunks (fp16-split tensor-core operands, see
+// svm_internal.cuh).  Query tiles of 128 rows and SV blocks of 256 (MMA N) are pre-split once per
+// call into [tile][kc][hi | lo][rows x 32]; a persistent CTA walks work items (query tile, SV
+// split), each a run of SV blocks.  Warp 0 lane 0 streams stages (query chunk 16 KB + SV chunk
+// 32 KB) through an mbarrier ring, warp 2 lane 0 issues three kind::f16 MMAs per 16 features into
+// one of two TMEM accumulators (128 x 256 fp32 each), 16 epilogue warps (TMEM lanes 32 (w % 4),
+// columns 64 (w / 4 % 4)) turn the dots into kernel values and contract them with the block's
+// coefficients (fp32 per block, fp64 across blocks); the four column quarters are written as
+// separate partials and summed in a fixed order by k_reduce_splits (bit-reproducible).
+constexpr int DF_KCH = 32, DF_SVB = 256, DF_EPI = 16;
+constexpr int DF_THREADS = (3 + DF_EPI) * 32;
+constexpr int DF_ATILE = 2 * 128 * DF_KCH, DF_BTILE = 2 * DF_SVB * DF_KCH;   // fp16 elements
+
+// [tile][kc][hi | lo][R x 32] from a feature-major fp32 matrix XT[d][ld] (rows >= nrows, k >= d -> 0)
+__global__ void k_split_tiles(const float* __restrict__ XT, int64_t ld, int64_t nrows, int64_t d, int R,
+                              int ntiles, int nkc, float sigma, uint16_t* __restrict__ out)
+{
+    const int RG = R / 8;
+    const int64_t total = (int64_t)ntiles * nkc * RG * (DF_KCH / 8) * 8;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int r7 = (int)(t & 7), kq = (int)((t >> 3) % (DF_KCH / 8));
+        const int64_t rest = (t >> 3) / (DF_KCH / 8);
+        const int rg = (int)(rest % RG);
+        const int64_t tk = rest / RG;                 // tile * nkc + kc
+        const int kc = (int)(tk % nkc);
+        const int64_t tile = tk / nkc;
+        const int r = rg * 8 + r7;
+        const int64_t row = tile * R + r;
+        const int64_t f0 = (int64_t)kc * DF_KCH + kq * 8;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+            uint16_t h0, l0, h1, l1;
+            const float x0 = (row < nrows && f0 + j < d) ? XT[(f0 + j) * ld + row] : 0.0f;
+            const float x1 = (row < nrows && f0 + j + 1 < d) ? XT[(f0 + j + 1) * ld + row] : 0.0f;
+            f16_split(x0, sigma, h0, l0);
+            f16_split(x1, sigma, h1, l1);
+            hw[j >> 1] = h0 | ((uint32_t)h1 << 16);
+            lw[j >> 1] = l0 | ((uint32_t)l1 << 16);
+        }
+        uint16_t* base = out + (size_t)tk * 2 * R * DF_KCH;
+        const int off = kmaj16_off_kc(r, kq * 8, DF_KCH / 8);
+        *reinterpret_cast<uint4*>(base + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(base + R * DF_KCH + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
+__device__ __forceinline__ void df_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void df_epi_bar()
+{
+    asm volatile("bar.sync 1, %0;" ::"n"(DF_EPI * 32) : "memory");
+}
+__device__ __forceinline__ void df_wait_sleep(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+        if (ok) return;
+        __nanosleep(32);
+        if ((spins & 1023) == 1023) {
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();
+        }
+    }
+}
+
+template <int NOUT>
+__global__ void __launch_bounds__(DF_THREADS, 1)
+    k_decision_f16(const uint16_t* __restrict__ QH, const float* __restrict__ qnorm, int64_t nq, int nqt,
+                   const uint16_t* __restrict__ SH, const float* __restrict__ svnorm,
+                   const float* __restrict__ coef32, int64_t nsv_ld, int nsb, int nkc, int n_out, KParams kp,
+                   float isg, int nsplit, int bps, int nstage, double* __restrict__ Fpart)
+{
+    extern __shared__ __align__(1024) unsigned char df_smem[];
+    uint16_t* As = reinterpret_cast<uint16_t*>(df_smem);                    // [NS][hi | lo][128 x 32]
+    uint16_t* Bs = As + (size_t)nstage * DF_ATILE;                           // [NS][hi | lo][256 x 32]
+    float* sCf = reinterpret_cast<float*>(Bs + (size_t)nstage * DF_BTILE);   // [2][NOUT][256]
+    float* sSn = sCf + 2 * NOUT * DF_SVB;                                    // [2][256]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sSn + 2 * DF_SVB);          // full[8] empty[8] accf[2] acce[2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 20);
+    const uint32_t b_full = su32(bars), b_empty = b_full + 64, b_accf = b_full + 128, b_acce = b_full + 144;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nitems = nqt * nsplit;
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < nstage; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_full + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_empty + 8 * i), "r"(1));
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_accf + 8 * i), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b_acce + 8 * i), "r"(DF_EPI));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        // ---------------- producer: stage = (query chunk, SV chunk) ------------------------------
+        if (lane == 0) {
+            const uint32_t abytes = DF_ATILE * 2, bbytes = DF_BTILE * 2;
+            int s = 0, c = 0;
+            uint32_t pe = 1;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int qt = it / nsplit, sp = it - qt * nsplit;
+                const int b0 = sp * bps, b1 = min(nsb, b0 + bps);
+                for (int sb = b0; sb < b1; ++sb)
+                    for (int kc = 0; kc < nkc; ++kc, ++c) {
+                        if (c >= nstage) mb_wait(b_empty + 8 * s, pe);
+                        const uint32_t bar = b_full + 8 * s;
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(abytes + bbytes) : "memory");
+                        bulk_g2s(su32(As + (size_t)s * DF_ATILE), QH + ((size_t)qt * nkc + kc) * DF_ATILE, abytes, bar);
+                        bulk_g2s(su32(Bs + (size_t)s * DF_BTILE), SH + ((size_t)sb * nkc + kc) * DF_BTILE, bbytes, bar);
+                        if (++s == nstage) { s = 0; pe ^= 1u; }
+                    }
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------- MMA issuer (lean loop: precomputed descriptors, counter slots) --------
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(DF_SVB >> 3) << 17) | (8u << 24);
+            const uint32_t sbo = (DF_KCH / 8) * 128u;
+            const uint64_t a0 = umma_desc_kmajor(su32(As), sbo), bd0 = umma_desc_kmajor(su32(Bs), sbo);
+            const uint64_t astep = DF_ATILE * 2 / 16, bstep = DF_BTILE * 2 / 16;
+            const uint64_t alo = 128 * DF_KCH * 2 / 16, blo = DF_SVB * DF_KCH * 2 / 16;
+            int s = 0, j = 0;
+            uint32_t pf = 0;
+            for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+                const int qt = it / nsplit, sp = it - qt * nsplit;
+                const int b0 = sp * bps, b1 = min(nsb, b0 + bps);
+                (void)qt;
+                for (int sb = b0; sb < b1; ++sb, ++j) {
+                    const int ab = j & 1;
+                    if (j >= 2) mb_wait(b_acce + 8 * ab, (uint32_t)(((j >> 1) - 1) & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t dcol = tmem + (uint32_t)(ab * DF_SVB);
+                    for (int kc = 0; kc < nkc; ++kc) {
+                        mb_wait(b_full + 8 * s, pf);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint64_t ah = a0 + (uint64_t)s * astep, bh = bd0 + (uint64_t)s * bstep;
+                        const uint32_t acc0 = kc > 0 ? 1u : 0u;
+#pragma unroll
+                        for (int ks = 0; ks < DF_KCH / 16; ++ks) {
+                            const uint64_t k16 = (uint64_t)(ks * 16);
+                            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                                         ::"r"(dcol), "l"(ah + k16), "l"(bh + k16), "r"(idesc), "r"(ks > 0 ? 1u : acc0));
+                            asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;"
+                                         ::"r"(dcol), "l"(ah + k16), "l"(bh + blo + k16), "r"(idesc));
+                            asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;"
+                                         ::"r"(dcol), "l"(ah + alo + k16), "l"(bh + k16), "r"(idesc));
+                        }
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_empty + 8 * s) : "memory");
+                        if (++s == nstage) { s = 0; pf ^= 1u; }
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b_accf + 8 * ab) : "memory");
+                }
+            }
+        }
+    } else if (warp >= 3) {
+        // ---------------- epilogue -------------------------------------------------------------
+        const int e = warp - 3, et = tid - 96;   // 0 .. 15, 0 .. 511
+        const int q = warp & 3, cq = (e >> 2) & 3;   // TMEM lane quadrant, column quarter
+        int j = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            const int qt = it / nsplit, sp = it - qt * nsplit;
+            const int b0 = sp * bps, b1 = min(nsb, b0 + bps);
+            const int64_t qi = (int64_t)qt * 128 + q * 32 + lane;
+            const float qn = qi < nq ? qnorm[qi] : 0.0f;
+            double facc[NOUT];
+#pragma unroll
+            for (int p = 0; p < NOUT; ++p) facc[p] = 0.0;
+            for (int sb = b0; sb < b1; ++sb, ++j) {
+                const int ab = j & 1;
+                float* cf = sCf + (size_t)ab * NOUT * DF_SVB;
+                float* sn = sSn + ab * DF_SVB;
+                for (int x = et; x < n_out * DF_SVB; x += DF_EPI * 32) {
+                    const int p = x / DF_SVB, c = x - p * DF_SVB;
+                    cf[p * DF_SVB + c] = coef32[(int64_t)p * nsv_ld + (int64_t)sb * DF_SVB + c];
+                }
+                if (et < DF_SVB) sn[et] = svnorm[(int64_t)sb * DF_SVB + et];
+                df_epi_bar();
+                df_wait_sleep(b_accf + 8 * ab, (uint32_t)((j >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t v[4][16];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * DF_SVB + cq * 64 + h * 16);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                 : "=r"(v[h][0]), "=r"(v[h][1]), "=r"(v[h][2]), "=r"(v[h][3]), "=r"(v[h][4]), "=r"(v[h][5]), "=r"(v[h][6]), "=r"(v[h][7]),
+                                   "=r"(v[h][8]), "=r"(v[h][9]), "=r"(v[h][10]), "=r"(v[h][11]), "=r"(v[h][12]), "=r"(v[h][13]), "=r"(v[h][14]), "=r"(v[h][15])
+                                 : "r"(ta));
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) df_arrive(b_acce + 8 * ab);
+                float part[NOUT];
+#pragma unroll
+                for (int p = 0; p < NOUT; ++p) part[p] = 0.0f;
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const int col = cq * 64 + h * 16 + c;
+                        const float kv = kernel_from_dot(kp, __uint_as_float(v[h][c]) * isg, qn, sn[col]);
+#pragma unroll
+                        for (int p = 0; p < NOUT; ++p)
+                            if (p < n_out) part[p] = fmaf(cf[p * DF_SVB + col], kv, part[p]);
+                    }
+#pragma unroll
+                for (int p = 0; p < NOUT; ++p) facc[p] += (double)part[p];
+            }
+            if (qi < nq) {
+                const int64_t count = nq * n_out;
+                double* dst = Fpart + (int64_t)(sp * 4 + cq) * count + qi * n_out;
+                for (int p = 0; p < n_out; ++p) dst[p] = facc[p];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // SV tiles for k_decision_tcp: [tile][hi | lo][TS * dp] in the K-major core layout
 __global__ void k_coef32(const double* __restrict__ coef, int64_t count, float* __restrict__ out)
 {
@@ -571,6 +811,9 @@ constexpr int decision_smem(int nout)
 
 }  // namespace
 
+static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
+                                     const float* SVT, const float* svnorm, int64_t nsv_pad, int64_t d,
+                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st);
 static double* g_fpart = nullptr;
 static size_t g_fpart_bytes = 0;
 
@@ -581,6 +824,10 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
 {
     (void)nsv;
     if (nq <= 0) return cudaSuccess;
+    if (d > 128 && nsv_pad > 0) {
+        const cudaError_t e = pred_decision_f16(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv_pad, d, coef, n_out, kp, F, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     // tcgen05 3xTF32 path for d <= 128 (query tile resident in shared memory)
     const bool tc = d <= 128 && n_out <= 16 && !getenv("SVMB200_NO_TC") && nq_pad % TQ == 0 && nsv_pad % TS == 0;
     int64_t q_tiles = nq_pad / (tc ? TQ : BQ), s_tiles = nsv_pad / (tc ? TS : BS);
@@ -666,6 +913,103 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     svm_note_launches(1);
     k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, splits, count, F);
     return cudaGetLastError();
+}
+
+// d > 128 on tcgen05 (fp16-split operands): pre-split query / SV tiles, persistent kernel,
+// partials per (split, column quarter) reduced in a fixed order.  Returns cudaErrorNotSupported when
+// the configuration is not covered (the caller falls back to the SIMT kernel).
+static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
+                                     const float* SVT, const float* svnorm, int64_t nsv_pad, int64_t d,
+                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st)
+{
+    if (d <= 128 || n_out > 16 || getenv("SVMB200_NO_TC") || getenv("SVMB200_NO_F16")) return cudaErrorNotSupported;
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
+    }
+    const int nkc = (int)((d + DF_KCH - 1) / DF_KCH);
+    const int nqt = (int)((nq + 127) / 128);
+    const int nsb = (int)((nsv_pad + DF_SVB - 1) / DF_SVB);
+    const int64_t nsv_ld = (int64_t)nsb * DF_SVB;
+    int nsplit = 1;
+    while (nsplit < nsb && (int64_t)nqt * nsplit < 4 * nsm) ++nsplit;
+    const int bps = (nsb + nsplit - 1) / nsplit;
+    nsplit = (nsb + bps - 1) / bps;
+    const size_t qh_b = (size_t)nqt * nkc * DF_ATILE * 2, sh_b = (size_t)nsb * nkc * DF_BTILE * 2;
+    const size_t cf_b = (size_t)n_out * nsv_ld * 4, sn_b = (size_t)nsv_ld * 4;
+    const size_t part_b = (size_t)nsplit * 4 * nq * n_out * 8;
+    // grow-only scratch (a stream-ordered allocation per call would return the memory to the OS at
+    // every synchronize: ~10 ms per call for the c3 certification's 200 MB)
+    static char* g_buf = nullptr;
+    static size_t g_buf_bytes = 0;
+    const size_t total = qh_b + sh_b + cf_b + sn_b + part_b + 256;
+    cudaError_t e = cudaSuccess;
+    if (total > g_buf_bytes) {
+        if (g_buf) {
+            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+            cudaFree(g_buf);
+            g_buf = nullptr;
+            g_buf_bytes = 0;
+        }
+        const size_t want = total + total / 4;
+        if ((e = cudaMalloc(reinterpret_cast<void**>(&g_buf), want)) != cudaSuccess) return e;
+        g_buf_bytes = want;
+    }
+    char* buf = g_buf;
+    uint16_t* QH = reinterpret_cast<uint16_t*>(buf);
+    uint16_t* SH = reinterpret_cast<uint16_t*>(buf + qh_b);
+    float* cf = reinterpret_cast<float*>(buf + qh_b + sh_b);
+    float* sn = reinterpret_cast<float*>(buf + qh_b + sh_b + cf_b);
+    double* part = reinterpret_cast<double*>(buf + qh_b + sh_b + cf_b + sn_b);
+    unsigned int* mx = reinterpret_cast<unsigned int*>(buf + qh_b + sh_b + cf_b + sn_b + part_b);
+    // sigma from max |x| over queries and SVs (one scale for both operands)
+    if ((e = cudaMemsetAsync(mx, 0, sizeof(unsigned int), st)) != cudaSuccess) goto out;
+    if ((e = launch_absmax(XqT, d * nq_pad, mx, st)) != cudaSuccess) goto out;
+    if ((e = launch_absmax(SVT, d * nsv_pad, mx, st)) != cudaSuccess) goto out;
+    {
+        unsigned int mb = 0;
+        if ((e = cudaMemcpyAsync(&mb, mx, sizeof mb, cudaMemcpyDeviceToHost, st)) != cudaSuccess) goto out;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) goto out;
+        float m = 0, sigma = 1, isg = 1;
+        memcpy(&m, &mb, sizeof m);
+        f16_sigma(m, &sigma, &isg);
+        svm_note_launches(4);
+        k_split_tiles<<<8 * nsm, 256, 0, st>>>(XqT, nq_pad, nq, d, 128, nqt, nkc, sigma, QH);
+        k_split_tiles<<<8 * nsm, 256, 0, st>>>(SVT, nsv_pad, nsv_pad, d, DF_SVB, nsb, nkc, sigma, SH);
+        if ((e = cudaMemsetAsync(cf, 0, cf_b + sn_b, st)) != cudaSuccess) goto out;
+        for (int p = 0; p < n_out; ++p) {
+            k_coef32<<<(unsigned)std::min<int64_t>((nsv_pad + 255) / 256, 148 * 16), 256, 0, st>>>(
+                coef + (int64_t)p * nsv_pad, nsv_pad, cf + (int64_t)p * nsv_ld);
+        }
+        svm_note_launches(n_out - 1);
+        if ((e = cudaMemcpyAsync(sn, svnorm, sizeof(float) * nsv_pad, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) goto out;
+        const int nout_t = n_out == 1 ? 1 : 16;
+        auto smem_for = [&](int ns) { return ns * (DF_ATILE + DF_BTILE) * 2 + (2 * nout_t * DF_SVB + 2 * DF_SVB) * 4 + 20 * 8 + 16; };
+        int nstage = 2;
+        while (nstage < 8 && smem_for(nstage + 1) <= 225 * 1024) ++nstage;
+        const int smem = smem_for(nstage);
+        const int grid = std::min(nsm, nqt * nsplit);
+        svm_note_launches(1);
+        if (n_out == 1) {
+            cudaFuncSetAttribute(k_decision_f16<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_decision_f16<1><<<grid, DF_THREADS, smem, st>>>(QH, qnorm, nq, nqt, SH, sn, cf, nsv_ld, nsb, nkc, n_out, kp,
+                                                              isg, nsplit, bps, nstage, part);
+        } else {
+            cudaFuncSetAttribute(k_decision_f16<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_decision_f16<16><<<grid, DF_THREADS, smem, st>>>(QH, qnorm, nq, nqt, SH, sn, cf, nsv_ld, nsb, nkc, n_out, kp,
+                                                               isg, nsplit, bps, nstage, part);
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) goto out;
+        const int64_t count = nq * n_out;
+        svm_note_launches(1);
+        k_reduce_splits<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(part, nsplit * 4, count, F);
+        e = cudaGetLastError();
+    }
+out:
+    return e;
 }
 
 int64_t pred_tc_dp(int64_t d)

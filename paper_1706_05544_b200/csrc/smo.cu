@@ -1478,14 +1478,6 @@ __device__ __forceinline__ void ovr_wait_sleep(uint32_t bar, uint32_t parity)
 // D = hA hB + hA lB + lA hB (three kind::f16 MMAs, fp32 accumulation in TMEM) ~= sigma^2 x.u with
 // the error of the dropped lA lB term (~2^-24 relative, the 3xTF32 level); the products of two
 // 11-bit significands are exact in fp32.
-__device__ __forceinline__ void f16_split(float x, float sigma, uint16_t& h, uint16_t& l)
-{
-    const float xs = x * sigma;
-    const __half hh = __float2half_rn(xs);
-    const float r = xs - __half2float(hh);   // exact
-    h = __half_as_ushort(hh);
-    l = __half_as_ushort(__float2half_rn(r));
-}
 __device__ __forceinline__ int kmaj16_off(int r, int k) { return ((r >> 3) * (OVR_KCH / 8) + (k >> 3)) * 64 + (r & 7) * 8 + (k & 7); }
 
 // XH[tile][kc][hi | lo][128 x KCH] from row-major X (one pass at setup; rows >= n, k >= d are 0)
@@ -2101,12 +2093,15 @@ cudaError_t ovr_prepare(OvrArgs& a, unsigned int* scratch, cudaStream_t st)
     if (e != cudaSuccess) return e;
     float mx = 0;
     memcpy(&mx, &mb, sizeof mx);
-    int ex = 0;
-    if (mx > 0) frexpf(mx, &ex);           // mx = f 2^ex, f in [0.5, 1)
-    const int sh = std::max(-100, std::min(100, 14 - ex - 1));   // mx 2^sh < 2^13
-    a.sigma = ldexpf(1.0f, sh);
-    a.inv_sigma2 = ldexpf(1.0f, -2 * sh);
+    f16_sigma(mx, &a.sigma, &a.inv_sigma2);
     k_ovr_xh<<<8 * 148, 256, 0, st>>>(a.XR, a.n, a.d, a.nct, a.nkc, a.sigma, a.XH);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cudaStream_t st)
+{
+    svm_note_launches(1);
+    k_absmax<<<4 * 148, 256, 0, st>>>(X, count, out);
     return cudaGetLastError();
 }
 

@@ -6,7 +6,9 @@
 // (P:59-69).  Layout and kernel design are in DESIGN.md.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #define SVM_MAX_RANKS 8
@@ -205,6 +207,8 @@ int ovr_pass_smem(const OvrArgs& a);
 cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st);
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st);
 cudaError_t ovr_prepare(OvrArgs& a, unsigned int* scratch, cudaStream_t st);
+// atomicMax of max |X[0 .. count)| as float bits into *out (caller zeroes *out)
+cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cudaStream_t st);
 
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
 void svm_note_launches(int k);
@@ -237,4 +241,33 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo)
 }
 __device__ __forceinline__ int kmaj_off(int r, int k, int KC) { return ((r >> 3) * KC + (k >> 2)) * 32 + (r & 7) * 4 + (k & 3); }
 
-
+// ---- fp16-split tensor-core operands (the batched pass in smo.cu, the d > 128 decision kernel in
+// predict.cu).  x is pre-split once into an fp16 pair with a power-of-two scale sigma:
+//   xs = sigma x,  h = fp16_rn(xs),  l = fp16_rn(xs - h)        (xs - h is exact in fp32)
+// and D = hA hB + hA lB + lA hB (three kind::f16 MMAs, fp32 accumulation) ~= sigma^2 x.u with the
+// error of the dropped lA lB term (~2^-24 relative, the 3xTF32 level); products of two 11-bit
+// significands are exact in fp32.  sigma puts max|x| sigma below 2^13 (fp16 range, no overflow).
+// Layout: K-major SWIZZLE_NONE core matrices of 8 rows x 8 k (128 B), KC8 = (k extent) / 8 per
+// 8-row group; LBO 128 B, SBO = KC8 x 128 B; one K = 16 MMA step advances 256 B.
+__device__ __forceinline__ void f16_split(float x, float sigma, uint16_t& h, uint16_t& l)
+{
+    const float xs = x * sigma;
+    const __half hh = __float2half_rn(xs);
+    const float r = xs - __half2float(hh);
+    h = __half_as_ushort(hh);
+    l = __half_as_ushort(__float2half_rn(r));
+}
+__device__ __forceinline__ int kmaj16_off_kc(int r, int k, int KC8)
+{
+    return ((r >> 3) * KC8 + (k >> 3)) * 64 + (r & 7) * 8 + (k & 7);
+}
+// sigma = 2^e with mx sigma < 2^13 (mx = max |x| over both operands), and 1 / sigma^2
+inline void f16_sigma(float mx, float* sigma, float* inv_sigma2)
+{
+    int ex = 0;
+    if (mx > 0) frexpf(mx, &ex);
+    int sh = 14 - ex - 1;
+    sh = sh < -100 ? -100 : (sh > 100 ? 100 : sh);
+    *sigma = ldexpf(1.0f, sh);
+    *inv_sigma2 = ldexpf(1.0f, -2 * sh);
+}
