@@ -34,6 +34,9 @@ constexpr int SOLVER_WARP = SMO_WARPS - 1;
 // 32 random features per warp, so the stride is padded to 20 floats (80 B = 5 x 16 B, coprime
 // with the 8 16-byte bank groups) -- with 16 all lanes fell into two bank groups (16-way conflict).
 constexpr int WSTR_CSR = 20;
+// CSR: the 16-bit group mask of X_W^T row k lives in one of the row's 4 padding words, chosen so
+// that 32 random rows hit 32 different banks (20 k mod 32 alone takes only 8 values)
+__device__ __forceinline__ int csr_mask_slot(int k) { return k * WSTR_CSR + 16 + ((k >> 3) & 3); }
 
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p, bool sys)
 {
@@ -124,6 +127,27 @@ __device__ __forceinline__ void fma_row16(float x, const float4 (&wv)[4], float*
         acc[4 * q + 1] = lo.y;
         acc[4 * q + 2] = hi.x;
         acc[4 * q + 3] = hi.y;
+    }
+}
+
+// CSR: acc[0..15] += x * X_W^T[k][0..15] reading only the 4-row groups of X_W with a nonzero at
+// feature k (16-bit mask m in the row's padding word, set while X_W is staged).  X_W rows are as
+// sparse as X (c5: ~1.6 of 16 nonzero), so most groups are skipped; a skipped group would add
+// x * 0, which leaves acc unchanged, so the result equals the dense update.
+__device__ __forceinline__ void fma_row16_masked(float x, const float4* w4k, uint32_t m, float* acc)
+{
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (m & (0xFu << (4 * q))) {
+            const float4 w = w4k[q];
+            const float2 xx = make_float2(x, x);
+            const float2 lo = __ffma2_rn(xx, make_float2(w.x, w.y), make_float2(acc[4 * q], acc[4 * q + 1]));
+            const float2 hi = __ffma2_rn(xx, make_float2(w.z, w.w), make_float2(acc[4 * q + 2], acc[4 * q + 3]));
+            acc[4 * q] = lo.x;
+            acc[4 * q + 1] = lo.y;
+            acc[4 * q + 2] = hi.x;
+            acc[4 * q + 3] = hi.y;
+        }
     }
 }
 
@@ -236,8 +260,8 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
     for (int64_t p = b; p < e; ++p) {
         int k = __ldg(indices + p);
         float v = __ldg(vals + p);
-        float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
-        fma_row16(v, wv, acc[0]);
+        const uint32_t m = __float_as_uint(sXW[csr_mask_slot(k)]);
+        fma_row16_masked(v, w4 + 5 * k, m, acc[0]);
     }
 }
 
@@ -265,9 +289,23 @@ __device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indp
         dots_csr(indptr, indices, vals, li, active, sXW, acc);
         return;
     }
-    for (int64_t p = z0 + lane; p < z1; p += 32) {
-        st_idx[p - z0] = (uint16_t)__ldg(indices + p);
-        st_val[p - z0] = __ldg(vals + p);
+    // 16 (index, value) loads in flight per lane before the shared-memory stores: the stage is a
+    // few memory round trips, not one per 32 nonzeros
+    const int cnt = (int)(z1 - z0);
+    for (int base = 0; base < cnt; base += 32 * 16) {
+        int32_t ii[16];
+        float vv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int q = base + u * 32 + lane;
+            ii[u] = q < cnt ? __ldg(indices + z0 + q) : 0;
+            vv[u] = q < cnt ? __ldg(vals + z0 + q) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int q = base + u * 32 + lane;
+            if (q < cnt) { st_idx[q] = (uint16_t)ii[u]; st_val[q] = vv[u]; }
+        }
     }
     __syncwarp();
     if (active) {
@@ -275,8 +313,8 @@ __device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indp
         for (int64_t p = b; p < e; ++p) {
             const int k = st_idx[p - z0];
             const float v = st_val[p - z0];
-            const float4 wv[4] = {w4[5 * k], w4[5 * k + 1], w4[5 * k + 2], w4[5 * k + 3]};
-            fma_row16(v, wv, acc[0]);
+            const uint32_t m = __float_as_uint(sXW[csr_mask_slot(k)]);
+            fma_row16_masked(v, w4 + 5 * k, m, acc[0]);
         }
     }
     __syncwarp();
@@ -1105,8 +1143,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 }
             } else {
                 const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
-                for (int64_t p = b + lane; p < e; p += 32)
-                    sXW[a.peer_indices[o][p] * WS + r] = a.peer_vals[o][p];
+                for (int64_t p = b + lane; p < e; p += 32) {
+                    const int k = a.peer_indices[o][p];
+                    const float v = a.peer_vals[o][p];
+                    sXW[k * WS + r] = v;
+                    if (v != 0.0f) atomicOr(reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);   // group mask
+                }
             }
             if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];
         }
@@ -1384,8 +1426,12 @@ __global__ void __launch_bounds__(256) kernel_rows_kernel(const SmoArgs a, const
     } else {
         for (int r = 0; r < nr; ++r) {
             int64_t b = a.peer_indptr[0][rows[r]], e = a.peer_indptr[0][rows[r] + 1];
-            for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x)
-                sXW[a.peer_indices[0][p] * WS + r] = a.peer_vals[0][p];
+            for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) {
+                const int k = a.peer_indices[0][p];
+                const float v = a.peer_vals[0][p];
+                sXW[k * WS + r] = v;
+                if (v != 0.0f) atomicOr(reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);
+            }
         }
     }
     if (threadIdx.x < SVM_WS) xn[threadIdx.x] = threadIdx.x < nr ? a.xnorm[rows[threadIdx.x]] : 0.0f;
