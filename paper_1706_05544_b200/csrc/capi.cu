@@ -941,8 +941,8 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     a.kch = OVR_KCH;
     a.nkc = (int)((D.d + a.kch - 1) / a.kch);
     a.nct = (int)((D.n + 127) / 128);
-    // k_ovr_solve stages X_W in fp32 and fp64: d (64 + 128) B + 96 B of shared memory
-    if (ovr_pass_smem(a) > 227 * 1024 || D.d * SVM_WS * 12 + SVM_WS * 6 * 8 > 200 * 1024) return SVM_OK;
+    // k_ovr_solve stages X_W in fp32 [d][16] and fp64 [d][24]: 256 B per feature of shared memory
+    if (ovr_pass_smem(a) > 227 * 1024 || ((D.d + 3) & ~3) * 256 + 20 * 1024 > 227 * 1024) return SVM_OK;
     DBuf Utc, XH, scratch, unorm, ucoef, cand, done, iters, mup, mlow, inner;
     TRY(Utc.alloc(sizeof(uint16_t) * (size_t)a.nkc * 2 * a.NU * a.kch));
     TRY(XH.alloc(sizeof(uint16_t) * (size_t)a.nct * a.nkc * 2 * 128 * a.kch));
@@ -998,18 +998,24 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     auto drain = [&]() {   // after a stream synchronize
         for (int k = 0; k < nrec; ++k) {
             float t = 0;
-            cudaEventElapsedTime(&t, pev[k][0], pev[k][1]);
+            const cudaError_t te = cudaEventElapsedTime(&t, pev[k][0], pev[k][1]);
+            if (te != cudaSuccess) {
+                cudaGetLastError();   // not sticky: clear it
+                if (getenv("SVMB200_PROFILE")) fprintf(stderr, "[svmb200] pass event %d: %s\n", k, cudaGetErrorString(te));
+            }
             pass_ms += t;
         }
         nrec = 0;
     };
     CK(cudaEventRecord(e0, st));
     TRY(timed_pass());   // candidates of the initial state (all coefficients 0)
+    CK(cudaStreamSynchronize(st));
+    drain();
     std::vector<int32_t> dh(P);
     for (int64_t it = 0; it <= a.max_iter; ++it) {
         CK(launch_ovr_solve(a, st));
         TRY(timed_pass());
-        if (nrec == NEV) {
+        if (nrec == NEV) {   // host poll of the done flags every NEV iterations
             CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             drain();

@@ -1913,23 +1913,31 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
     }
     for (int i = tid; i < d * SVM_WS; i += OVR_THREADS)
         if ((i & 15) >= nr) sXW[i] = 0.0f;
-    double* sXW64 = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);   // [16][dp64 + 2] fp64 rows
-    const int dp64 = (d + 3) & ~3, s64 = dp64 + 2;   // +16 B per row: rows start in different banks
+    // X_W also in fp64, feature-major [dp4][24] (row stride 24 doubles: the m8n8k4 fragment loads of
+    // four k-rows fall into two disjoint bank halves -> conflict-free), for the Gram on DMMA
+    double* sW64 = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);
+    const int dp4 = (d + 3) & ~3;
+    for (int i = tid; i < dp4 * 16; i += OVR_THREADS) {
+        const int k = i >> 4, r = i & 15;
+        if (r >= nr || k >= d) sW64[k * 24 + r] = 0.0;
+    }
     if (warp < nr) {
         const int64_t row = sh.r_row[warp];
         const float* src = a.XR + row * a.d;
-        for (int k0 = 0; k0 < dp64; k0 += 8 * 32) {   // 8 loads in flight per lane
-            float x[8];
+        for (int k0 = 0; k0 < d; k0 += 32 * 32) {   // 32 loads in flight per lane (one round trip for d <= 1024)
+            float x[32];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 32; ++u) {
                 const int k = k0 + u * 32 + lane;
                 x[u] = k < d ? __ldg(src + k) : 0.0f;
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 32; ++u) {
                 const int k = k0 + u * 32 + lane;
-                if (k < d) sXW[k * SVM_WS + warp] = x[u];
-                if (k < dp64) sXW64[warp * s64 + k] = (double)x[u];
+                if (k < d) {
+                    sXW[k * SVM_WS + warp] = x[u];
+                    sW64[k * 24 + warp] = (double)x[u];
+                }
             }
         }
         if (lane == 0) sh.xn[warp] = a.xnorm[row];
@@ -1937,47 +1945,58 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
     if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
     __syncthreads();
     SOLVE_MARK(1)
-    // ---- K_WW in fp64 from the fp32 tile (pairs k-split, four interleaved accumulators) -------
+    // ---- K_WW in fp64: Gram X_W X_W^T on the fp64 tensor cores (mma.sync m8n8k4, three 8x8 tiles
+    // x 5 k-parts = 15 warps, fixed summation order), then K from the Gram entries (RBF: the
+    // distance G_aa + G_bb - 2 G_ab, clamped at 0; 0 exactly on the diagonal) --------------------
     {
-        const int npairs = nr * (nr + 1) / 2;
-        const int kp = max(1, min(4, OVR_THREADS / max(npairs, 1)));
-        const int dp = (d + 3) & ~3;
-        const int klen = ((d + kp - 1) / kp + 3) & ~3;
-        if (tid < npairs * kp) {
-            const int pr = tid / kp, part = tid - pr * kp;
-            int r = 0, rem = pr;
-            while (rem >= nr - r) { rem -= nr - r; ++r; }
-            const int sidx = r + rem;
-            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-            if (sidx != r || a.kp.kernel != 2) {
-                const int k0 = part * klen, k1 = min(k0 + klen, dp);
-                const double2* ur = reinterpret_cast<const double2*>(sXW64 + r * s64);
-                const double2* vr = reinterpret_cast<const double2*>(sXW64 + sidx * s64);
-                for (int k = k0; k < k1; k += 4) {   // rows zero-padded to dp64
-                    const double2 u0 = ur[k >> 1], u1 = ur[(k >> 1) + 1], v0 = vr[k >> 1], v1 = vr[(k >> 1) + 1];
-                    if (a.kp.kernel == 2) {
-                        const double t0 = u0.x - v0.x, t1 = u0.y - v0.y, t2 = u1.x - v1.x, t3 = u1.y - v1.y;
-                        acc0 = fma(t0, t0, acc0); acc1 = fma(t1, t1, acc1);
-                        acc2 = fma(t2, t2, acc2); acc3 = fma(t3, t3, acc3);
-                    } else {
-                        acc0 = fma(u0.x, v0.x, acc0); acc1 = fma(u0.y, v0.y, acc1);
-                        acc2 = fma(u1.x, v1.x, acc2); acc3 = fma(u1.y, v1.y, acc3);
-                    }
-                }
+        __shared__ double gpart[5][3][64];
+        __shared__ double gram[SVM_WS * SVM_WS];
+        if (warp < 15) {
+            const int t = warp / 5, part = warp - t * 5;
+            const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
+            const int nsteps = dp4 >> 2;
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+            const int ra = I * 8 + (lane >> 2), rb = J * 8 + (lane >> 2), kk = lane & 3;
+            int s = part;
+            for (; s + 5 < nsteps; s += 10) {   // two accumulator pairs: independent DMMA chains
+                const double a0 = sW64[(4 * s + kk) * 24 + ra], b0 = sW64[(4 * s + kk) * 24 + rb];
+                const double a1 = sW64[(4 * (s + 5) + kk) * 24 + ra], b1 = sW64[(4 * (s + 5) + kk) * 24 + rb];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c0), "+d"(c1) : "d"(a0), "d"(b0));
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(e0), "+d"(e1) : "d"(a1), "d"(b1));
             }
-            sh.qpart[pr * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
+            if (s < nsteps) {
+                const double a0 = sW64[(4 * s + kk) * 24 + ra], b0 = sW64[(4 * s + kk) * 24 + rb];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c0), "+d"(c1) : "d"(a0), "d"(b0));
+            }
+            gpart[part][t][(lane >> 2) * 8 + (lane & 3) * 2] = c0 + e0;
+            gpart[part][t][(lane >> 2) * 8 + (lane & 3) * 2 + 1] = c1 + e1;
         }
         __syncthreads();
         SOLVE_MARK(5)
-        if (tid < npairs) {
-            int r = 0, rem = tid;
-            while (rem >= nr - r) { rem -= nr - r; ++r; }
-            const int sidx = r + rem;
-            double v = 0.0;
-            for (int part = 0; part < kp; ++part) v += sh.qpart[tid * 4 + part];
-            const double kv = kernel_fp64_from(v, a.kp);
-            sh.kr[r * SVM_WS + sidx] = kv;
-            sh.kr[sidx * SVM_WS + r] = kv;
+        if (tid < SVM_WS * SVM_WS) {
+            int ra = tid >> 4, rb = tid & 15;
+            const bool sw = (ra >> 3) > (rb >> 3);
+            const int I = sw ? rb >> 3 : ra >> 3, J = sw ? ra >> 3 : rb >> 3;
+            const int t = I == 0 ? (J == 0 ? 0 : 1) : 2;
+            const int e = sw ? (rb & 7) * 8 + (ra & 7) : (ra & 7) * 8 + (rb & 7);
+            double g = 0.0;
+            for (int part = 0; part < 5; ++part) g += gpart[part][t][e];
+            gram[tid] = g;
+        }
+        __syncthreads();
+        if (tid < SVM_WS * SVM_WS) {
+            const int ra = tid >> 4, rb = tid & 15;
+            if (ra < nr && rb < nr) {
+                double v = gram[tid];
+                if (a.kp.kernel == 2) {
+                    v = ra == rb ? 0.0 : gram[ra * 17] + gram[rb * 17] - 2.0 * gram[tid];
+                    v = v > 0.0 ? v : 0.0;
+                }
+                sh.kr[tid] = kernel_fp64_from(v, a.kp);
+            }
         }
         __syncthreads();
         SOLVE_MARK(6)
@@ -2117,8 +2136,12 @@ cudaError_t launch_ovr_pass(const OvrArgs& a0, cudaStream_t st)
     OvrArgs a = a0;
     ovr_rings(a.NU, &a.na, &a.nb);
     const int smem = ovr_pass_smem_n(a.NU, a.na, a.nb);
-    cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    static int smem_set = 0;   // the attribute is set outside stream capture (launch_ovr_pass_prepare)
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
     svm_note_launches(1);
     k_ovr_pass<<<std::min(nsm, a.nct), OVR_PASS_THREADS, smem, st>>>(a);
     return cudaGetLastError();
@@ -2151,10 +2174,20 @@ cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cuda
     return cudaGetLastError();
 }
 
+static int ovr_solve_smem(const OvrArgs& a) { return (int)(a.d * SVM_WS * 4 + ((a.d + 3) & ~3) * 24 * 8); }
+static int g_solve_smem_set = 0;
+cudaError_t launch_ovr_solve_prepare(const OvrArgs& a)
+{
+    const int smem = ovr_solve_smem(a);
+    if (smem <= g_solve_smem_set) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) g_solve_smem_set = smem;
+    return e;
+}
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st)
 {
-    const int smem = (int)(a.d * SVM_WS * 4 + SVM_WS * (((a.d + 3) & ~3) + 2) * 8);
-    cudaError_t e = cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = ovr_solve_smem(a);
+    cudaError_t e = launch_ovr_solve_prepare(a);
     if (e != cudaSuccess) return e;
     svm_note_launches(1);
     k_ovr_solve<<<a.P, OVR_THREADS, smem, st>>>(a);

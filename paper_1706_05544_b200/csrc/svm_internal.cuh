@@ -207,6 +207,7 @@ int ovr_pass_smem(const OvrArgs& a);
 cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st);
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st);
 cudaError_t ovr_prepare(OvrArgs& a, unsigned int* scratch, cudaStream_t st);
+cudaError_t launch_ovr_solve_prepare(const OvrArgs& a);   // kernel attribute of k_ovr_solve
 // atomicMax of max |X[0 .. count)| as float bits into *out (caller zeroes *out)
 cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cudaStream_t st);
 

@@ -1,2 +1,2 @@
-timeout 600 python scripts/prof_train.py c5 3000 2>&1 | tail -1
-timeout 900 python -m pytest tests -m gpu -q -x -k "csr or CSR or c5 or kernel_rows" > gpurun_out/pytest_csr.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest_csr.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "ovr" > gpurun_out/pytest_ovr.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_ovr.log
+SVMB200_PROFILE=1 timeout 300 python scripts/prof_ovr.py 64 2>&1 | grep -v "^\[svmb200\] certify"; echo rc=$?
