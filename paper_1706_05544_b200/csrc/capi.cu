@@ -838,6 +838,8 @@ struct svm_model {
 static int build_sv_tiles(svm_model* M, cudaStream_t st)
 {
     if (pred_tc_dp(M->d) == 0 || M->nsv_pad == 0) return SVM_OK;
+    // predict takes the fp16-split kernel (k_decision_f16) for up to 16 outputs: no tiles needed
+    if (M->n_out <= 16 && !getenv("SVMB200_NO_F16")) return SVM_OK;
     TRY(M->SVtc.alloc(sizeof(float) * pred_sv_tiles_floats(M->nsv_pad, M->d, M->n_out)));
     CK(pred_sv_tiles(M->SVT.as<float>(), M->nsv_pad, M->d, M->coef.as<double>(), M->n_out,
                      M->SVtc.as<float>(), st));
@@ -1267,7 +1269,8 @@ static int predict_common(const svm_model* M, int64_t nq, const float* Xq_dense,
         CK(lay_norms_XT(QT.as<float>(), m, M->d, cpad, qn.as<float>(), st));
         CK(pred_decision(QT.as<float>(), qn.as<float>(), m, cpad, M->SVT.as<float>(),
                          M->svnorm.as<float>(), M->nsv, M->nsv_pad, M->d, M->coef.as<double>(),
-                         M->n_out, M->kp, F.as<double>(), st, M->SVtc.p ? M->SVtc.as<float>() : nullptr));
+                         M->n_out, M->kp, F.as<double>(), st, M->SVtc.p ? M->SVtc.as<float>() : nullptr,
+                         /*f16_any_d=*/true));
         CK(pred_finalize(F.as<double>(), m, M->n_out, M->b.as<double>(), M->mode,
                          M->labels.as<double>(), M->first_label, ddec.as<float>(),
                          dout.as<float>(), st));

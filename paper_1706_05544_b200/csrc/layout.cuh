@@ -73,7 +73,9 @@ cudaError_t lay_gather_global_sv(const SvPeers& P, int64_t nsv, int64_t nsv_pad,
 cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
                           const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad,
                           int64_t d, const double* coef, int n_out, const KParams& kp,
-                          double* F, cudaStream_t st, const float* SVtc = nullptr);
+                          double* F, cudaStream_t st, const float* SVtc = nullptr, bool f16_any_d = false);
+// (f16_any_d: use the fp16-split tcgen05 kernel for every d -- predict; the certification keeps the
+// 3xTF32 kernel for d <= 128, whose measured violations decide the resume of the loop)
 // tcgen05 predict (d <= 128): SV tiles [nsv_pad / 64][hi | lo][64 * dp] in the K-major core
 // layout (dp = pred_tc_dp(d)); 0 when the tensor-core path does not apply
 int64_t pred_tc_dp(int64_t d);

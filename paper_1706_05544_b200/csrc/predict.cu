@@ -589,6 +589,20 @@ __global__ void k_split_tiles(const float* __restrict__ XT, int64_t ld, int64_t 
     }
 }
 
+// max |X[k][c]| over k < d, c < ncols of a feature-major [d][ld] matrix (padding columns excluded:
+// they may hold stale values), as float bits into *out
+__global__ void k_absmax2d(const float* __restrict__ XT, int64_t ld, int64_t ncols, int64_t d, unsigned int* out)
+{
+    float m = 0.0f;
+    const int64_t total = d * ncols;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / ncols, c = t - k * ncols;
+        m = fmaxf(m, fabsf(XT[k * ld + c]));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
 __device__ __forceinline__ void df_arrive(uint32_t bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -812,20 +826,22 @@ constexpr int decision_smem(int nout)
 }  // namespace
 
 static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
-                                     const float* SVT, const float* svnorm, int64_t nsv_pad, int64_t d,
-                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st);
+                                     const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad, int64_t d,
+                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st,
+                                     bool any_d);
 static double* g_fpart = nullptr;
 static size_t g_fpart_bytes = 0;
 
 cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
                           const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad,
                           int64_t d, const double* coef, int n_out, const KParams& kp, double* F,
-                          cudaStream_t st, const float* SVtc)
+                          cudaStream_t st, const float* SVtc, bool f16_any_d)
 {
     (void)nsv;
     if (nq <= 0) return cudaSuccess;
-    if (d > 128 && nsv_pad > 0) {
-        const cudaError_t e = pred_decision_f16(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv_pad, d, coef, n_out, kp, F, st);
+    if ((d > 128 || f16_any_d || getenv("SVMB200_F16_ALL")) && nsv_pad > 0) {
+        const cudaError_t e = pred_decision_f16(XqT, qnorm, nq, nq_pad, SVT, svnorm, nsv, nsv_pad, d, coef, n_out, kp, F, st,
+                                                f16_any_d);
         if (e != cudaErrorNotSupported) return e;
     }
     // tcgen05 3xTF32 path for d <= 128 (query tile resident in shared memory)
@@ -919,10 +935,13 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
 // partials per (split, column quarter) reduced in a fixed order.  Returns cudaErrorNotSupported when
 // the configuration is not covered (the caller falls back to the SIMT kernel).
 static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
-                                     const float* SVT, const float* svnorm, int64_t nsv_pad, int64_t d,
-                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st)
+                                     const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad, int64_t d,
+                                     const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st,
+                                     bool any_d)
 {
-    if (d <= 128 || n_out > 16 || getenv("SVMB200_NO_TC") || getenv("SVMB200_NO_F16")) return cudaErrorNotSupported;
+    // d <= 128: the resident-query 3xTF32 kernel (k_decision_tcp) unless SVMB200_F16_ALL is set
+    if ((d <= 128 && !any_d && !getenv("SVMB200_F16_ALL")) || n_out > 16 || getenv("SVMB200_NO_TC") || getenv("SVMB200_NO_F16"))
+        return cudaErrorNotSupported;
     static int nsm = 0;
     if (nsm == 0) {
         int dev = 0;
@@ -932,7 +951,7 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
     }
     const int nkc = (int)((d + DF_KCH - 1) / DF_KCH);
     const int nqt = (int)((nq + 127) / 128);
-    const int nsb = (int)((nsv_pad + DF_SVB - 1) / DF_SVB);
+    const int nsb = (int)((std::max<int64_t>(nsv, 1) + DF_SVB - 1) / DF_SVB);   // blocks of the real SVs
     const int64_t nsv_ld = (int64_t)nsb * DF_SVB;
     int nsplit = 1;
     while (nsplit < nsb && (int64_t)nqt * nsplit < 4 * nsm) ++nsplit;
@@ -967,8 +986,10 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
     unsigned int* mx = reinterpret_cast<unsigned int*>(buf + qh_b + sh_b + cf_b + sn_b + part_b);
     // sigma from max |x| over queries and SVs (one scale for both operands)
     if ((e = cudaMemsetAsync(mx, 0, sizeof(unsigned int), st)) != cudaSuccess) goto out;
-    if ((e = launch_absmax(XqT, d * nq_pad, mx, st)) != cudaSuccess) goto out;
-    if ((e = launch_absmax(SVT, d * nsv_pad, mx, st)) != cudaSuccess) goto out;
+    svm_note_launches(2);
+    k_absmax2d<<<4 * nsm, 256, 0, st>>>(XqT, nq_pad, nq, d, mx);
+    k_absmax2d<<<4 * nsm, 256, 0, st>>>(SVT, nsv_pad, nsv, d, mx);
+    if ((e = cudaGetLastError()) != cudaSuccess) goto out;
     {
         unsigned int mb = 0;
         if ((e = cudaMemcpyAsync(&mb, mx, sizeof mb, cudaMemcpyDeviceToHost, st)) != cudaSuccess) goto out;
@@ -976,16 +997,19 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
         float m = 0, sigma = 1, isg = 1;
         memcpy(&m, &mb, sizeof m);
         f16_sigma(m, &sigma, &isg);
-        svm_note_launches(4);
+        svm_note_launches(2);
         k_split_tiles<<<8 * nsm, 256, 0, st>>>(XqT, nq_pad, nq, d, 128, nqt, nkc, sigma, QH);
-        k_split_tiles<<<8 * nsm, 256, 0, st>>>(SVT, nsv_pad, nsv_pad, d, DF_SVB, nsb, nkc, sigma, SH);
+        k_split_tiles<<<8 * nsm, 256, 0, st>>>(SVT, nsv_pad, nsv, d, DF_SVB, nsb, nkc, sigma, SH);
+        // coefficients and norms of the nsv real SVs; the padding is 0 (not the model's padding)
         if ((e = cudaMemsetAsync(cf, 0, cf_b + sn_b, st)) != cudaSuccess) goto out;
-        for (int p = 0; p < n_out; ++p) {
-            k_coef32<<<(unsigned)std::min<int64_t>((nsv_pad + 255) / 256, 148 * 16), 256, 0, st>>>(
-                coef + (int64_t)p * nsv_pad, nsv_pad, cf + (int64_t)p * nsv_ld);
+        if (nsv > 0) {
+            for (int p = 0; p < n_out; ++p) {
+                k_coef32<<<(unsigned)std::min<int64_t>((nsv + 255) / 256, 148 * 16), 256, 0, st>>>(
+                    coef + (int64_t)p * nsv_pad, nsv, cf + (int64_t)p * nsv_ld);
+            }
+            svm_note_launches(n_out - 1);
+            if ((e = cudaMemcpyAsync(sn, svnorm, sizeof(float) * nsv, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) goto out;
         }
-        svm_note_launches(n_out - 1);
-        if ((e = cudaMemcpyAsync(sn, svnorm, sizeof(float) * nsv_pad, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) goto out;
         const int nout_t = n_out == 1 ? 1 : 16;
         auto smem_for = [&](int ns) { return ns * (DF_ATILE + DF_BTILE) * 2 + (2 * nout_t * DF_SVB + 2 * DF_SVB) * 4 + 20 * 8 + 16; };
         int nstage = 2;

@@ -1,2 +1,2 @@
-timeout 600 python scripts/repeat_train.py c2 8
-timeout 600 python scripts/repeat_train.py c4 4
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_all.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest_gpu_all.log
+timeout 600 python scripts/predict_probe.py c2 2>&1 | tail -1
