@@ -44,13 +44,16 @@ ROOF_NOTES = {
     "c3": "batched one-vs-rest: X (188 MB > L2) read once per batched iteration for all 10 "
           "problems; see DESIGN.md",
     "c4": "X (108 MB) streamed from HBM/L2 through per-lane cp.async rings; see DESIGN.md",
+    "c5": "CSR pass: per-warp staged nonzeros, masked X_W groups in shared memory (L1/shared-pipe "
+          "bound, not HBM); algorithmic bytes 8 nnz + 17 n per iteration; see DESIGN.md",
 }
-ITERS_TO_TOL = {"c1": 296, "c2": 19291, "c3": 10616, "c4": 70000}
+ITERS_TO_TOL = {"c1": 296, "c2": 19291, "c3": 10531, "c4": 68611, "c5": 280000}
 WORKLOADS = {
     "c1": "binary C-SVC, RBF, two Gaussian blobs, n=2,000 d=20 dense",
     "c2": "eps-SVR, RBF, Friedman #1, n=50,000 d=100 dense (m=100,000 duals)",
     "c3": "10-class one-vs-rest C-SVC, RBF, MNIST-shaped, n=60,000 d=784 dense",
     "c4": "binary C-SVC, RBF, covertype-shaped, n=500,000 d=54 dense",
+    "c5": "binary C-SVC, RBF, genomics-shaped, n=2,000,000 d=400 CSR-sparse (~10% density)",
 }
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -138,9 +141,12 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def fused_bytes_per_iter(cfg, n_rows, d, ncopy):
-    """Algorithmic bytes of one fused kernel-row + gradient pass: X (4d per row),
-    |x|^2 (4), G read + write (8 per dual), status (1 per dual)."""
+def fused_bytes_per_iter(cfg, n_rows, d, ncopy, nnz=None):
+    """Algorithmic bytes of one fused kernel-row + gradient pass: X (4d per row
+    dense; 8 per nonzero + 8 of indptr per row CSR), |x|^2 (4), G read + write (8 per dual),
+    status (1 per dual)."""
+    if nnz is not None:
+        return 8 * nnz + n_rows * (8 + 4 + 9 * ncopy)
     return n_rows * (4 * d + 4 + 9 * ncopy)
 
 
@@ -152,12 +158,13 @@ def cpu_baseline(ds, kw, seconds):
     prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
                        ds.y if reg else ora.binary_labels(ds.y)[0], ds.n, kw.get("epsilon", 0.1))
     ks = ora.kspec("rbf", kw["gamma"], d=ds.d)
+    X = ds.X if ds.X is not None else ds.dense()   # c5: the oracle takes the densified rows
     t = time.perf_counter()
-    ora.train_dual(ds.X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=2)
+    ora.train_dual(X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=2)
     per = (time.perf_counter() - t) / 2
     k = max(2, min(5000, int(seconds / max(per, 1e-6))))
     t = time.perf_counter()
-    r = ora.train_dual(ds.X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=k)
+    r = ora.train_dual(X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=k)
     el = time.perf_counter() - t
     k = max(1, r["iterations"])
     return el, k, ora.num_threads()
@@ -243,7 +250,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     pkg.lib()
 
-    ds = synth.make(args.config)
+    # (SVMB200_BENCH_N: debugging only -- a reduced n is not the BASELINE workload)
+    ds = synth.make(args.config, n=int(os.environ["SVMB200_BENCH_N"]) if os.environ.get("SVMB200_BENCH_N") else None)
     hq = synth.make(args.config, n=min(ds.n, 100000), heldout=True)
     kw = workload_params(ds)
     ncopy = 2 if kw["svm_type"] == "eps-regression" else 1
@@ -251,10 +259,23 @@ def main():
     from paper_1706_05544_b200.dist import all_gather_bytes, shard_bounds
     r0, r1 = shard_bounds(n, world, rank)
     q0, q1 = shard_bounds(nq, world, rank)
-    X = torch.from_numpy(ds.X).to(dev)
+    csr = ds.is_csr
     y = torch.from_numpy(ds.y).to(dev)
-    Xq = torch.from_numpy(hq.X[q0:q1]).to(dev)
-    Xl = X[r0:r1].contiguous()
+    if csr:   # c5: CSR training rows (this rank's slice re-based at 0) and CSR held-out rows
+        ip = ds.indptr
+        loc = (ip[r0:r1 + 1] - ip[r0]).astype(np.int64)
+        csr_l = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                      for a in (loc, ds.indices[ip[r0]:ip[r1]], ds.data[ip[r0]:ip[r1]]))
+        qip = hq.indptr
+        q_csr = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                      for a in ((qip[q0:q1 + 1] - qip[q0]).astype(np.int64),
+                                hq.indices[qip[q0]:qip[q1]], hq.data[qip[q0]:qip[q1]]))
+        X = Xl = csr_l
+        Xq = q_csr
+    else:
+        X = torch.from_numpy(ds.X).to(dev)
+        Xq = torch.from_numpy(hq.X[q0:q1]).to(dev)
+        Xl = X[r0:r1].contiguous()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     def barrier():
@@ -262,16 +283,23 @@ def main():
             torch.distributed.barrier()
 
     def train(Xa, ya):
+        if csr:
+            if world == 1:
+                return pkg.train_csr(*Xa, ya, d, **kw)
+            return pkg.binding.train_sharded_csr(*Xa, d, r0, ya, rank, world, all_gather_bytes, **kw)
         if world == 1:
             return pkg.train(Xa, ya, **kw)
         return pkg.binding.train_sharded(Xa, r0, ya, rank, world, all_gather_bytes, **kw)
+
+    def predict(m, Xqa):
+        return m.predict_csr(*Xqa, d) if csr else m.predict(Xqa)
 
     def step(Xa, ya, Xqa):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record()
         m = train(Xa, ya)
         e1.record()
-        out = m.predict(Xqa)
+        out = predict(m, Xqa)
         e2.record()
         torch.cuda.synchronize()
         return m, out, e0.elapsed_time(e1), e1.elapsed_time(e2)
@@ -305,7 +333,8 @@ def main():
     # ---- roofline of the persistent working-set kernel ---------------------------------------
     peaks, peak_src = measured_peaks()
     n_rows_local = r1 - r0
-    bpi = fused_bytes_per_iter(args.config, n_rows_local, d, ncopy)
+    bpi = fused_bytes_per_iter(args.config, n_rows_local, d, ncopy,
+                               nnz=int(ds.indptr[r1] - ds.indptr[r0]) if csr else None)
     loop_s = info.loop_ms / 1e3
     achieved = bpi * info.iterations / loop_s / 1e9 if loop_s > 0 else 0.0
     traffic = None
@@ -329,10 +358,14 @@ def main():
     # ---- e2e: pinned host buffers through the C ABI ------------------------------------------
     e2e = None
     if not args.no_e2e:
-        Xh = torch.from_numpy(ds.X[r0:r1] if world > 1 else ds.X).pin_memory()
         yh = torch.from_numpy(ds.y).pin_memory()
-        Xqh = torch.from_numpy(hq.X[q0:q1]).pin_memory()
-        xa, ya, qa = Xh.numpy(), yh.numpy(), Xqh.numpy()
+        ya = yh.numpy()
+        if csr:
+            xa = tuple(t.cpu().pin_memory().numpy() for t in Xl)
+            qa = tuple(t.cpu().pin_memory().numpy() for t in Xq)
+        else:
+            xa = torch.from_numpy(ds.X[r0:r1] if world > 1 else ds.X).pin_memory().numpy()
+            qa = torch.from_numpy(hq.X[q0:q1]).pin_memory().numpy()
         step(xa, ya, qa)  # warm
         barrier()
         et, ep = [], []
@@ -343,16 +376,18 @@ def main():
             m = train(xa, ya)                 # H2D of X, y inside; model D2H inside
             torch.cuda.synchronize()
             t1 = time.perf_counter()
-            m.predict(qa)                     # H2D of Xq, D2H of the labels
+            predict(m, qa)                    # H2D of Xq, D2H of the labels
             torch.cuda.synchronize()
             et.append(t1 - t0)
             ep.append(time.perf_counter() - t1)
         barrier()
         nsv = m.info.n_sv
+        nb = (lambda a: sum(x.nbytes for x in a)) if csr else (lambda a: a.nbytes)
+        nqr = (len(qa[0]) - 1) if csr else qa.shape[0]
         e2e = {"value": statistics.mean(et), "unit": "s",
-               "h2d_bytes_per_step": int(xa.nbytes + ya.nbytes + qa.nbytes),
-               "d2h_bytes_per_step": int(4 * qa.shape[0] + 16 * nsv),
-               "predict_rows_per_s": qa.shape[0] / statistics.mean(ep)}
+               "h2d_bytes_per_step": int(nb(xa) + ya.nbytes + nb(qa)),
+               "d2h_bytes_per_step": int(4 * nqr + 16 * nsv),
+               "predict_rows_per_s": nqr / statistics.mean(ep)}
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

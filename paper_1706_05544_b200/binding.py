@@ -306,6 +306,35 @@ class Solver:
         return K
 
 
+def _shard_run(sh, world, all_gather_bytes) -> Model:
+    try:
+        blob = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
+        _check(lib().svm_shard_handle(sh, blob))
+        blobs = all_gather_bytes(blob.raw)
+        allh = ctypes.create_string_buffer(b"".join(blobs), SHARD_HANDLE_BYTES * world)
+        _check(lib().svm_shard_connect(sh, allh))
+        h = ctypes.c_void_p()
+        _check(lib().svm_shard_train(sh, ctypes.byref(h)))
+        return Model(h.value)
+    finally:
+        lib().svm_shard_free(sh)
+
+
+def train_sharded_csr(indptr, indices, data, d: int, row0: int, y_global, rank: int, world: int,
+                      all_gather_bytes, **kw) -> Model:
+    """svm_shard_create_csr: as train_sharded, this rank's rows [row0, row0 + n_local) in CSR
+    (indptr of the local rows, starting at 0)."""
+    n_local = int(len(indptr)) - 1
+    n_global = int(len(y_global))
+    p = params(int(d), **kw)
+    a, b, c = _Arr(indptr, np.int64), _Arr(indices, np.int32), _Arr(data, np.float32)
+    yy = _Arr(y_global, np.float32)
+    sh = ctypes.c_void_p()
+    _check(lib().svm_shard_create_csr(a.p, b.p, c.p, n_local, int(d), int(row0), yy.p, n_global,
+                                      int(rank), int(world), ctypes.byref(p), ctypes.byref(sh)))
+    return _shard_run(sh, world, all_gather_bytes)
+
+
 def train_sharded(X_local, row0: int, y_global, rank: int, world: int, all_gather_bytes,
                   layout=ROW_MAJOR, **kw) -> Model:
     """svm_shard_*: row-sharded training over `world` GPUs (one process per GPU).
@@ -322,14 +351,4 @@ def train_sharded(X_local, row0: int, y_global, rank: int, world: int, all_gathe
     sh = ctypes.c_void_p()
     _check(lib().svm_shard_create(x.p, n_local, d, int(row0), yy.p, n_global, int(rank),
                                   int(world), ctypes.byref(p), ctypes.byref(sh)))
-    try:
-        blob = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
-        _check(lib().svm_shard_handle(sh, blob))
-        blobs = all_gather_bytes(blob.raw)
-        allh = ctypes.create_string_buffer(b"".join(blobs), SHARD_HANDLE_BYTES * world)
-        _check(lib().svm_shard_connect(sh, allh))
-        h = ctypes.c_void_p()
-        _check(lib().svm_shard_train(sh, ctypes.byref(h)))
-        return Model(h.value)
-    finally:
-        lib().svm_shard_free(sh)
+    return _shard_run(sh, world, all_gather_bytes)

@@ -1,2 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_all.log 2>&1; echo pytest_rc=$?; tail -2 gpurun_out/pytest_gpu_all.log
-timeout 600 python scripts/predict_probe.py c2 2>&1 | tail -1
+SVMB200_BENCH_N=100000 timeout 900 python bench.py --config c5 --steps 1 --warmup 3 --cpu-seconds 5 > gpurun_out/bench_c5_small.log 2>&1; echo rc=$?; tail -c 1500 gpurun_out/bench_c5_small.log
