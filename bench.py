@@ -206,8 +206,10 @@ def batched_roofline(info, n, d, peaks, peak_src):
     gradient / selection epilogue.  fp32-accurate products come from three kind::f16 MMAs per
     product (operands pre-split into fp16 hi + lo pairs with a power-of-two scale), so
     the peak is the f16 dense rate / 3, the f16 rate being the measured bf16 peak (same tensor rate,
-    B200_PROFILING.md).  Algorithmic FLOPs per pass = 2 n d |U|.  Timing: CUDA event pairs around
-    every k_ovr_pass launch on the library's stream (info.pass_ms over info.passes)."""
+    B200_PROFILING.md).  Algorithmic FLOPs per pass = 2 n d |U|.  Timing: CUDA event pairs on the
+    library's stream around every 8th k_ovr_pass launch (an event between the solve and the pass
+    would serialise the programmatic dependent launch of the others): info.pass_ms = mean sampled
+    duration x info.passes."""
     nu = 16 * info.n_problem
     flops = 2.0 * n * d * nu
     per_launch_s = info.pass_ms / 1e3 / max(1, info.passes)

@@ -105,8 +105,9 @@ typedef struct svm_model_info {
     double setup_ms, certify_ms;
     int64_t passes;       /* passes of the dominant X-pass kernel in the loop: the iterations of  */
                           /* the persistent kernel, or the k_ovr_pass launches (batched OvR)      */
-    double pass_ms;       /* their device time: loop_ms (persistent), or the sum of CUDA event    */
-                          /* pairs around every k_ovr_pass launch (batched one-vs-rest)           */
+    double pass_ms;       /* their device time: loop_ms (persistent), or for the batched one-vs- */
+                          /* rest passes the mean of CUDA event pairs around every 8th k_ovr_pass */
+                          /* launch times the launch count                                        */
     int32_t batched;      /* 1 if the one-vs-rest problems iterated together      */
 } svm_model_info;
 

@@ -1000,20 +1000,26 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    // every pass launch is bracketed by a CUDA event pair on this stream (the bench's per-launch
-    // timing of the dominant kernel); the ring is read at each host poll
-    constexpr int NEV = 16;
+    // The pass launches are timed with CUDA event pairs on this stream, one launch in every
+    // PASS_SAMPLE (an event between two kernels serialises them, which would undo the programmatic
+    // dependent launch that overlaps a kernel's prologue with its predecessor's tail):
+    // pass_ms = mean sampled duration x passes.  The host polls the done flags every POLL
+    // iterations.
+    constexpr int NEV = 16, PASS_SAMPLE = 8, POLL = 16;
     cudaEvent_t pev[NEV][2];
     for (int k = 0; k < NEV; ++k)
         for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&pev[k][j]));
-    int nrec = 0;
+    int nrec = 0, nsampled = 0;
     int64_t passes = 0;
-    double pass_ms = 0;
+    double sampled_ms = 0;
     auto timed_pass = [&]() -> int {
-        CK(cudaEventRecord(pev[nrec][0], st));
+        const bool sample = (passes % PASS_SAMPLE) == 0 && nrec < NEV;
+        if (sample) CK(cudaEventRecord(pev[nrec][0], st));
         CK(launch_ovr_pass(a, st));
-        CK(cudaEventRecord(pev[nrec][1], st));
-        ++nrec;
+        if (sample) {
+            CK(cudaEventRecord(pev[nrec][1], st));
+            ++nrec;
+        }
         ++passes;
         return SVM_OK;
     };
@@ -1021,23 +1027,19 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
         for (int k = 0; k < nrec; ++k) {
             float t = 0;
             const cudaError_t te = cudaEventElapsedTime(&t, pev[k][0], pev[k][1]);
-            if (te != cudaSuccess) {
-                cudaGetLastError();   // not sticky: clear it
-                if (getenv("SVMB200_PROFILE")) fprintf(stderr, "[svmb200] pass event %d: %s\n", k, cudaGetErrorString(te));
-            }
-            pass_ms += t;
+            if (te != cudaSuccess) { cudaGetLastError(); continue; }
+            sampled_ms += t;
+            ++nsampled;
         }
         nrec = 0;
     };
     CK(cudaEventRecord(e0, st));
     TRY(timed_pass());   // candidates of the initial state (all coefficients 0)
-    CK(cudaStreamSynchronize(st));
-    drain();
     std::vector<int32_t> dh(P);
     for (int64_t it = 0; it <= a.max_iter; ++it) {
         CK(launch_ovr_solve(a, st));
         TRY(timed_pass());
-        if (nrec == NEV) {   // host poll of the done flags every NEV iterations
+        if ((it % POLL) == POLL - 1) {   // host poll of the done flags
             CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             drain();
@@ -1058,6 +1060,7 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     drain();
     for (int k = 0; k < NEV; ++k)
         for (int j = 0; j < 2; ++j) cudaEventDestroy(pev[k][j]);
+    const double pass_ms = nsampled ? sampled_ms / nsampled * (double)passes : 0.0;
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
