@@ -336,7 +336,7 @@ struct SmoShared {
     double kr[SVM_WS * SVM_WS];          // K between distinct rows, fp64
     double kpos[SVM_WS * SVM_WS];        // K between working-set positions, fp64
     double inv_eta[SVM_WS * SVM_WS];     // 1 / max(K_aa + K_bb - 2 K_ab, tau)
-    double qpart[960 + 256];             // Gram partials [5 k-parts][3 tiles][64] + the Gram [16][16]
+    double qpart[136 * 4];               // k-split partial sums of the row-pair reductions
     double w_alpha[SVM_WS], w_G[SVM_WS], w_dalpha[SVM_WS], w_anew[SVM_WS];
     int32_t w_y[SVM_WS];
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
@@ -1158,58 +1158,55 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         wmark(-1);
         // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
         {
-            // Gram X_W X_W^T on the fp64 tensor cores (mma.sync m8n8k4: three 8x8 tiles x 5 k-parts
-            // = 15 warps; fp32 inputs promoted exactly, fixed-order sums), then K from the Gram
-            // (RBF: G_aa + G_bb - 2 G_ab clamped at 0, exactly 0 on the diagonal)
-            double* gpart = sh.qpart;             // [5][3][64] partials (960 doubles)
-            double* gram = sh.qpart + 960;        // [16][16]
-            if (warp < 15) {
-                const int t = warp / 5, part = warp - t * 5;
-                const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
-                const int nsteps = (d + 3) >> 2;
-                const int ra = I * 8 + (lane >> 2), rb = J * 8 + (lane >> 2), kk = lane & 3;
-                double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-                auto ld = [&](int k, int r) { return k < d ? (double)sXW[k * WS + r] : 0.0; };
-                int st = part;
-                for (; st + 5 < nsteps; st += 10) {
-                    const double a0 = ld(4 * st + kk, ra), b0 = ld(4 * st + kk, rb);
-                    const double a1 = ld(4 * (st + 5) + kk, ra), b1 = ld(4 * (st + 5) + kk, rb);
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(c0), "+d"(c1) : "d"(a0), "d"(b0));
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(e0), "+d"(e1) : "d"(a1), "d"(b1));
+            const int npairs = nr * (nr + 1) / 2;
+            const int kp = max(1, min(4, SMO_THREADS / max(npairs, 1)));
+            const int klen = ((d + kp - 1) / kp + 3) & ~3;
+            if (tid < npairs * kp) {
+                const int p = tid / kp, part = tid - p * kp;
+                int r = 0, rem = p;
+                while (rem >= nr - r) { rem -= nr - r; ++r; }
+                const int sidx = r + rem;
+                double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+                // from the fp32 [d][WS] tile (the fp32 inputs promoted exactly): four interleaved
+                // fp64 accumulators over k, features >= d contribute exact zeros
+                if (sidx != r || a.kp.kernel != 2) {
+                    const int k0 = part * klen, k1 = min(k0 + klen, dp);
+                    const float* xr = sXW + r;
+                    const float* xs = sXW + sidx;
+                    auto ld = [&](const float* x, int k) { return k < d ? (double)x[k * WS] : 0.0; };
+                    if (a.kp.kernel == 2) {
+#pragma unroll 1
+                        for (int k = k0; k < k1; k += 4) {
+                            const double t0 = ld(xr, k) - ld(xs, k), t1 = ld(xr, k + 1) - ld(xs, k + 1);
+                            const double t2 = ld(xr, k + 2) - ld(xs, k + 2), t3 = ld(xr, k + 3) - ld(xs, k + 3);
+                            acc0 = fma(t0, t0, acc0);
+                            acc1 = fma(t1, t1, acc1);
+                            acc2 = fma(t2, t2, acc2);
+                            acc3 = fma(t3, t3, acc3);
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int k = k0; k < k1; k += 4) {
+                            acc0 = fma(ld(xr, k), ld(xs, k), acc0);
+                            acc1 = fma(ld(xr, k + 1), ld(xs, k + 1), acc1);
+                            acc2 = fma(ld(xr, k + 2), ld(xs, k + 2), acc2);
+                            acc3 = fma(ld(xr, k + 3), ld(xs, k + 3), acc3);
+                        }
+                    }
                 }
-                if (st < nsteps) {
-                    const double a0 = ld(4 * st + kk, ra), b0 = ld(4 * st + kk, rb);
-                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                 : "+d"(c0), "+d"(c1) : "d"(a0), "d"(b0));
-                }
-                gpart[(part * 3 + t) * 64 + (lane >> 2) * 8 + (lane & 3) * 2] = c0 + e0;
-                gpart[(part * 3 + t) * 64 + (lane >> 2) * 8 + (lane & 3) * 2 + 1] = c1 + e1;
+                sh.qpart[p * 4 + part] = (acc0 + acc1) + (acc2 + acc3);
             }
             __syncthreads();
             wmark(6);
-            if (tid < SVM_WS * SVM_WS) {
-                const int ra = tid >> 4, rb = tid & 15;
-                const bool sw = (ra >> 3) > (rb >> 3);
-                const int I = sw ? rb >> 3 : ra >> 3, J = sw ? ra >> 3 : rb >> 3;
-                const int t = I == 0 ? (J == 0 ? 0 : 1) : 2;
-                const int e = sw ? (rb & 7) * 8 + (ra & 7) : (ra & 7) * 8 + (rb & 7);
-                double g = 0.0;
-                for (int part = 0; part < 5; ++part) g += gpart[(part * 3 + t) * 64 + e];
-                gram[tid] = g;
-            }
-            __syncthreads();
-            if (tid < SVM_WS * SVM_WS) {
-                const int ra = tid >> 4, rb = tid & 15;
-                if (ra < nr && rb < nr) {
-                    double v = gram[tid];
-                    if (a.kp.kernel == 2) {
-                        v = ra == rb ? 0.0 : gram[ra * 17] + gram[rb * 17] - 2.0 * gram[tid];
-                        v = v > 0.0 ? v : 0.0;
-                    }
-                    sh.kr[tid] = kernel_fp64_from(v, a.kp);
-                }
+            if (tid < npairs) {
+                int r = 0, rem = tid;
+                while (rem >= nr - r) { rem -= nr - r; ++r; }
+                const int sidx = r + rem;
+                double v = 0.0;
+                for (int part = 0; part < kp; ++part) v += sh.qpart[tid * 4 + part];
+                const double kv = kernel_fp64_from(v, a.kp);
+                sh.kr[r * SVM_WS + sidx] = kv;
+                sh.kr[sidx * SVM_WS + r] = kv;
             }
             __syncthreads();
             wmark(7);
@@ -1969,8 +1966,8 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
     // x 5 k-parts = 15 warps, fixed summation order), then K from the Gram entries (RBF: the
     // distance G_aa + G_bb - 2 G_ab, clamped at 0; 0 exactly on the diagonal) --------------------
     {
-        double (*gpart)[3][64] = reinterpret_cast<double (*)[3][64]>(sh.qpart);   // [5][3][64]
-        double* gram = sh.qpart + 960;                                            // [16][16]
+        __shared__ double gpart[5][3][64];
+        __shared__ double gram[SVM_WS * SVM_WS];
         if (warp < 15) {
             const int t = warp / 5, part = warp - t * 5;
             const int I = t == 2 ? 1 : 0, J = t == 0 ? 0 : 1;
