@@ -690,7 +690,8 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
     const float* qT = nullptr;
     const float* qnorm = nullptr;
     int64_t ld = 0;
-    if (!D.csr && D.n_pad % 128 == 0) {
+    // (the fp16-split kernel for d > 128 reads X^T with any leading dimension: no padded copy)
+    if (!D.csr && (D.n_pad % 128 == 0 || D.d > 128)) {
         qT = D.XT.as<float>();
         qnorm = D.norms.as<float>();
         ld = D.n_pad;
@@ -702,9 +703,8 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
         if (D.csr) {
             CK(lay_csr_to_XT(D.indptr, D.indices, D.vals, nullptr, D.n, 0, QT.as<float>(), nq_pad, st));
         } else {
-            for (int64_t k = 0; k < D.d; ++k)
-                CK(cudaMemcpyAsync(QT.as<float>() + k * nq_pad, D.XT.as<float>() + k * D.n_pad,
-                                   sizeof(float) * D.n, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpy2DAsync(QT.p, sizeof(float) * nq_pad, D.XT.p, sizeof(float) * D.n_pad,
+                                 sizeof(float) * D.n, D.d, cudaMemcpyDeviceToDevice, st));
         }
         CK(cudaMemcpyAsync(qn.p, D.norms.p, sizeof(float) * D.n, cudaMemcpyDeviceToDevice, st));
         qT = QT.as<float>();
