@@ -963,8 +963,8 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     a.kch = OVR_KCH;
     a.nkc = (int)((D.d + a.kch - 1) / a.kch);
     a.nct = (int)((D.n + 127) / 128);
-    // k_ovr_solve stages X_W in fp32 [d][16] and fp64 [d][24]: 256 B per feature of shared memory
-    if (ovr_pass_smem(a) > 227 * 1024 || ((D.d + 3) & ~3) * 256 + 20 * 1024 > 227 * 1024) return SVM_OK;
+    // k_ovr_solve stages X_W in fp64 [d][24]: 192 B per feature of shared memory
+    if (ovr_pass_smem(a) > 227 * 1024 || ((D.d + 3) & ~3) * 192 + 28 * 1024 > 227 * 1024) return SVM_OK;
     DBuf Utc, XH, scratch, unorm, ucoef, cand, done, iters, mup, mlow, inner;
     TRY(Utc.alloc(sizeof(uint16_t) * (size_t)a.nkc * 2 * a.NU * a.kch));
     TRY(XH.alloc(sizeof(uint16_t) * (size_t)a.nct * a.nkc * 2 * 128 * a.kch));

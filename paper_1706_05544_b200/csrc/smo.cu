@@ -1809,7 +1809,7 @@ __global__ void __launch_bounds__(OVR_PASS_THREADS, 1) k_ovr_pass(const OvrArgs 
 __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
 {
     extern __shared__ __align__(16) unsigned char ovr_smem[];
-    float* sXW = reinterpret_cast<float*>(ovr_smem);   // [d][16]
+    float* sXW = reinterpret_cast<float*>(ovr_smem);   // dynamic shared memory: the fp64 X_W below
     __shared__ SmoShared sh;
     __shared__ uint64_t gm[16][8];
     __shared__ int32_t gms[16][8];
@@ -1921,43 +1921,36 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
         return;
     }
     const int nw = sh.nw, nr = sh.nr;
-    // payloads of W, X_W rows (fp32 [d][16], columns >= nr zero), norms
+    // payloads of W, X_W rows, norms
     if (tid < nw) {
         const int64_t g = sh.w_gidx[tid];
         sh.w_alpha[tid] = a.alpha[p][g];
         sh.w_G[tid] = (double)a.G[p][g];
         sh.w_y[tid] = (a.status[p][g] & ST_YPOS) ? 1 : -1;
     }
-    for (int i = tid; i < d * SVM_WS; i += OVR_THREADS)
-        if ((i & 15) >= nr) sXW[i] = 0.0f;
-    // X_W also in fp64, feature-major [dp4][24] (row stride 24 doubles: the m8n8k4 fragment loads of
-    // four k-rows fall into two disjoint bank halves -> conflict-free), for the Gram on DMMA
-    double* sW64 = reinterpret_cast<double*>(sXW + (size_t)d * SVM_WS);
+    // X_W in fp64 (fp32 inputs, exact), feature-major [dp4][24] (row stride 24 doubles: the
+    // m8n8k4 fragment loads of four k-rows fall into two disjoint bank halves).  Thread t gathers
+    // row r = t % 16 at features k = t / 16 + 32 j: the 32 lanes of a warp store 2 consecutive
+    // 16-double rows (conflict-free); rows >= nr and features >= d are 0.
+    double* sW64 = reinterpret_cast<double*>(sXW);
     const int dp4 = (d + 3) & ~3;
-    for (int i = tid; i < dp4 * 16; i += OVR_THREADS) {
-        const int k = i >> 4, r = i & 15;
-        if (r >= nr || k >= d) sW64[k * 24 + r] = 0.0;
-    }
-    if (warp < nr) {
-        const int64_t row = sh.r_row[warp];
-        const float* src = a.XR + row * a.d;
-        for (int k0 = 0; k0 < d; k0 += 32 * 32) {   // 32 loads in flight per lane (one round trip for d <= 1024)
+    {
+        const int r = tid & 15, kb = tid >> 4;
+        const float* src = r < nr ? a.XR + sh.r_row[r] * a.d : nullptr;
+        for (int k0 = kb; k0 < dp4; k0 += 32 * 32) {   // all loads in flight (one round trip, d <= 1024)
             float x[32];
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
-                const int k = k0 + u * 32 + lane;
-                x[u] = k < d ? __ldg(src + k) : 0.0f;
+                const int k = k0 + u * 32;
+                x[u] = (src && k < d) ? __ldg(src + k) : 0.0f;
             }
 #pragma unroll
             for (int u = 0; u < 32; ++u) {
-                const int k = k0 + u * 32 + lane;
-                if (k < d) {
-                    sXW[k * SVM_WS + warp] = x[u];
-                    sW64[k * 24 + warp] = (double)x[u];
-                }
+                const int k = k0 + u * 32;
+                if (k < dp4) sW64[k * 24 + r] = (double)x[u];
             }
         }
-        if (lane == 0) sh.xn[warp] = a.xnorm[row];
+        if (tid < nr) sh.xn[tid] = a.xnorm[sh.r_row[tid]];
     }
     if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
     __syncthreads();
@@ -2060,7 +2053,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
         for (int e = tid; e < total; e += OVR_THREADS) {
             const int f = e >> 4, r = e & 15;
             const int kc = f / OVR_KCH, k = f - kc * OVR_KCH;
-            const float x = f < d ? sXW[f * SVM_WS + r] : 0.0f;
+            const float x = f < d ? (float)sW64[f * 24 + r] : 0.0f;   // exact (fp32 promoted)
             uint16_t h, l;
             f16_split(x, a.sigma, h, l);
             uint16_t* base = a.Uh + (size_t)kc * 2 * NU * OVR_KCH;
@@ -2208,7 +2201,7 @@ cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cuda
     return cudaGetLastError();
 }
 
-static int ovr_solve_smem(const OvrArgs& a) { return (int)(a.d * SVM_WS * 4 + ((a.d + 3) & ~3) * 24 * 8); }
+static int ovr_solve_smem(const OvrArgs& a) { return (int)(((a.d + 3) & ~3) * 24 * 8); }   // fp64 X_W
 static int g_solve_smem_set = 0;
 cudaError_t launch_ovr_solve_prepare(const OvrArgs& a)
 {
