@@ -593,12 +593,9 @@ __global__ void k_split_tiles(const float* __restrict__ XT, int64_t ld, int64_t 
 // they may hold stale values), as float bits into *out
 __global__ void k_absmax2d(const float* __restrict__ XT, int64_t ld, int64_t ncols, int64_t d, unsigned int* out)
 {
-    float m = 0.0f;
-    const int64_t total = d * ncols;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = t / ncols, c = t - k * ncols;
-        m = fmaxf(m, fabsf(XT[k * ld + c]));
-    }
+    float m = 0.0f;   // blocks stride over the feature rows, threads over the columns (no division)
+    for (int64_t k = blockIdx.x; k < d; k += gridDim.x)
+        for (int64_t c = threadIdx.x; c < ncols; c += blockDim.x) m = fmaxf(m, fabsf(XT[k * ld + c]));
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
