@@ -582,6 +582,10 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     SmoInfo info;
     CK(cudaMemcpyAsync(&info, E.info.p, sizeof info, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (!a.x_in_smem) {   // X^T's persisting L2 lines (launch_smo's access-policy window) -> normal
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);

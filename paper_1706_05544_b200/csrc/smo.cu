@@ -2091,9 +2091,47 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
 #undef SMO_PICK
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.nblk);
+    cfg.blockDim = dim3(SMO_THREADS);
+    cfg.dynamicSmemBytes = (size_t)smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+    // X streamed from HBM every iteration (not resident in shared memory): an L2 access-policy
+    // window marks this rank's X^T as persisting, so the part that fits the L2 set-aside stays
+    // in L2 across iterations (c4: X = 108 MB against a 126 MB L2).  Arithmetic is unchanged.
+    static size_t persist_max = (size_t)-1, window_max = 0;
+    if (persist_max == (size_t)-1) {
+        int dev = 0, pm = 0, wm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&pm, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&wm, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        persist_max = (size_t)pm;
+        window_max = (size_t)wm;
+        if (persist_max > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_max) != cudaSuccess) {
+            cudaGetLastError();
+            persist_max = 0;
+        }
+    }
+    const size_t xbytes = a.XT ? (size_t)a.d * (size_t)a.n_pad * sizeof(float) : 0;
+    if (a.XT && !a.x_in_smem && persist_max > 0 && window_max > 0 && !getenv("SVMB200_NO_L2PERSIST")) {
+        const size_t win = std::min(xbytes, window_max);
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = const_cast<float*>(a.XT);
+        attr[na].val.accessPolicyWindow.num_bytes = win;
+        attr[na].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist_max / (double)win);
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     svm_note_launches(1);
-    return cudaLaunchCooperativeKernel(fn, dim3(a.nblk), dim3(SMO_THREADS), args,
-                                       (size_t)smem_bytes, st);
+    return cudaLaunchKernelExC(&cfg, fn, args);   // (run_loop demotes the persisting lines after the loop)
 }
 
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
