@@ -983,7 +983,6 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     TRY(inner.alloc(sizeof(int64_t) * P));
     for (DBuf* b : {&Utc, &unorm, &ucoef, &done, &iters, &inner}) CK(cudaMemsetAsync(b->p, 0, b->bytes, st));
     const bool prof = getenv("SVMB200_PROFILE") != nullptr;
-    if (const char* e = getenv("SVMB200_OVR_DBG")) a.dbg = atoi(e);
     DBuf profb;
     if (prof) {
         TRY(profb.alloc(sizeof(long long) * 64 * 3));

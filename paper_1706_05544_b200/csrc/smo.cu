@@ -1574,8 +1574,10 @@ __global__ void k_absmax(const float* __restrict__ X, int64_t count, unsigned in
 }
 
 // Pipelined persistent pass (one CTA per SM) over 128-row tiles t = blockIdx.x + j gridDim.x:
-//   A producer  : one cp.async.bulk per K-chunk of the tile's pre-split X (16 KB) into a ring;
-//   U producer  : one cp.async.bulk per K-chunk of U (hi | lo, written by k_ovr_solve);
+//   producer    : per stage (K-chunk of 32 features) one cp.async.bulk of the tile's pre-split X
+//   (warp 0)      (16 KB) and one of U (hi | lo, written by k_ovr_solve) into an mbarrier ring;
+//                 the first stages' X is issued before griddepcontrol.wait (PDL), U after it;
+//   (warp 1 idle: the epilogue warps' TMEM lane quadrant is warp mod 4)
 //   MMA warp    : 3 kind::f16 MMAs per 16 features (M = 128, N = |U|), D[tile] in TMEM
 //                 columns (j & 1) NU (double-buffered), tcgen05.commit releases the slots;
 //   16 epilogue : per problem the kernel values of its 16 columns, G update, the tile's top-8;

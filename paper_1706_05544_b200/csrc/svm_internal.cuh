@@ -201,7 +201,6 @@ struct OvrArgs {
     int64_t* inner_total;      // [P]
     int na, nb;                // k_ovr_pass ring depths (set at launch)
     long long* prof;           // optional [warps][3] cycle counters of CTA 0's roles (profiling)
-    int dbg;                   // experiments only (SVMB200_OVR_DBG): 1 skip U loads, 2 skip X loads
 };
 int ovr_pass_smem(const OvrArgs& a);
 cudaError_t launch_ovr_pass(const OvrArgs& a, cudaStream_t st);
