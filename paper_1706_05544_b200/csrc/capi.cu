@@ -694,8 +694,10 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
     const float* qT = nullptr;
     const float* qnorm = nullptr;
     int64_t ld = 0;
-    // (the fp16-split kernel for d > 128 reads X^T with any leading dimension: no padded copy)
-    if (!D.csr && (D.n_pad % 128 == 0 || D.d > 128)) {
+    // the certification runs on the fp16-split kernel for every d (as predict does; 3xTF32 only
+    // with SVMB200_NO_F16): it reads X^T with any leading dimension, so no padded copy
+    const bool f16 = getenv("SVMB200_NO_F16") == nullptr;
+    if (!D.csr && (D.n_pad % 128 == 0 || D.d > 128 || f16)) {
         qT = D.XT.as<float>();
         qnorm = D.norms.as<float>();
         ld = D.n_pad;
@@ -717,13 +719,13 @@ static int training_decision(const Data& D, const DBuf& SVT, const DBuf& svn, in
     }
     DBuf SVtc;
     const float* svtc = nullptr;
-    if (pred_tc_dp(D.d)) {
+    if (pred_tc_dp(D.d) && !f16) {
         TRY(SVtc.alloc(sizeof(float) * pred_sv_tiles_floats(nsv_pad, D.d, 1)));
         CK(pred_sv_tiles(SVT.as<float>(), nsv_pad, D.d, coef_sv.as<double>(), 1, SVtc.as<float>(), st));
         svtc = SVtc.as<float>();
     }
     CK(pred_decision(qT, qnorm, D.n, ld, SVT.as<float>(), svn.as<float>(), nsv, nsv_pad, D.d,
-                     coef_sv.as<double>(), 1, kp, F.as<double>(), st, svtc));
+                     coef_sv.as<double>(), 1, kp, F.as<double>(), st, svtc, /*f16_any_d=*/f16));
     return SVM_OK;
 }
 

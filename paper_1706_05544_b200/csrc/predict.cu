@@ -22,6 +22,26 @@ namespace {
 
 constexpr int BQ = 128, BS = 64, BK = 16, PT = 256;
 
+// RBF epilogue of the tcgen05 decision kernels: K = exp(-g (|q|^2 + |s|^2 - 2 q.s)) evaluated as
+// 2^min(a dot + (ng |s|^2 + bq), 0) with ng = -g log2(e), bq = ng |q|^2 (per query) and a = -2 ng
+// times the operand scale: two FFMA, one FMNMX and one MUFU.EX2 per pair (kernel_from_dot's
+// generic switch, __expf range handling and separate scalings cost ~4x the issue slots).  The
+// min(., 0) is the d2 >= 0 clamp of kernel_from_dot.
+struct RbfEpi {
+    float a, ng, bq;
+};
+__device__ __forceinline__ RbfEpi rbf_epi(const KParams& kp, float dot_scale, float qn)
+{
+    const float ng = -kp.gamma * 1.4426950408889634f;
+    return {-2.0f * ng * dot_scale, ng, ng * qn};
+}
+__device__ __forceinline__ float rbf_k(const RbfEpi& r, float dot, float sn)
+{
+    float t = fminf(fmaf(r.a, dot, fmaf(r.ng, sn, r.bq)), 0.0f), y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
+    return y;
+}
+
 template <int NOUT>
 __global__ void __launch_bounds__(PT, 2)
     k_decision(const float* __restrict__ XqT, const float* __restrict__ qnorm, int64_t nq,
@@ -503,6 +523,36 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             EMARK(1)
             const float* sn = sSn + ss * TS + half * 16;
+            if (kp.kernel == 2) {
+                // RBF: kernel values once (two FFMA + FMNMX + EX2 each), then the contractions
+                const RbfEpi r = rbf_epi(kp, 1.0f, qn);
+                const float4* sn4 = reinterpret_cast<const float4*>(sn);
+                float kv[16];
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const float4 s = sn4[c4];
+                    kv[4 * c4 + 0] = rbf_k(r, __uint_as_float(v[4 * c4 + 0]), s.x);
+                    kv[4 * c4 + 1] = rbf_k(r, __uint_as_float(v[4 * c4 + 1]), s.y);
+                    kv[4 * c4 + 2] = rbf_k(r, __uint_as_float(v[4 * c4 + 2]), s.z);
+                    kv[4 * c4 + 3] = rbf_k(r, __uint_as_float(v[4 * c4 + 3]), s.w);
+                }
+#pragma unroll
+                for (int p = 0; p < NOUT; ++p) {
+                    if (p < n_out) {
+                        const float4* cf4 = reinterpret_cast<const float4*>(sCf + ((size_t)ss * NOUT + p) * TS + half * 16);
+                        float part = 0.0f;
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const float4 w = cf4[c4];
+                            part = fmaf(w.x, kv[4 * c4 + 0], part);
+                            part = fmaf(w.y, kv[4 * c4 + 1], part);
+                            part = fmaf(w.z, kv[4 * c4 + 2], part);
+                            part = fmaf(w.w, kv[4 * c4 + 3], part);
+                        }
+                        facc[p] += (double)part;
+                    }
+                }
+            } else {
 #pragma unroll
             for (int p = 0; p < NOUT; ++p) {
                 if (p < n_out) {
@@ -513,6 +563,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                         part = fmaf(cf[sI], kernel_from_dot(kp, __uint_as_float(v[sI]), qn, sn[sI]), part);
                     facc[p] += (double)part;
                 }
+            }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
@@ -763,21 +814,51 @@ __global__ void __launch_bounds__(DF_THREADS, 1)
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) df_arrive(b_acce + 8 * ab);
+                if (NOUT == 1 && kp.kernel == 2) {
+                    // RBF, one output: four partial sums (one per TMEM load), 16-byte smem reads
+                    const RbfEpi r = rbf_epi(kp, isg, qn);
+                    float ph[4];
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const float4* sn4 = reinterpret_cast<const float4*>(sn + cq * 64 + h * 16);
+                        const float4* cf4 = reinterpret_cast<const float4*>(cf + cq * 64 + h * 16);
+                        float acc = 0.0f;
+#pragma unroll
+                        for (int c4 = 0; c4 < 4; ++c4) {
+                            const float4 s = sn4[c4], w = cf4[c4];
+                            acc = fmaf(w.x, rbf_k(r, __uint_as_float(v[h][4 * c4 + 0]), s.x), acc);
+                            acc = fmaf(w.y, rbf_k(r, __uint_as_float(v[h][4 * c4 + 1]), s.y), acc);
+                            acc = fmaf(w.z, rbf_k(r, __uint_as_float(v[h][4 * c4 + 2]), s.z), acc);
+                            acc = fmaf(w.w, rbf_k(r, __uint_as_float(v[h][4 * c4 + 3]), s.w), acc);
+                        }
+                        ph[h] = acc;
+                    }
+                    facc[0] += (double)((ph[0] + ph[1]) + (ph[2] + ph[3]));
+                } else {
                 float part[NOUT];
 #pragma unroll
                 for (int p = 0; p < NOUT; ++p) part[p] = 0.0f;
+                auto contract = [&](auto kfun) {
 #pragma unroll
-                for (int h = 0; h < 4; ++h)
+                    for (int h = 0; h < 4; ++h)
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const int col = cq * 64 + h * 16 + c;
-                        const float kv = kernel_from_dot(kp, __uint_as_float(v[h][c]) * isg, qn, sn[col]);
+                        for (int c = 0; c < 16; ++c) {
+                            const int col = cq * 64 + h * 16 + c;
+                            const float kv = kfun(__uint_as_float(v[h][c]), sn[col]);
 #pragma unroll
-                        for (int p = 0; p < NOUT; ++p)
-                            if (p < n_out) part[p] = fmaf(cf[p * DF_SVB + col], kv, part[p]);
-                    }
+                            for (int p = 0; p < NOUT; ++p)
+                                if (p < n_out) part[p] = fmaf(cf[p * DF_SVB + col], kv, part[p]);
+                        }
+                };
+                if (kp.kernel == 2) {
+                    const RbfEpi r = rbf_epi(kp, isg, qn);
+                    contract([&](float dot, float s) { return rbf_k(r, dot, s); });
+                } else {
+                    contract([&](float dot, float s) { return kernel_from_dot(kp, dot * isg, qn, s); });
+                }
 #pragma unroll
                 for (int p = 0; p < NOUT; ++p) facc[p] += (double)part[p];
+                }
             }
             if (qi < nq) {
                 const int64_t count = nq * n_out;
