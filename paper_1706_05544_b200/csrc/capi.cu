@@ -799,6 +799,19 @@ static int solve_problem(const Data& D, Problem& P, Exchange& E, const svm_param
     return certify_resume(D, P, E, prm, st);
 }
 
+// After a failed certification G has been recomputed from the SVs (fp64 accumulation), so the
+// resumed loop starts from an accurate G; it stops below tol by resume_factor() times the measured
+// excess (the fp32 drift of the first loop), and at least 1% of tol below the previous stop.
+static double resume_factor()
+{
+    static double f = -1;
+    if (f < 0) {
+        const char* e = getenv("SVMB200_RESUME_K");
+        f = e ? atof(e) : 0.5;
+    }
+    return f;
+}
+
 // Certification (a4, reading R16) and resumption of the persistent loop after a loop stopped.
 static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
                           cudaStream_t st)
@@ -819,7 +832,7 @@ static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_para
         if (viol <= P.tol) { P.converged = true; break; }
         P.converged = false;
         // fp32 G stopped just inside tol: resume below it by 4x the measured excess (>= 1% of tol)
-        P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - 4.0 * (viol - P.tol));
+        P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - resume_factor() * (viol - P.tol));
         int64_t left = P.max_iter - P.iterations;
         if (left <= 0) break;
         TRY(run_loop(D, P, E, left, st, nullptr));
@@ -1858,7 +1871,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
             TRY(shard_certify(S, P, &viol));
             if (viol <= P.tol) break;
             P.converged = false;
-            P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - 4.0 * (viol - P.tol));
+            P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - resume_factor() * (viol - P.tol));
             int64_t left = P.max_iter - P.iterations;
             if (left <= 0) break;
             TRY(run_loop(D, P, S->E, left, S->st, nullptr, &S->sc));
