@@ -1031,8 +1031,19 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
     const int nqt = (int)((nq + 127) / 128);
     const int nsb = (int)((std::max<int64_t>(nsv, 1) + DF_SVB - 1) / DF_SVB);   // blocks of the real SVs
     const int64_t nsv_ld = (int64_t)nsb * DF_SVB;
+    // SV splits: items (query tile, split) go round-robin to the nsm CTAs, so the makespan is
+    // ceil(items / nsm) * bps blocks; take the split count with the best balance (c2: 3 splits,
+    // 98% against 88% for the old "items >= 4 nsm" rule)
     int nsplit = 1;
-    while (nsplit < nsb && (int64_t)nqt * nsplit < 4 * nsm) ++nsplit;
+    {
+        double best = -1;
+        for (int ns = 1; ns <= std::min(nsb, n_out > 1 ? 4 : 16); ++ns) {   // (16 outputs: partials 8 x 16 B per query per split)
+            const int b = (nsb + ns - 1) / ns, nse = (nsb + b - 1) / b;
+            const int64_t items = (int64_t)nqt * nse, waves = (items + nsm - 1) / nsm;
+            const double eff = (double)nqt * nsb / ((double)waves * nsm * b);
+            if (eff > best + 0.01) { best = eff; nsplit = nse; }
+        }
+    }
     const int bps = (nsb + nsplit - 1) / nsplit;
     nsplit = (nsb + bps - 1) / bps;
     const size_t qh_b = (size_t)nqt * nkc * DF_ATILE * 2, sh_b = (size_t)nsb * nkc * DF_BTILE * 2;
