@@ -789,16 +789,33 @@ __global__ void __launch_bounds__(DF_THREADS, 1)
             double facc[NOUT];
 #pragma unroll
             for (int p = 0; p < NOUT; ++p) facc[p] = 0.0;
+            // the coefficients and norms of SV block sb + 1 are loaded into registers while block
+            // sb is computed (their L2 latency used to stall every block before its barrier)
+            constexpr int PF = (NOUT * DF_SVB + DF_EPI * 32 - 1) / (DF_EPI * 32);
+            float rcf[PF], rsn = 0.0f;
+            auto load_block = [&](int sb) {
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const int x = et + u * DF_EPI * 32, p = x / DF_SVB, c = x - p * DF_SVB;
+                    rcf[u] = x < n_out * DF_SVB ? coef32[(int64_t)p * nsv_ld + (int64_t)sb * DF_SVB + c] : 0.0f;
+                }
+                if (et < DF_SVB) rsn = svnorm[(int64_t)sb * DF_SVB + et];
+            };
+            if (b0 < b1) load_block(b0);
             for (int sb = b0; sb < b1; ++sb, ++j) {
                 const int ab = j & 1;
                 float* cf = sCf + (size_t)ab * NOUT * DF_SVB;
                 float* sn = sSn + ab * DF_SVB;
-                for (int x = et; x < n_out * DF_SVB; x += DF_EPI * 32) {
-                    const int p = x / DF_SVB, c = x - p * DF_SVB;
-                    cf[p * DF_SVB + c] = coef32[(int64_t)p * nsv_ld + (int64_t)sb * DF_SVB + c];
+                // (slot ab was last read in block j - 2: every epilogue thread has passed the
+                // barrier of block j - 1 since)
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const int x = et + u * DF_EPI * 32;
+                    if (x < n_out * DF_SVB) cf[x] = rcf[u];   // [p][DF_SVB] = x
                 }
-                if (et < DF_SVB) sn[et] = svnorm[(int64_t)sb * DF_SVB + et];
+                if (et < DF_SVB) sn[et] = rsn;
                 df_epi_bar();
+                if (sb + 1 < b1) load_block(sb + 1);
                 df_wait_sleep(b_accf + 8 * ab, (uint32_t)((j >> 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 uint32_t v[4][16];
