@@ -96,6 +96,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's start-up (NVML init) holds driver locks for tens of ms and used to
+            # stall the host launches of the first timed steps (c3: 141 -> 200+ ms): wait for its
+            # first sample, so that the timed region starts with the sampler already running
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self

@@ -8,6 +8,7 @@ import paper_1706_05544_b200 as pkg
 from paper_1706_05544_b200 import synth
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+retrain = len(sys.argv) > 3 and sys.argv[3] == "retrain"   # a new model before every predict (as bench.py)
 ds = synth.make(cfg)
 q = synth.make(cfg, n=min(ds.n, 100000), heldout=True)
 reg = ds.svm_type == synth.EPS_REGRESSION
@@ -15,6 +16,8 @@ kw = dict(svm_type="eps-regression" if reg else "C-classification", gamma=1.0 / 
 m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), **kw)
 Xq = torch.from_numpy(q.X).cuda()
 for r in range(reps):
+    if retrain:
+        m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), **kw)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); out = m.predict(Xq); e1.record(); torch.cuda.synchronize()
