@@ -334,10 +334,13 @@ def main():
     pred_s = statistics.mean(pr) / 1e3
     step_ms = statistics.mean(a + b for a, b in zip(tr, pr))
     info = infos[-1]
+    # per-iteration candidate exchange (the collective of SURVEY 8(e), fused into the persistent
+    # kernel): CTA 0's publish -> every slot staged, as a share of the device-timed loop
+    exch_us = info.exchange_ms * 1e3 / max(1, info.iterations)
     if world > 1:
-        t = torch.tensor([train_s, pred_s, step_ms], device=dev)
+        t = torch.tensor([train_s, pred_s, step_ms, exch_us], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        train_s, pred_s, step_ms = t.tolist()
+        train_s, pred_s, step_ms, exch_us = t.tolist()
     # ---- roofline of the persistent working-set kernel ---------------------------------------
     peaks, peak_src = measured_peaks()
     n_rows_local = r1 - r0
@@ -427,6 +430,12 @@ def main():
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(),
         }
+        if not getattr(info, "batched", 0):
+            line["exchange"] = {
+                "us_per_iteration": exch_us, "frac_of_loop": exch_us * info.iterations / 1e3 / max(info.loop_ms, 1e-9),
+                "measured": "clock64 on CTA 0 (max over ranks): its candidate publish -> every CTA's "
+                            "keys staged (transport + wait for the slowest CTA); in-kernel NVLink "
+                            "peer-memory exchange, no NCCL call per iteration"}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

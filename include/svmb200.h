@@ -109,6 +109,11 @@ typedef struct svm_model_info {
                           /* rest passes the mean of CUDA event pairs around every 8th k_ovr_pass */
                           /* launch times the launch count                                        */
     int32_t batched;      /* 1 if the one-vs-rest problems iterated together      */
+    double exchange_ms;   /* part of loop_ms the persistent kernel spent in the per-iteration    */
+                          /* candidate exchange (a1), measured on CTA 0 of this rank: from its  */
+                          /* publish until every CTA's (every rank's, when sharded) keys are    */
+                          /* staged -- transport latency plus the wait for the slowest CTA.     */
+                          /* 0 for the batched one-vs-rest passes.                               */
 } svm_model_info;
 
 /*

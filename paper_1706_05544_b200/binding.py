@@ -54,7 +54,7 @@ class svm_model_info(ctypes.Structure):
                 ("train_ms", ctypes.c_double), ("loop_ms", ctypes.c_double),
                 ("setup_ms", ctypes.c_double), ("certify_ms", ctypes.c_double),
                 ("passes", ctypes.c_int64), ("pass_ms", ctypes.c_double),
-                ("batched", ctypes.c_int32)]
+                ("batched", ctypes.c_int32), ("exchange_ms", ctypes.c_double)]
 
 
 class svm_solver_stats(ctypes.Structure):

@@ -395,6 +395,7 @@ struct Problem {
     bool converged = false, certified = false;
     double tol_loop = 0;   // the loop's stop threshold: tol, lowered after a failed certification (R16)
     double loop_ms = 0, cert_ms = 0;
+    double exch_ms = 0;    // share of loop_ms CTA 0 spent in the candidate exchange
     int64_t passes = 0;    // X passes of the dominant pass kernel (batched one-vs-rest: k_ovr_pass)
     double pass_ms = 0;    // their device time (CUDA event pairs around each launch)
     SmoInfo last_info;
@@ -597,6 +598,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     P.M_low = info.M_low;
     P.converged = info.converged != 0;
     P.loop_ms += ms;
+    if (info.loop_cycles > 0) P.exch_ms += ms * (double)info.exch_cycles / (double)info.loop_cycles;
     P.last_info = info;
     if (getenv("SVMB200_PROFILE")) {
         int clk = 0, dev = 0;
@@ -1129,7 +1131,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     TRY(E.alloc(D.nblk));
     std::vector<Problem> probs(ys.size());
     std::vector<double> bs(ys.size());
-    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, pass_ms = 0;
+    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, pass_ms = 0, exch_ms = 0;
     int64_t iters = 0, passes = 0;
     bool conv = true, cert = true;
     for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
@@ -1150,6 +1152,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
         conv = conv && P.converged;
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
+        exch_ms += P.exch_ms;
         cert_ms += P.cert_ms;
         if (!batched) { passes += P.iterations; pass_ms += P.loop_ms; }
     }
@@ -1186,6 +1189,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     I.certified = cert ? 1 : 0;
     I.dual_objective = dual;
     I.loop_ms = loop_ms;
+    I.exchange_ms = exch_ms;
     I.certify_ms = cert_ms;
     I.setup_ms = t_setup;
     I.passes = passes;
@@ -1857,7 +1861,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     TRY(shard_xchg(S, {0.0}, none, 300.0));        // start barrier
     std::vector<Problem> probs(S->nprob);
     std::vector<double> bs(S->nprob);
-    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0;
+    double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, exch_ms = 0;
     int64_t iters = 0;
     bool conv = true, cert = true;
     for (int p = 0; p < S->nprob; ++p) {
@@ -1886,6 +1890,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         conv = conv && P.converged;
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
+        exch_ms += P.exch_ms;
         cert_ms += P.cert_ms;
     }
     // model: union of SVs over problems, coefficients of every problem, rows gathered
@@ -1948,6 +1953,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     I.certified = cert ? 1 : 0;
     I.dual_objective = dual;
     I.loop_ms = loop_ms;
+    I.exchange_ms = exch_ms;
     I.certify_ms = cert_ms;
     I.passes = iters;
     I.pass_ms = loop_ms;

@@ -878,6 +878,13 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
     exact_select();
     publish(a.tag0 + 1);
+    // per-iteration exchange latency (CTA 0, thread 0): its publish -> every rank's slots staged.
+    // Includes the wait for the slowest CTA of any rank, i.e. what the collective costs the loop.
+    // One 32-bit register across the loop (differences mod 2^32); the sums go out as fire-and-
+    // forget reductions into the zeroed info block.
+    uint32_t x_pub = (uint32_t)clock();
+    if (reporter && tid == 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->loop_cycles), (unsigned long long)(-clock64()));
 
 #ifdef SMO_PROFILE
     // B200 __syncthreads is BAR.SYNC.DEFER_BLOCKING: the warp only blocks at the next use of
@@ -959,6 +966,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
         }
         __syncthreads();
+        if (reporter && tid == 0) {   // a shared load first: the barrier is DEFER_BLOCKING
+            const int v = *reinterpret_cast<volatile int*>(&sh.timeout);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->exch_cycles),
+                      (unsigned long long)(uint32_t)((uint32_t)clock() - x_pub + (uint32_t)(v & 0)));
+        }
         mark(0);
         if (sh.timeout) {
             if (reporter && tid == 0) a.info->error = 1;
@@ -1088,6 +1100,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 a.info->m_up = sh.m_up;
                 a.info->M_low = sh.M_low;
                 a.info->converged = (sh.m_up - sh.M_low <= a.tol) ? 1 : 0;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->loop_cycles), (unsigned long long)clock64());
             }
 #ifdef SMO_PROFILE
             if (reporter && tid == SOLVER_WARP * 32)
@@ -1402,6 +1415,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         mark(6);
         wmark(5);
         publish(tag + 1);
+        if (reporter && tid == 0) x_pub = (uint32_t)clock();
         mark(7);
     }
 }

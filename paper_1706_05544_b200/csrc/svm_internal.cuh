@@ -120,6 +120,8 @@ struct SmoInfo {
     double last_dalpha[SVM_WS];
     int64_t inner_total;
     int64_t phase_cycles[16]; // CTA 0: clock64 per phase (solver [0,8), worker warp 0 [8,16))
+    int64_t exch_cycles;      // CTA 0, thread 0: clock64 from its publish to all slots staged
+    int64_t loop_cycles;      // CTA 0, thread 0: clock64 over the whole loop (prologue excluded)
 };
 
 // All arguments of the persistent working-set kernel (passed by value).
