@@ -31,7 +31,10 @@ def _cuda():
     pkg.lib()
 
 
-def _sample_checks(ds, model, reg, rng, n_sample=300):
+def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=200,
+                   held_rows=None):
+    """prob: which binary problem of the model (one-vs-rest: class index); ybin: its +-1 labels
+    (default: the binary mapping of ds.y)."""
     import torch  # noqa: F401  (device already initialised by the fixture)
     C, tol = 1.0, 1e-3
     ks = ora.kspec("rbf", 1.0 / ds.d, d=ds.d)
@@ -39,7 +42,7 @@ def _sample_checks(ds, model, reg, rng, n_sample=300):
     assert info.converged == 1 and info.certified == 1
     assert info.dual_objective <= 0.0
     idx, coef = model.support()
-    coef = coef[0]
+    coef = coef[prob]
     # invariants from the coefficients: box and the equality constraint of Eq. 2
     assert (np.abs(coef) <= C * (1 + 1e-12)).all()
     if reg:
@@ -65,7 +68,7 @@ def _sample_checks(ds, model, reg, rng, n_sample=300):
                 if (yv > 0 and a > 0) or (yv < 0 and a < C):
                     low.append(s)
     else:
-        y = ora.binary_labels(ds.y)[0][rows].astype(np.float64)
+        y = (ora.binary_labels(ds.y)[0] if ybin is None else ybin)[rows].astype(np.float64)
         for k, r in enumerate(rows):
             a = abs(c_row[r])
             G = -1.0 + y[k] * f[k]
@@ -78,7 +81,7 @@ def _sample_checks(ds, model, reg, rng, n_sample=300):
     # sampled held-out decision values vs the oracle's fp64 decision of the same model
     H = synth.make(ds.name, n=2000, heldout=True)
     Xh = H.dense() if H.is_csr else H.X
-    hr = rng.choice(Xh.shape[0], size=200, replace=False)
+    hr = rng.choice(Xh.shape[0], size=n_held, replace=False) if held_rows is None else held_rows
     if H.is_csr:
         sub = Xh[hr]
         ip = np.concatenate([[0], np.cumsum((sub != 0).sum(1))]).astype(np.int64)
@@ -86,13 +89,14 @@ def _sample_checks(ds, model, reg, rng, n_sample=300):
                                      decision=True)
     else:
         out, dec = model.predict(Xh[hr], decision=True)
-    fo = ora.decision(SV, coef, info.b[0], ks, Xh[hr])
+    fo = ora.decision(SV, coef, info.b[prob], ks, Xh[hr])
     # fp32 kernel values carry a few ulps each: bound by 1e-5 sum_s |coef_s K_s| (+1e-6), which
     # the oracle evaluates exactly (RBF K >= 0); north_star's end-to-end bar is 1e-3 absolute.
     mass = ora.decision(SV, np.abs(coef), 0.0, ks, Xh[hr])
-    err = np.abs(dec[:, 0] - fo)
+    err = np.abs(dec[:, prob] - fo)
     assert (err <= 1e-5 * mass + 1e-6).all(), (err.max(), (err / (mass + 1e-12)).max())
     assert err.max() <= 1e-3
+    return dec, fo
 
 
 def test_c2_full_size():
@@ -110,6 +114,34 @@ def test_c4_full_size():
     import torch
     m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d)
     _sample_checks(ds, m, False, np.random.default_rng(1))
+
+
+def test_c3_full_size_ovr():
+    """configs[2]: 10-class one-vs-rest C-SVC, MNIST-shaped 60,000 x 784 (the batched tcgen05
+    passes bench.py times).  Every class problem is checked on its own sample (y = +1 iff the
+    label is that class, S:325 / BASELINE config 3), and the one-vs-rest label is the argmax of
+    the decision values (ties -> lowest class)."""
+    ds = synth.make("c3")
+    import torch
+    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d)
+    info = m.info
+    assert info.n_problem == 10 and info.n_class == 10
+    labels = np.array(info.labels[:10])
+    assert sorted(labels.tolist()) == sorted(set(ds.y.astype(np.float64).tolist()))
+    H = synth.make("c3", n=2000, heldout=True)
+    hr = np.random.default_rng(30).choice(H.n, size=60, replace=False)
+    fo_all = np.empty((60, 10))
+    for p in range(10):
+        ybin = np.where(ds.y.astype(np.float64) == labels[p], 1.0, -1.0)
+        _, fo_all[:, p] = _sample_checks(ds, m, False, np.random.default_rng(30), n_sample=100,
+                                         prob=p, ybin=ybin, held_rows=hr)
+    out, dec = m.predict(H.X[hr], decision=True)
+    assert np.array_equal(out, labels[np.argmax(dec, axis=1)].astype(np.float32))
+    # labels agree with the oracle's argmax wherever the oracle's top-2 gap exceeds the
+    # decision tolerance (1e-3); north_star asks >= 99.9% agreement overall
+    srt = np.sort(fo_all, axis=1)
+    clear = srt[:, -1] - srt[:, -2] > 2e-3
+    assert np.array_equal(out[clear], labels[np.argmax(fo_all, axis=1)][clear].astype(np.float32))
 
 
 def test_c5_csr_sample_size():
