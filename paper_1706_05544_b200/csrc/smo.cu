@@ -355,6 +355,76 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
                                              const float (&acc)[RPT][SVM_WS],
                                              uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT])
 {
+    if constexpr (RPT == 4) {
+        // A lane's 4 rows are consecutive and li0 is a multiple of 4 (rows_per_cta and n_pad are):
+        // the norms, G and status of all 4 rows (both copies) are loaded up front as one 16-byte /
+        // one 4-byte load per array, before any store.  (Row by row, the uint8_t status load of
+        // row j + 1 may alias the G store of row j, so the compiler kept 4 dependent global round
+        // trips per call.)  Identical arithmetic; rows >= cta_end are never written.
+#pragma unroll
+        for (int q = 0; q < 2 * RPT; ++q) ku[q] = kl[q] = 0ull;
+        if (li0 >= cta_end) return;
+        float4 g4[2];
+        uint32_t st4[2] = {0u, 0u};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            g4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < a.ncopy) {
+                const int64_t idx = (int64_t)c * a.n_pad + li0;
+                st4[c] = *reinterpret_cast<const uint32_t*>(a.status + idx);
+                g4[c] = *reinterpret_cast<const float4*>(a.G + idx);
+            }
+        }
+        float S[4] = {0.f, 0.f, 0.f, 0.f};
+        if (do_update) {
+            const float4 xn4 = __ldg(reinterpret_cast<const float4*>(a.xnorm + li0));
+            const float xn[4] = {xn4.x, xn4.y, xn4.z, xn4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if constexpr (RBFK) {
+                    const float ng = -a.kp.gamma * 1.4426950408889634f;
+#pragma unroll
+                    for (int r = 0; r < SVM_WS; ++r) {
+                        const float d2 = fmaxf(fmaf(-2.0f, acc[j][r], xn[j] + sh.xn[r]), 0.0f);
+                        S[j] = fmaf(sh.c[r], exp2f_approx(ng * d2), S[j]);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < SVM_WS; ++r)
+                        S[j] = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn[j], sh.xn[r]), S[j]);
+                }
+            }
+        }
+        const bool full = li0 + 4 <= cta_end;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (c >= a.ncopy) break;
+            float g[4] = {g4[c].x, g4[c].y, g4[c].z, g4[c].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t st = (st4[c] >> (8 * j)) & 0xffu;
+                const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
+                if (do_update) g[j] = fmaf(yv, S[j], g[j]);
+                const float sc = -yv * g[j];
+                const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(a.row0 + li0 + j);
+                const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)gi);
+                const bool in = li0 + j < cta_end;
+                if (in && st_in_up(st)) ku[2 * j + c] = ((uint64_t)ord_f32(sc) << 32) | lo;
+                if (in && st_in_low(st)) kl[2 * j + c] = ((uint64_t)ord_f32(-sc) << 32) | lo;
+            }
+            if (do_update) {
+                const int64_t idx = (int64_t)c * a.n_pad + li0;
+                if (full) {
+                    *reinterpret_cast<float4*>(a.G + idx) = make_float4(g[0], g[1], g[2], g[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (li0 + j < cta_end) a.G[idx + j] = g[j];
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int64_t li = li0 + j;
