@@ -425,6 +425,24 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
         }
         return;
     }
+    // RPT 1 / 2: every row's status, G and norm loaded before the first G store (as above)
+    uint32_t stv[RPT][2];
+    float gv[RPT][2], xnv[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int64_t li = li0 + j;
+        xnv[j] = (do_update && li < cta_end) ? __ldg(a.xnorm + li) : 0.0f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            stv[j][c] = 0u;
+            gv[j][c] = 0.0f;
+            if (li < cta_end && c < a.ncopy) {
+                const int64_t idx = (int64_t)c * a.n_pad + li;
+                stv[j][c] = a.status[idx];
+                gv[j][c] = a.G[idx];
+            }
+        }
+    }
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int64_t li = li0 + j;
@@ -432,7 +450,7 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
         if (li >= cta_end) continue;
         float S = 0.0f;
         if (do_update) {
-            const float xn = __ldg(a.xnorm + li);
+            const float xn = xnv[j];
             if constexpr (RBFK) {  // exp(-gamma |x_i - x_r|^2) with the distance from the norms
                 const float ng = -a.kp.gamma * 1.4426950408889634f;  // exp(z) = 2^(z log2 e)
 #pragma unroll
@@ -450,9 +468,9 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
         for (int c = 0; c < 2; ++c) {
             if (c >= a.ncopy) break;
             const int64_t idx = (int64_t)c * a.n_pad + li;
-            const uint32_t st = a.status[idx];
+            const uint32_t st = stv[j][c];
             const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
-            float g = a.G[idx];
+            float g = gv[j][c];
             if (do_update) {
                 g = fmaf(yv, S, g);
                 a.G[idx] = g;
