@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libsvmb200.so")
-SOURCES = ["smo.cu", "layout.cu", "predict.cu", "capi.cu", "shard.cu"]
+SOURCES = ["smo.cu", "layout.cu", "predict.cu", "capi.cu"]
 HEADERS = ["svm_internal.cuh", "layout.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
