@@ -4,18 +4,24 @@
 One step = one pass of the whole hot path over the bench workload:
   svm_train to KKT tolerance (problem build, selection, subproblem, fused kernel-row + gradient
   pass, certification, bias, model extraction) + svm_predict of the held-out rows.
-Workload (BASELINE.json configs[1], the metric's config): c2 = eps-SVR, RBF, Friedman #1 in
-100-d, n = 50,000 (m = 100,000 dual variables), gamma = 1/d, C = 1, eps = 0.1, tol = 1e-3, |W| = 16;
-held-out predict set n_q = 50,000 (seed + 100).  Data: seeded synthetic (paper_1706_05544_b200.synth).
+Workload (default): c4 = binary C-SVC, RBF, covertype-shaped, n = 500,000 x d = 54 dense
+(BASELINE.json configs[3]) -- the largest dense config that fits one GPU and the one north_star
+names for HBM evidence and 1/2/4/8-GPU scaling (BASELINE.json's metric names no config).  gamma =
+1/d, C = 1, tol = 1e-3, |W| = 16; held-out predict set n_q = 100,000 (seed + 100).  Data: seeded
+synthetic (paper_1706_05544_b200.synth).  --config c1..c5 selects another BASELINE config.
 
 metric/value: BASELINE.json's metric; value = train time to KKT tol [s] (mean over timed steps,
   CUDA events on the library's stream, max over ranks); lower is better.
-e2e: the same through the C ABI with pinned HOST buffers (H2D of X, y, Xq and D2H of labels and
-  the model inside the timed region).
+e2e: one full step through the public API from pinned HOST buffers: svm_train (H2D of X and y
+  inside) + svm_predict of the held-out rows (H2D of Xq, D2H of the labels) [s].
 roofline: the persistent working-set kernel (the dominant kernel): algorithmic bytes of the fused
-  pass (n (4d + 22) B per iteration for eps-SVR) x iterations / its device time.
-cpu_baseline: the fp64 oracle (oracle/) on the host cores, a bounded sample of the same workload.
---impl reference: the oracle arm of the contract (rank 0 only).
+  pass (n (4d + 13) B per iteration for C-SVC) x iterations / its device time.  "pass_only": the
+  same fused a3 pass timed in isolation (svm_solver_pass_bench: W fixed, no exchange, no
+  subproblem) -- the north_star "fused kernel-row + gradient step" GB/s.
+cpu_baseline: the fp64 oracle (oracle/) on the host cores: a bounded sample (the first k SMO
+  iterations of the same workload), scaled to the metric with the ORACLE's own iteration count to
+  tol (tests/golden/full_<cfg>.npz, written by scripts/make_goldens.py from oracle/ alone).
+--impl reference: the oracle arm of the contract (rank 0 only), the same sample and scaling.
 
 Multi-GPU (torchrun, N > 1): rows are sharded (svm_shard_*), candidates exchanged over NVLink peer
 memory inside the kernel; the model is identical on all ranks; predict shards the query rows.
@@ -35,8 +41,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "train time to KKT tol & fused kernel-row GB/s vs HBM peak; predict rows/s"
-# iterations to KKT tol of each workload on this path (B200 runs of this round; the oracle runs
-# the same algorithm in fp64): used only to project the oracle's bounded sample to the metric.
 ROOF_NOTES = {
     "c1": "2,000 rows on 8 CTAs: launch/serial latency bound; see DESIGN.md",
     "c2": "X is SMEM-resident for c2 (135 KB per CTA): the per-iteration chain (exchange, merge, "
@@ -47,7 +51,6 @@ ROOF_NOTES = {
     "c5": "CSR pass: per-warp staged nonzeros, masked X_W groups in shared memory (L1/shared-pipe "
           "bound, not HBM); algorithmic bytes 8 nnz + 17 n per iteration; see DESIGN.md",
 }
-ITERS_TO_TOL = {"c1": 296, "c2": 19291, "c3": 10531, "c4": 68611, "c5": 280000}
 WORKLOADS = {
     "c1": "binary C-SVC, RBF, two Gaussian blobs, n=2,000 d=20 dense",
     "c2": "eps-SVR, RBF, Friedman #1, n=50,000 d=100 dense (m=100,000 duals)",
@@ -66,9 +69,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--config", default="c4", choices=list(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pass", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -156,24 +160,85 @@ def fused_bytes_per_iter(cfg, n_rows, d, ncopy, nnz=None):
     return n_rows * (4 * d + 4 + 9 * ncopy)
 
 
+def oracle_to_tol(cfg):
+    """The oracle's own run to tol at the full BASELINE size (tests/golden/full_<cfg>.npz, written
+    by scripts/make_goldens.py, which imports only oracle/ and synth): iterations summed over the
+    problems, wall seconds and threads of that run.  None when the config has no golden."""
+    path = os.path.join(ROOT, "tests", "golden", f"full_{cfg}.npz")
+    if not os.path.exists(path):
+        return None
+    import numpy as np
+    g = np.load(path)
+    return {"iterations": int(np.sum(g["iterations"])), "wall_s": float(g["wall_s"]),
+            "threads": int(g["threads"]), "source": os.path.relpath(path, ROOT)}
+
+
 def cpu_baseline(ds, kw, seconds):
     """The fp64 oracle as it stands, on a bounded sample: the first k SMO iterations of the same
-    workload (k sized to ~`seconds`), projected to the workload's iteration count to tol."""
+    workload (first problem; k sized to ~`seconds`).  Returns (seconds, k, threads)."""
     import oracle as ora
     reg = kw["svm_type"] == "eps-regression"
-    prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
-                       ds.y if reg else ora.binary_labels(ds.y)[0], ds.n, kw.get("epsilon", 0.1))
+    if reg:
+        yb = ds.y
+    elif len(set(ds.y.tolist())) > 2:          # one-vs-rest: the first class against the rest
+        yb = (ds.y == ds.y[0]).astype("float32") * 2 - 1
+    else:
+        yb = ora.binary_labels(ds.y)[0]
+    prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION, yb, ds.n,
+                       kw.get("epsilon", 0.1))
     ks = ora.kspec("rbf", kw["gamma"], d=ds.d)
     X = ds.X if ds.X is not None else ds.dense()   # c5: the oracle takes the densified rows
     t = time.perf_counter()
     ora.train_dual(X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=2)
     per = (time.perf_counter() - t) / 2
-    k = max(2, min(5000, int(seconds / max(per, 1e-6))))
+    k = max(2, min(20000, int(seconds / max(per, 1e-6))))
     t = time.perf_counter()
     r = ora.train_dual(X, prob, ks, C=kw["cost"], tol=kw["tolerance"], max_iter=k)
     el = time.perf_counter() - t
-    k = max(1, r["iterations"])
-    return el, k, ora.num_threads()
+    return el, max(1, r["iterations"]), ora.num_threads()
+
+
+def host_cpu():
+    """lscpu-style record of the host the oracle ran on (model, sockets, cores)."""
+    rec = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                rec[k] = v
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return rec
+
+
+def cpu_record(cfg, el, k, cores):
+    """cpu_baseline object: the sample's iterations/s, scaled to train time to tol with the
+    oracle's own iteration count (no GPU number enters); did_not_finish when none exists."""
+    ref = oracle_to_tol(cfg)
+    rec = {"unit": "s", "cores": cores, "kind": "oracle", "iterations_per_s": k / el,
+           "host": host_cpu(),
+           "sample": f"first {k} SMO iterations of {cfg} at full size in {el:.1f} s"}
+    if ref is None:
+        rec.update(value=None, did_not_finish=True,
+                   note="no oracle run to tol at this size (SURVEY 8(d)): iterations/s only")
+    else:
+        rec.update(value=el / k * ref["iterations"],
+                   scaled_to=f"{ref['iterations']} iterations to tol of the oracle's own full "
+                             f"run ({ref['source']}: {ref['wall_s']:.0f} s on {ref['threads']} "
+                             "threads of the build host)")
+    return rec
+
+
+def config_object(cfg, ds, hq_n, kw, world):
+    """The `config` object of both arms (identical keys and values)."""
+    ncopy = 2 if kw["svm_type"] == "eps-regression" else 1
+    return {"workload": f"{cfg}: {WORKLOADS[cfg]}", "n": ds.n, "d": ds.d, "duals": ds.n * ncopy,
+            "heldout_rows": hq_n, "C": kw["cost"], "gamma": kw["gamma"],
+            "epsilon": kw["epsilon"], "tolerance": kw["tolerance"], "working_set": 16,
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "l2": "flushed (256 MB write) before every timed step"}
 
 
 def run_reference(args):
@@ -182,28 +247,51 @@ def run_reference(args):
         return 0
     from paper_1706_05544_b200 import synth
     ds = synth.make(args.config)
+    hq_n = min(ds.n, 100000)
     kw = workload_params(ds)
-    iters = ITERS_TO_TOL.get(args.config, 10000)
-    vals, samples = [], []
+    vals, walls, recs = [], [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         el, k, cores = cpu_baseline(ds, kw, args.cpu_seconds)
+        wall = time.perf_counter() - t0
         if i >= args.warmup:
-            vals.append(el / k * iters)
-            samples.append((el, k))
-    v = statistics.mean(vals)
-    sample = (f"first {samples[0][1]} SMO iterations of {args.config} (full n={ds.n}, d={ds.d}) per "
-              f"step ({statistics.mean(s[0] for s in samples):.1f} s), projected to "
-              f"{iters} iterations to tol")
+            rec = cpu_record(args.config, el, k, cores)
+            recs.append(rec)
+            walls.append(wall)
+            vals.append(rec["value"])
+    rec = recs[-1]
+    v = statistics.mean(vals) if vals[0] is not None else None
+    if v is not None:
+        rec["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}"},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+            "ms_per_step": statistics.mean(walls) * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_object(args.config, ds, hq_n, kw, args.gpus),
+            "projected": v is not None,
+            "ms_per_step_is": "wall time of the bounded oracle sample each step ran",
+            "cpu_baseline": rec,
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pass_only(pkg, X, y, kw, ncopy, n, d, peaks, passes=200):
+    """The fused a3 pass (kernel rows + G update + candidate selection) in its production launch,
+    timed in isolation: svm_solver_pass_bench with W = 16 fixed rows, `passes` passes in one
+    launch (CUDA events on the library's stream).  Algorithmic bytes per pass: n (4d + 4 + 9 ncopy)."""
+    import numpy as np
+    s = pkg.Solver(X, y, **kw)
+    rows = np.linspace(0, n - 1, 16).astype(np.int64)
+    coef = np.full(16, 1e-6, np.float32)   # tiny: G stays near p over the passes
+    s.pass_bench(rows, coef, 4)            # warm
+    ms = s.pass_bench(rows, coef, passes)
+    bpp = n * (4 * d + 4 + 9 * ncopy)
+    gbs = bpp * passes / (ms / 1e3) / 1e9
+    return {"kernel": "smo_persistent, pass-only mode (svm_solver_pass_bench)",
+            "passes": passes, "us_per_pass": ms * 1e3 / passes,
+            "algorithmic_bytes_per_pass": bpp, "achieved": gbs, "unit": "GB/s",
+            "peak": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"]}
 
 
 def batched_roofline(info, n, d, peaks, peak_src):
@@ -337,10 +425,11 @@ def main():
     # per-iteration candidate exchange (the collective of SURVEY 8(e), fused into the persistent
     # kernel): CTA 0's publish -> every slot staged, as a share of the device-timed loop
     exch_us = info.exchange_ms * 1e3 / max(1, info.iterations)
+    p50, p99 = info.exchange_p50_us, info.exchange_p99_us
     if world > 1:
-        t = torch.tensor([train_s, pred_s, step_ms, exch_us], device=dev)
+        t = torch.tensor([train_s, pred_s, step_ms, exch_us, p50, p99], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        train_s, pred_s, step_ms, exch_us = t.tolist()
+        train_s, pred_s, step_ms, exch_us, p50, p99 = t.tolist()
     # ---- roofline of the persistent working-set kernel ---------------------------------------
     peaks, peak_src = measured_peaks()
     n_rows_local = r1 - r0
@@ -379,46 +468,49 @@ def main():
             qa = torch.from_numpy(hq.X[q0:q1]).pin_memory().numpy()
         step(xa, ya, qa)  # warm
         barrier()
-        et, ep = [], []
+        et, ep, ea = [], [], []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            m = train(xa, ya)                 # H2D of X, y inside; model D2H inside
-            torch.cuda.synchronize()
+            m = train(xa, ya)                 # H2D of X, y inside
             t1 = time.perf_counter()
-            predict(m, qa)                    # H2D of Xq, D2H of the labels
-            torch.cuda.synchronize()
+            out = predict(m, qa)              # H2D of Xq, D2H of the labels (host array)
+            t2 = time.perf_counter()
             et.append(t1 - t0)
-            ep.append(time.perf_counter() - t1)
+            ep.append(t2 - t1)
+            ea.append(t2 - t0)
         barrier()
-        nsv = m.info.n_sv
         nb = (lambda a: sum(x.nbytes for x in a)) if csr else (lambda a: a.nbytes)
         nqr = (len(qa[0]) - 1) if csr else qa.shape[0]
-        e2e = {"value": statistics.mean(et), "unit": "s",
+        e = statistics.mean(ea)
+        if world > 1:
+            t = torch.tensor([e], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e = t.item()
+        e2e = {"value": e, "unit": "s",
                "h2d_bytes_per_step": int(nb(xa) + ya.nbytes + nb(qa)),
-               "d2h_bytes_per_step": int(4 * nqr + 16 * nsv),
+               "d2h_bytes_per_step": int(out.nbytes),
+               "includes": "svm_train + svm_predict of the held-out rows from pinned host "
+                           "buffers (wall clock, synchronous API)",
+               "train_s": statistics.mean(et), "predict_s": statistics.mean(ep),
                "predict_rows_per_s": nqr / statistics.mean(ep)}
     # ---- CPU baseline (rank 0, N = 1 only) ---------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         el, k, cores = cpu_baseline(ds, kw, args.cpu_seconds)
-        cpu = {"value": el / k * info.iterations, "unit": "s", "cores": cores, "kind": "oracle",
-               "sample": f"first {k} SMO iterations of {args.config} (full n={n}, d={d}) in "
-                         f"{el:.1f} s, projected to this run's {info.iterations} iterations to tol",
-               "iterations_per_s": k / el}
+        cpu = cpu_record(args.config, el, k, cores)
+    # ---- pass-only diagnostic of the fused a3 step (rank 0, dense single-problem workloads) --
+    if (rank == 0 and world == 1 and not csr and not getattr(info, "batched", 0)
+            and not args.no_pass and roofline.get("bound") == "hbm"):
+        roofline["pass_only"] = pass_only(pkg, X, y, dict(kw), ncopy, n, d, peaks)
     if rank == 0:
         line = {
             "metric": METRIC, "value": train_s, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}",
-                       "n": n, "d": d, "duals": n * ncopy, "heldout_rows": nq,
-                       "C": kw["cost"], "gamma": kw["gamma"], "epsilon": kw["epsilon"],
-                       "tolerance": kw["tolerance"], "working_set": 16,
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
-                       "l2": "flushed (256 MB write) before every timed step"},
+            "config": config_object(args.config, ds, nq, kw, world),
             "iterations": info.iterations, "iterations_per_s": info.iterations / loop_s,
             "train_breakdown_ms": {"setup": info.setup_ms, "loop": info.loop_ms,
                                    "certify": info.certify_ms, "total": info.train_ms,
@@ -432,7 +524,8 @@ def main():
         }
         if not getattr(info, "batched", 0):
             line["exchange"] = {
-                "us_per_iteration": exch_us, "frac_of_loop": exch_us * info.iterations / 1e3 / max(info.loop_ms, 1e-9),
+                "us_per_iteration": exch_us, "p50_us": p50, "p99_us": p99,
+                "frac_of_loop": exch_us * info.iterations / 1e3 / max(info.loop_ms, 1e-9),
                 "measured": "clock64 on CTA 0 (max over ranks): its candidate publish -> every CTA's "
                             "keys staged (transport + wait for the slowest CTA); in-kernel NVLink "
                             "peer-memory exchange, no NCCL call per iteration"}

@@ -114,6 +114,8 @@ typedef struct svm_model_info {
                           /* publish until every CTA's (every rank's, when sharded) keys are    */
                           /* staged -- transport latency plus the wait for the slowest CTA.     */
                           /* 0 for the batched one-vs-rest passes.                               */
+    double exchange_p50_us; /* median and 99th percentile of that per-iteration exchange latency */
+    double exchange_p99_us; /* (histogram of 512-cycle bins, converted at the loop's clock)       */
 } svm_model_info;
 
 /*
@@ -199,14 +201,35 @@ int svm_solver_run(svm_solver* s, int64_t max_iter, svm_solver_stats* stats);
 /* Debug view of the fused pass's kernel rows: K[i * nr + r] = K(x_i, x_rows[r]) for all n
  * training rows i, through the same dot-product and kernel code as the pass (nr <= 16). */
 int svm_solver_kernel_rows(svm_solver* s, const int64_t* rows, int32_t nr, float* K);
+/* Virtual ranks: subsequent svm_solver_run calls split the
+ * solver's nblk CTAs into vranks ranks of nblk / vranks CTAs inside ONE launch on this GPU.  Each
+ * virtual rank owns the rows its CTAs own in a one-rank launch, keeps its own exchange buffer,
+ * merges its CTAs' lists, publishes one 8+8 list per rank, gathers W rows / payloads from their
+ * owner rank -- the code path of a multi-GPU run.  Per-row arithmetic and the merges are exact,
+ * so alpha, G and the iteration count must equal vranks = 1 bit for bit.  vranks = 1 restores
+ * the one-rank launch.  SVM_EINVAL unless 1 <= vranks <= 8 and vranks divides nblk. */
+int svm_solver_set_ranks(svm_solver* s, int32_t vranks);
+/* Launch geometry of the solver: CTAs of the persistent kernel and training rows per CTA. */
+int svm_solver_geometry(const svm_solver* s, int32_t* nblk, int64_t* rows_per_cta);
+/* Pass-only diagnostic of the fused kernel-row + gradient step (a3) in its production launch
+ * configuration: `passes` repetitions of { for every training row i: K(x_i, x_rows[r]) for the
+ * nr <= 16 distinct rows, G_i += y_i sum_r coef[r] K_ir, new candidate keys, CTA top-8 lists },
+ * with W fixed (no exchange, no subproblem).  rows: int64[nr] training-row indices, coef:
+ * fp32[nr] (host or device).  *ms receives the device time of the launch (CUDA events on the
+ * solver's stream).  The solver's G is modified (G += passes x the update): restore it with
+ * svm_solver_set_state before training further.  Single-rank solvers only. */
+int svm_solver_pass_bench(svm_solver* s, const int64_t* rows, int32_t nr, const float* coef,
+                          int64_t passes, double* ms);
 void svm_solver_free(svm_solver* s);
 
 /* ---- row-sharded training over several GPUs (one process per GPU) --------------------------
  * Rank r holds training rows [row0, row0 + n_local) of an n_global-row problem (contiguous
- * blocks).  Every iteration each CTA of every rank writes its 8+8 working-set
- * candidates straight into every rank's receive buffer over NVLink peer memory (a one-shot
- * all-gather fused into the pass); every rank merges identically, so all ranks pick the same W
- * and solve the same subproblem redundantly.  Working-set rows are read from their owner over
+ * blocks).  Every iteration each CTA of a rank publishes its 8+8 working-set
+ * candidates into its rank's own buffer; every CTA merges the rank's lists; CTA 0 of every rank
+ * then writes the rank's merged 8+8 list straight into every rank's buffer over NVLink peer
+ * memory (a one-shot all-gather of one list per rank, fused into the pass); every CTA merges the
+ * `world` lists identically, so all ranks pick the same W and solve the same subproblem
+ * redundantly.  Working-set rows are read from their owner over
  * NVLink.  Setup is two-phase because peer mappings need an exchange of opaque handles between
  * processes, which the caller performs (e.g. torch.distributed all_gather_object):
  *   svm_shard_create   allocates this rank's state and its exported buffers;

@@ -54,7 +54,8 @@ class svm_model_info(ctypes.Structure):
                 ("train_ms", ctypes.c_double), ("loop_ms", ctypes.c_double),
                 ("setup_ms", ctypes.c_double), ("certify_ms", ctypes.c_double),
                 ("passes", ctypes.c_int64), ("pass_ms", ctypes.c_double),
-                ("batched", ctypes.c_int32), ("exchange_ms", ctypes.c_double)]
+                ("batched", ctypes.c_int32), ("exchange_ms", ctypes.c_double),
+                ("exchange_p50_us", ctypes.c_double), ("exchange_p99_us", ctypes.c_double)]
 
 
 class svm_solver_stats(ctypes.Structure):
@@ -90,6 +91,9 @@ SIGNATURES = {
     "svm_solver_get_state": (ctypes.c_int, [_P, _P, _P]),
     "svm_solver_run": (ctypes.c_int, [_P, _i64, ctypes.POINTER(svm_solver_stats)]),
     "svm_solver_kernel_rows": (ctypes.c_int, [_P, _P, _i32, _P]),
+    "svm_solver_set_ranks": (ctypes.c_int, [_P, _i32]),
+    "svm_solver_geometry": (ctypes.c_int, [_P, ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
+    "svm_solver_pass_bench": (ctypes.c_int, [_P, _P, _i32, _P, _i64, ctypes.POINTER(ctypes.c_double)]),
     "svm_solver_free": (None, [_P]),
     "svm_shard_create": (ctypes.c_int, [_P, _i64, _i64, _i64, _P, _i64, _i32, _i32,
                                         ctypes.POINTER(svm_params), ctypes.POINTER(_P)]),
@@ -297,6 +301,25 @@ class Solver:
         st = svm_solver_stats()
         _check(lib().svm_solver_run(self._h, int(max_iter), ctypes.byref(st)))
         return st
+
+    def set_ranks(self, vranks: int):
+        """svm_solver_set_ranks: run the next svm_solver_run calls as `vranks` virtual ranks."""
+        _check(lib().svm_solver_set_ranks(self._h, int(vranks)))
+
+    def geometry(self):
+        """(nblk, rows_per_cta) of the persistent launch (svm_solver_geometry)."""
+        nb, rpc = ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().svm_solver_geometry(self._h, ctypes.byref(nb), ctypes.byref(rpc)))
+        return int(nb.value), int(rpc.value)
+
+    def pass_bench(self, rows, coef, passes: int) -> float:
+        """svm_solver_pass_bench: device ms of `passes` fused a3 passes with W fixed."""
+        r = np.ascontiguousarray(rows, np.int64)
+        c = np.ascontiguousarray(coef, np.float32)
+        ms = ctypes.c_double()
+        _check(lib().svm_solver_pass_bench(self._h, r.ctypes.data_as(_P), len(r),
+                                           c.ctypes.data_as(_P), int(passes), ctypes.byref(ms)))
+        return float(ms.value)
 
     def kernel_rows(self, rows):
         rows = np.ascontiguousarray(rows, np.int64)

@@ -14,11 +14,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
 // ================================================================ launch counter
 #include <atomic>
+#include <mutex>
 static std::atomic<long long> g_launches{0};
 void svm_note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 extern "C" int64_t svm_launch_count(void) { return (int64_t)g_launches.load(); }
@@ -57,23 +59,36 @@ static int fail(int code, const char* fmt, ...)
 // Device buffers come from the stream-ordered pool (cudaMallocAsync on the legacy stream): no
 // device-wide synchronisation on free, and repeated trainings reuse pooled memory.  Every entry
 // point synchronises its stream before returning, so pool reuse never races user work.
-// The library's device buffers come from the device's default stream-ordered pool.  Its release
-// threshold is raised once so that memory freed by one training is kept for the next: with the
-// default threshold (0) every synchronize returned it to the OS and the next training re-mapped
-// it, which made single trainings 10-30% slower at random (c2: +40 ms, c4: +1.2 s measured).
-static void keep_pool_memory()
+// The library's device buffers come from a PRIVATE stream-ordered pool per device (the default
+// pool and the caller's allocators are left alone).  Its release threshold keeps up to
+// min(8 GiB, 1/16 of the device) of freed memory cached for the next training: with threshold 0
+// every synchronize returned it to the OS and the next training re-mapped it, which made single
+// trainings 10-30% slower at random (c2: +40 ms, c4: +1.2 s measured); beyond the bound, freed
+// memory goes back to the device at the next synchronize, so a host framework sharing the GPU
+// never loses more than the bound to this library.
+cudaMemPool_t svm_mem_pool()
 {
-    static int done_dev = -1;
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return; }
-    if (done_dev == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) { cudaGetLastError(); return nullptr; }
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps pp = {};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &pp) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        uint64_t thr = std::min<uint64_t>(8ull << 30, (uint64_t)tot / 16);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        cudaGetLastError();
+        pools[dev] = pool;
     }
-    cudaGetLastError();
-    done_dev = dev;
+    return pools[dev];
 }
 
 struct DBuf {
@@ -115,8 +130,8 @@ struct DBuf {
     {
         release();
         if (b == 0) b = 16;
-        keep_pool_memory();
-        cudaError_t e = cudaMallocAsync(&p, b, 0);
+        cudaMemPool_t pool = svm_mem_pool();
+        cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, b, pool, 0) : cudaMallocAsync(&p, b, 0);
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
@@ -161,20 +176,6 @@ static int to_host(std::vector<T>& dst, const T* src, int64_t n, cudaStream_t st
         CK(cudaStreamSynchronize(st));
     }
     return SVM_OK;
-}
-
-static void pool_setup()
-{
-    static bool done = false;
-    if (done) return;
-    done = true;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
 }
 
 static int sm_count()
@@ -260,7 +261,6 @@ struct Data {
 
 static int pick_nblk(int64_t n)
 {
-    pool_setup();
     const char* env = getenv("SVMB200_NBLK");
     int sms = sm_count();
     if (env && atoi(env) > 0) return std::min(atoi(env), sms);
@@ -370,14 +370,19 @@ static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, con
 
 // ================================================================ one binary problem (Eq. 2)
 struct Exchange {
-    int L = 0;
-    DBuf xw, info;               // candidate words [2][L][XW_PER_SLOT] (self-tagged), loop info
+    int L = 0, nbuf = 0;         // CTA lists per rank; buffers (1, or the virtual ranks of a launch)
+    DBuf xw, info;               // per buffer: rank level [2][SVM_MAX_RANKS][XW_RANK_SLOT] then the
+                                 // local level [2][L][XW_PER_SLOT] (self-tagged words); loop info
     uint32_t epoch = 0;
-    int alloc(int L_)
+    static int64_t words(int L_) { return XW_RANK_WORDS + 2 * (int64_t)L_ * XW_PER_SLOT; }
+    uint64_t* buf(int r) const { return xw.as<uint64_t>() + r * words(L); }
+    int alloc(int L_, int nbuf_ = 1)
     {
         L = L_;
-        TRY(xw.alloc(sizeof(uint64_t) * 2 * L * XW_PER_SLOT));
-        TRY(info.alloc(sizeof(SmoInfo)));
+        nbuf = nbuf_;
+        xw.release();
+        TRY(xw.alloc(sizeof(uint64_t) * words(L) * nbuf));
+        if (!info.p) TRY(info.alloc(sizeof(SmoInfo)));
         CK(cudaMemset(xw.p, 0, xw.bytes));
         return SVM_OK;
     }
@@ -396,6 +401,9 @@ struct Problem {
     double tol_loop = 0;   // the loop's stop threshold: tol, lowered after a failed certification (R16)
     double loop_ms = 0, cert_ms = 0;
     double exch_ms = 0;    // share of loop_ms CTA 0 spent in the candidate exchange
+    double exch_hist[SMO_EXCH_BINS] = {};   // per-iteration exchange latency histogram (us units
+                                            // after scaling: see exch_percentile)
+    double us_per_cycle = 0;                // loop_ms / loop_cycles of the last launch
     int64_t passes = 0;    // X passes of the dominant pass kernel (batched one-vs-rest: k_ovr_pass)
     double pass_ms = 0;    // their device time (CUDA event pairs around each launch)
     SmoInfo last_info;
@@ -469,7 +477,9 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.kp = P.kp;
     a.rank = 0;
     a.world = 1;
+    a.virt = 0;
     a.nblk = D.nblk;
+    for (int r = 0; r < SVM_MAX_RANKS; ++r) a.rank_nblk[r] = D.nblk;   // equal on every rank
     a.rank_row0[0] = 0;
     a.rank_row0[1] = D.n;
     a.peer_XR[0] = D.XR;
@@ -478,7 +488,7 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.peer_indices[0] = D.indices;
     a.peer_vals[0] = D.vals;
     a.rank_rpc[0] = D.rows_per_cta;
-    a.peer_xw[0] = E.xw.as<uint64_t>();
+    a.peer_xw[0] = E.buf(0);
     a.timeout_ns = 30ull * 1000000000ull;
     a.overlap = 2;   // measured: c2 -5%, c4 -2% per iteration vs 1 (all warps in phase A)
     if (const char* e = getenv("SVMB200_OVERLAP")) a.overlap = atoi(e);
@@ -503,17 +513,68 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     return a;
 }
 
+// Launch variants of the persistent loop beyond plain training (tests and diagnostics).
+struct LoopMode {
+    int vranks = 1;                     // > 1: that many virtual ranks inside one launch
+    const int64_t* pass_rows = nullptr; // pass-only diagnostic: fixed W rows (device) ...
+    const float* pass_c = nullptr;      // ... and coefficients (device); max_iter = passes
+    int pass_nr = 0;
+    double* pass_ms = nullptr;          // out: device time of the pass-only launch
+};
+
+// Virtual ranks (LoopMode::vranks = P): the launch's D.nblk CTAs form P ranks of D.nblk / P CTAs;
+// rank r owns rows [r nblk_r R, (r + 1) nblk_r R) (clipped to n) -- the same rows its CTAs own in a
+// one-rank launch, so alpha, G and the iteration count must be bit-identical to it.  Each virtual
+// rank has its own exchange buffer; W rows, norms and payloads are gathered from their owner.
+static int set_virtual_ranks(SmoArgs& a, const Data& D, Exchange& E, int P)
+{
+    if (P < 2 || P > SVM_MAX_RANKS || D.nblk % P != 0)
+        return fail(SVM_EINVAL, "virtual ranks: %d must be in [2, %d] and divide the %d CTAs", P,
+                    SVM_MAX_RANKS, D.nblk);
+    const int nb = D.nblk / P;
+    if (E.L != nb || E.nbuf != P) TRY(E.alloc(nb, P));
+    a.virt = 1;
+    a.world = P;
+    a.nblk = nb;
+    a.rank = 0;
+    a.row0 = 0;
+    a.n_global = D.n;
+    for (int r = 0; r <= P; ++r) a.rank_row0[r] = std::min<int64_t>(D.n, (int64_t)r * nb * D.rows_per_cta);
+    for (int r = 0; r < P; ++r) {
+        const int64_t o = a.rank_row0[r];
+        a.rank_nblk[r] = nb;
+        a.rank_rpc[r] = D.rows_per_cta;
+        a.peer_XR[r] = D.csr ? nullptr : D.XR + o * D.d;
+        a.peer_xnorm[r] = D.norms.as<float>() + o;
+        a.peer_indptr[r] = D.csr ? D.indptr + o : nullptr;
+        a.peer_indices[r] = D.indices;
+        a.peer_vals[r] = D.vals;
+        a.peer_xw[r] = E.buf(r);
+    }
+    return SVM_OK;
+}
+
 // Run up to max_iter iterations of the persistent loop; accumulates into P.
 static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cudaStream_t st,
-                    SmoInfo* info_out, const ShardCtx* sc = nullptr)
+                    SmoInfo* info_out, const ShardCtx* sc = nullptr, const LoopMode* mode = nullptr)
 {
+    const LoopMode M0;
+    const LoopMode& M = mode ? *mode : M0;
+    if (M.vranks <= 1 && !sc && (E.L != D.nblk || E.nbuf != 1)) TRY(E.alloc(D.nblk));
     SmoArgs a = make_args(D, P, E, sc);
+    if (M.vranks > 1) TRY(set_virtual_ranks(a, D, E, M.vranks));
+    if (M.pass_rows) {
+        a.pass_only = 1;
+        a.pass_rows = M.pass_rows;
+        a.pass_c = M.pass_c;
+        a.pass_nr = M.pass_nr;
+    }
     a.tag0 = E.epoch;
     a.max_iter = max_iter;
     CK(cudaMemsetAsync(E.info.p, 0, sizeof(SmoInfo), st));
     const int64_t pos_elems = D.rows_per_cta * P.ncopy;
     const int64_t smem_cap = 200 * 1024;
-    int smem = smo_smem_bytes(D.d, a.world, D.nblk, D.csr ? 0 : D.rows_per_cta);
+    int smem = smo_smem_bytes(D.d, a.world, a.nblk, D.csr ? 0 : D.rows_per_cta);
     if (!D.csr && smem <= smem_cap && !getenv("SVMB200_NO_XSMEM")) {
         a.x_in_smem = 1;  // this CTA's X slice stays resident in shared memory
     } else {
@@ -522,7 +583,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         if (!D.csr && D.d >= 256 && !getenv("SVMB200_RPT")) a.rpt = 1;
         a.x_ring = (!D.csr && (a.rpt >= 2 || D.d >= 256)) ? 1 : 0;
         if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
-        smem = smo_smem_bytes(D.d, a.world, D.nblk, 0) +
+        smem = smo_smem_bytes(D.d, a.world, a.nblk, 0) +
                (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
     }
@@ -531,7 +592,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         // wide streamed rows: CTA-wide bulk-copy pipeline (8 stages of wide_kc features x Rs
         // rows, Rs = 8 mod 32) feeding one-row-per-lane dot products held in registers
         const int64_t ncw = (D.rows_per_cta + 31) / 32, Rs = ncw * 32 + 8;
-        const int base = smo_smem_bytes(D.d, a.world, D.nblk, 0);
+        const int base = smo_smem_bytes(D.d, a.world, a.nblk, 0);
         int64_t kc = std::min<int64_t>(16, (210 * 1024 - base) / (8 * 4 * Rs));
         if (kc < 4) kc = 0;
         if (kc > 0) {
@@ -542,8 +603,8 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         }
     }
     if (smem > 220 * 1024)
-        return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d lists)", smem,
-                    (long long)D.d, a.world * D.nblk);
+        return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d + %d lists)",
+                    smem, (long long)D.d, a.nblk, a.world);
     {   // buffer the dot products of as many rows as fit (64 B per row), whole chunks only
         const int64_t chunk = 32 * a.rpt;
         const int64_t all_rows = (D.rows_per_cta + chunk - 1) / chunk * chunk;
@@ -574,6 +635,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     CK(cudaEventRecord(e0, st));
     cudaError_t le = launch_smo(a, smem, st);
     if (le != cudaSuccess) {
+        smo_l2_restore();
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         return fail(SVM_ECUDA, "persistent working-set kernel launch failed: %s (smem %d B, %d CTAs)",
@@ -583,16 +645,18 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     SmoInfo info;
     CK(cudaMemcpyAsync(&info, E.info.p, sizeof info, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (!a.x_in_smem) {   // X^T's persisting L2 lines (launch_smo's access-policy window) -> normal
-        cudaCtxResetPersistingL2Cache();
-        cudaGetLastError();
-    }
+    smo_l2_restore();   // launch_smo's persisting-L2 set-aside -> the caller's limit
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (info.error) return fail(SVM_ETIMEOUT, "working-set exchange timed out (a rank stopped)");
     E.epoch += (uint32_t)info.iterations + 1;
+    if (a.pass_only) {   // a diagnostic: the solver's iteration bookkeeping is not advanced
+        if (M.pass_ms) *M.pass_ms = ms;
+        if (info_out) *info_out = info;
+        return SVM_OK;
+    }
     P.iterations += info.iterations;
     P.m_up = info.m_up;
     P.M_low = info.M_low;
@@ -600,6 +664,10 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     P.loop_ms += ms;
     if (info.loop_cycles > 0) P.exch_ms += ms * (double)info.exch_cycles / (double)info.loop_cycles;
     P.last_info = info;
+    if (info.loop_cycles > 0) {
+        P.us_per_cycle = ms * 1e3 / (double)info.loop_cycles;
+        for (int b = 0; b < SMO_EXCH_BINS; ++b) P.exch_hist[b] += (double)info.exch_hist[b];
+    }
     if (getenv("SVMB200_PROFILE")) {
         int clk = 0, dev = 0;
         cudaGetDevice(&dev);
@@ -629,6 +697,20 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     }
     if (info_out) *info_out = info;
     return SVM_OK;
+}
+
+// q-quantile (cycles, bin midpoint) of an exchange-latency histogram; 0 when empty.
+static double exch_percentile(const double* h, double q)
+{
+    double tot = 0;
+    for (int b = 0; b < SMO_EXCH_BINS; ++b) tot += h[b];
+    if (tot <= 0) return 0.0;
+    double acc = 0;
+    for (int b = 0; b < SMO_EXCH_BINS; ++b) {
+        acc += h[b];
+        if (acc >= q * tot) return exch_bin_mid(b);
+    }
+    return exch_bin_mid(SMO_EXCH_BINS - 1);
 }
 
 // Per-row coefficients of problem P (device, fp64[n]) and the SV flags they imply.
@@ -815,10 +897,14 @@ static double resume_factor()
 }
 
 // Certification (a4, reading R16) and resumption of the persistent loop after a loop stopped.
+// Every loop that stops converged is followed by a certification, including the last resumed
+// one: the reported state is always the re-measured one (converged = 0 if the last check failed
+// after SVM_MAX_RESUMES resumptions).
+#define SVM_MAX_RESUMES 4
 static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
                           cudaStream_t st)
 {
-    for (int round = 0; round < 4; ++round) {
+    for (int round = 0;; ++round) {
         if (!P.converged || prm->certify == 0) break;
         if (prm->certify < 0) {  // auto: only when one pass over n x n_SV is affordable
             DBuf coef, flag, idx;
@@ -833,7 +919,9 @@ static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_para
         TRY(certify(D, P, &viol, st));
         if (viol <= P.tol) { P.converged = true; break; }
         P.converged = false;
-        // fp32 G stopped just inside tol: resume below it by 4x the measured excess (>= 1% of tol)
+        if (round == SVM_MAX_RESUMES) break;
+        // fp32 G stopped just inside tol: resume below it by resume_factor() times the measured
+        // excess, and at least 1% of tol below the previous stop
         P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - resume_factor() * (viol - P.tol));
         int64_t left = P.max_iter - P.iterations;
         if (left <= 0) break;
@@ -1132,6 +1220,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     std::vector<Problem> probs(ys.size());
     std::vector<double> bs(ys.size());
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, pass_ms = 0, exch_ms = 0;
+    double xh[SMO_EXCH_BINS] = {}, upc = 0;
     int64_t iters = 0, passes = 0;
     bool conv = true, cert = true;
     for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
@@ -1153,6 +1242,8 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
         exch_ms += P.exch_ms;
+        for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
+        if (P.us_per_cycle > 0) upc = P.us_per_cycle;
         cert_ms += P.cert_ms;
         if (!batched) { passes += P.iterations; pass_ms += P.loop_ms; }
     }
@@ -1190,6 +1281,8 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     I.dual_objective = dual;
     I.loop_ms = loop_ms;
     I.exchange_ms = exch_ms;
+    I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
+    I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
     I.certify_ms = cert_ms;
     I.setup_ms = t_setup;
     I.passes = passes;
@@ -1364,6 +1457,7 @@ struct svm_solver {
     Exchange E;
     svm_params prm;
     cudaStream_t st = nullptr;
+    int vranks = 1;   // svm_solver_set_ranks
 };
 
 static int solver_create_common(svm_solver* S, const float* y, const svm_params* params)
@@ -1470,7 +1564,9 @@ extern "C" int svm_solver_run(svm_solver* s, int64_t max_iter, svm_solver_stats*
     s->P.loop_ms = 0;
     int64_t before = s->P.iterations;
     SmoInfo info;
-    TRY(run_loop(s->D, s->P, s->E, max_iter, s->st, &info));
+    LoopMode mode;
+    mode.vranks = s->vranks;
+    TRY(run_loop(s->D, s->P, s->E, max_iter, s->st, &info, nullptr, &mode));
     if (stats) {
         memset(stats, 0, sizeof *stats);
         stats->iterations = s->P.iterations - before;
@@ -1505,6 +1601,51 @@ extern "C" int svm_solver_kernel_rows(svm_solver* s, const int64_t* rows, int32_
                        is_device_ptr(K) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
     return SVM_OK;
+}
+
+extern "C" int svm_solver_set_ranks(svm_solver* s, int32_t vranks)
+{
+    if (!s) return fail(SVM_EINVAL, "NULL solver");
+    if (vranks < 1 || vranks > SVM_MAX_RANKS || (vranks > 1 && s->D.nblk % vranks != 0))
+        return fail(SVM_EINVAL, "vranks = %d must be in [1, %d] and divide the %d CTAs", vranks,
+                    SVM_MAX_RANKS, s->D.nblk);
+    s->vranks = vranks;
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_geometry(const svm_solver* s, int32_t* nblk, int64_t* rows_per_cta)
+{
+    if (!s) return fail(SVM_EINVAL, "NULL solver");
+    if (nblk) *nblk = s->D.nblk;
+    if (rows_per_cta) *rows_per_cta = s->D.rows_per_cta;
+    return SVM_OK;
+}
+
+extern "C" int svm_solver_pass_bench(svm_solver* s, const int64_t* rows, int32_t nr,
+                                     const float* coef, int64_t passes, double* ms)
+{
+    if (!s || !rows || !coef || !ms) return fail(SVM_EINVAL, "NULL argument");
+    if (nr < 1 || nr > SVM_WS) return fail(SVM_EINVAL, "nr must be in [1, 16]");
+    if (passes < 1) return fail(SVM_EINVAL, "passes must be >= 1");
+    std::vector<int64_t> rh;
+    std::vector<float> ch;
+    TRY(to_host(rh, rows, nr, s->st));
+    TRY(to_host(ch, coef, nr, s->st));
+    for (int i = 0; i < nr; ++i) {
+        if (rh[i] < 0 || rh[i] >= s->D.n) return fail(SVM_EINVAL, "row index out of range");
+        for (int j = 0; j < i; ++j)
+            if (rh[j] == rh[i]) return fail(SVM_EINVAL, "rows must be distinct");
+    }
+    DBuf drows, dc;
+    TRY(to_device(drows, rh.data(), nr, s->st));
+    TRY(to_device(dc, ch.data(), nr, s->st));
+    LoopMode mode;
+    mode.pass_rows = drows.as<int64_t>();
+    mode.pass_c = dc.as<float>();
+    mode.pass_nr = nr;
+    mode.pass_ms = ms;
+    SmoInfo info;
+    return run_loop(s->D, s->P, s->E, passes, s->st, &info, nullptr, &mode);
 }
 
 extern "C" void svm_solver_free(svm_solver* s) { delete s; }
@@ -1579,8 +1720,7 @@ static int shard_create_common(svm_shard* S, const float* y_global, const svm_pa
     S->ys.resize(ys.size());
     for (size_t p = 0; p < ys.size(); ++p)
         S->ys[p].assign(ys[p].begin() + S->row0, ys[p].begin() + S->row0 + S->D.n);
-    const int L = S->world * S->D.nblk;
-    TRY(S->E.alloc(L));
+    TRY(S->E.alloc(S->D.nblk));   // local level: this rank's CTAs; rank level: <= SVM_MAX_RANKS
     TRY(S->xbuf.alloc(sizeof(double) * 2 * S->world * XCH_K));
     TRY(S->xflags.alloc(sizeof(uint32_t) * S->world));
     CK(cudaMemset(S->xflags.p, 0, S->xflags.bytes));
@@ -1862,6 +2002,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     std::vector<Problem> probs(S->nprob);
     std::vector<double> bs(S->nprob);
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, exch_ms = 0;
+    double xh[SMO_EXCH_BINS] = {}, upc = 0;
     int64_t iters = 0;
     bool conv = true, cert = true;
     for (int p = 0; p < S->nprob; ++p) {
@@ -1891,6 +2032,8 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
         exch_ms += P.exch_ms;
+        for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
+        if (P.us_per_cycle > 0) upc = P.us_per_cycle;
         cert_ms += P.cert_ms;
     }
     // model: union of SVs over problems, coefficients of every problem, rows gathered
@@ -1954,6 +2097,8 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     I.dual_objective = dual;
     I.loop_ms = loop_ms;
     I.exchange_ms = exch_ms;
+    I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
+    I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
     I.certify_ms = cert_ms;
     I.passes = iters;
     I.pass_ms = loop_ms;

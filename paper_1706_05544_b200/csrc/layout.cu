@@ -65,12 +65,13 @@ __global__ void k_colmajor_to_XT(const float* __restrict__ X, int64_t n, int64_t
     }
 }
 
-// X^T [d][n_pad] -> row-major X [n][d] (used when the input was column-major)
+// X^T [d][n_pad] -> row-major X [n][d] (used when the input was column-major).  Row tiles on
+// grid.x (2^31 - 1 blocks), feature tiles on grid.y (d <= 2,097,120 features).
 __global__ void k_XT_to_rowmajor(const float* __restrict__ XT, int64_t n, int64_t d, int64_t n_pad,
                                  float* __restrict__ X)
 {
     __shared__ float tile[32][33];
-    int64_t k0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+    int64_t k0 = (int64_t)blockIdx.y * 32, i0 = (int64_t)blockIdx.x * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         int64_t k = k0 + r, i = i0 + threadIdx.x;
         tile[r][threadIdx.x] = (k < d && i < n) ? XT[k * n_pad + i] : 0.0f;
@@ -423,7 +424,7 @@ cudaError_t lay_colmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, 
 cudaError_t lay_XT_to_rowmajor(const float* XT, int64_t n, int64_t d, int64_t n_pad, float* X,
                                cudaStream_t st)
 {
-    dim3 grid(nblocks(d, 32), nblocks(n, 32));
+    dim3 grid(nblocks(n, 32), nblocks(d, 32));
     svm_note_launches(1);
     k_XT_to_rowmajor<<<grid, dim3(32, 8), 0, st>>>(XT, n, d, n_pad, X);
     return cudaGetLastError();

@@ -924,8 +924,6 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
                                      const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad, int64_t d,
                                      const double* coef, int n_out, const KParams& kp, double* F, cudaStream_t st,
                                      bool any_d);
-static double* g_fpart = nullptr;
-static size_t g_fpart_bytes = 0;
 
 cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int64_t nq_pad,
                           const float* SVT, const float* svnorm, int64_t nsv, int64_t nsv_pad,
@@ -949,17 +947,17 @@ cudaError_t pred_decision(const float* XqT, const float* qnorm, int64_t nq, int6
     splits = (int)((s_tiles + tps - 1) / tps);
     size_t need = sizeof(double) * (size_t)splits * nq * n_out;
     double* part = F;
+    double* fpart = nullptr;   // per-call scratch on the caller's stream (private pool)
     if (splits > 1) {
-        if (need > g_fpart_bytes) {
-            if (g_fpart) cudaFreeAsync(g_fpart, st);
-            g_fpart = nullptr;
-            g_fpart_bytes = 0;
-            cudaError_t e = cudaMallocAsync(&g_fpart, need, st);
-            if (e != cudaSuccess) return e;
-            g_fpart_bytes = need;
-        }
-        part = g_fpart;
+        cudaError_t e = svm_scratch_alloc(reinterpret_cast<void**>(&fpart), need, st);
+        if (e != cudaSuccess) return e;
+        part = fpart;
     }
+    struct StreamFree {   // the partials go back to the pool after the reduction, on `st`
+        void* p;
+        cudaStream_t st;
+        ~StreamFree() { if (p) cudaFreeAsync(p, st); }
+    } free_part{fpart, st};
     dim3 grid((unsigned)q_tiles, (unsigned)splits);
     if (tc && SVtc) {   // pipelined variant (pre-laid-out SV tiles), when its shared memory fits
         const int dp = (int)pred_tc_dp(d);
@@ -1037,13 +1035,7 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
     // d <= 128: the resident-query 3xTF32 kernel (k_decision_tcp) unless SVMB200_F16_ALL is set
     if ((d <= 128 && !any_d && !getenv("SVMB200_F16_ALL")) || n_out > 16 || getenv("SVMB200_NO_TC") || getenv("SVMB200_NO_F16"))
         return cudaErrorNotSupported;
-    static int nsm = 0;
-    if (nsm == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-    }
+    const int nsm = svm_device_sms();
     const int nkc = (int)((d + DF_KCH - 1) / DF_KCH);
     const int nqt = (int)((nq + 127) / 128);
     const int nsb = (int)((std::max<int64_t>(nsv, 1) + DF_SVB - 1) / DF_SVB);   // blocks of the real SVs
@@ -1066,24 +1058,12 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
     const size_t qh_b = (size_t)nqt * nkc * DF_ATILE * 2, sh_b = (size_t)nsb * nkc * DF_BTILE * 2;
     const size_t cf_b = (size_t)n_out * nsv_ld * 4, sn_b = (size_t)nsv_ld * 4;
     const size_t part_b = (size_t)nsplit * 4 * nq * n_out * 8;
-    // grow-only scratch (a stream-ordered allocation per call would return the memory to the OS at
-    // every synchronize: ~10 ms per call for the c3 certification's 200 MB)
-    static char* g_buf = nullptr;
-    static size_t g_buf_bytes = 0;
+    // per-call scratch on the caller's stream from the library's private pool (its release
+    // threshold keeps the memory mapped between calls: no OS round trip per certification)
     const size_t total = qh_b + sh_b + cf_b + sn_b + part_b + 256;
-    cudaError_t e = cudaSuccess;
-    if (total > g_buf_bytes) {
-        if (g_buf) {
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-            cudaFree(g_buf);
-            g_buf = nullptr;
-            g_buf_bytes = 0;
-        }
-        const size_t want = total + total / 4;
-        if ((e = cudaMalloc(reinterpret_cast<void**>(&g_buf), want)) != cudaSuccess) return e;
-        g_buf_bytes = want;
-    }
-    char* buf = g_buf;
+    char* buf = nullptr;
+    cudaError_t e = svm_scratch_alloc(reinterpret_cast<void**>(&buf), total, st);
+    if (e != cudaSuccess) return e;
     uint16_t* QH = reinterpret_cast<uint16_t*>(buf);
     uint16_t* SH = reinterpret_cast<uint16_t*>(buf + qh_b);
     float* cf = reinterpret_cast<float*>(buf + qh_b + sh_b);
@@ -1139,6 +1119,7 @@ static cudaError_t pred_decision_f16(const float* XqT, const float* qnorm, int64
         e = cudaGetLastError();
     }
 out:
+    cudaFreeAsync(buf, st);
     return e;
 }
 

@@ -341,16 +341,56 @@ struct SmoShared {
     int32_t w_y[SVM_WS];
     float c[SVM_WS];                     // c_r = sum_{a: row r} y_a dalpha_a
     float xn[SVM_WS];                    // |x_r|^2 of the distinct rows
+    uint64_t rk_key[2][SVM_MAX_RANKS * 8];   // rank level: [side][rank * 8 + position]
+    int32_t rk_src[2][SVM_MAX_RANKS * 8];
     int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
     alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode pipeline barriers
     double m_up, M_low;
 };
 
+// The rows one CTA's rank owns, as seen by that CTA.  A real rank (one GPU) sees its own arrays;
+// a virtual rank (SmoArgs::virt, all ranks in one launch) sees its row range of the full arrays
+// through offset pointers (the copy stride n_pad stays the full one).
+struct RankView {
+    const float* XT;
+    const int64_t* indptr;
+    const float* xnorm;
+    double* alpha;
+    float* G;
+    uint8_t* status;
+    int64_t n_local, row0;
+    int rank, cta, nblk;
+};
+__device__ __forceinline__ RankView rank_view(const SmoArgs& a)
+{
+    RankView v;
+    if (a.virt) {
+        v.rank = (int)blockIdx.x / a.nblk;
+        v.cta = (int)blockIdx.x - v.rank * a.nblk;
+        v.row0 = a.rank_row0[v.rank];
+        v.n_local = a.rank_row0[v.rank + 1] - v.row0;
+    } else {
+        v.rank = a.rank;
+        v.cta = (int)blockIdx.x;
+        v.row0 = a.row0;
+        v.n_local = a.n_local;
+    }
+    v.nblk = a.nblk;
+    const int64_t off = a.virt ? v.row0 : 0;
+    v.XT = a.XT ? a.XT + off : nullptr;
+    v.indptr = a.indptr ? a.indptr + off : nullptr;
+    v.xnorm = a.xnorm + off;
+    v.alpha = a.alpha + off;
+    v.G = a.G + off;
+    v.status = a.status + off;
+    return v;
+}
+
 // Per-row epilogue shared by the scan (do_update = false) and the pass: kernel values from the
 // dot products, G update, and each dual's 64-bit up / low candidate keys (score << 32 | ~index;
 // 0 = not a candidate) kept in registers: ku[2 j + c], kl[2 j + c] for row j, copy c.
 template <int RPT, bool RBFK>
-__device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& sh, int64_t li0,
+__device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v, const SmoShared& sh, int64_t li0,
                                              int64_t cta_end, bool do_update,
                                              const float (&acc)[RPT][SVM_WS],
                                              uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT])
@@ -371,13 +411,13 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
             g4[c] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (c < a.ncopy) {
                 const int64_t idx = (int64_t)c * a.n_pad + li0;
-                st4[c] = *reinterpret_cast<const uint32_t*>(a.status + idx);
-                g4[c] = *reinterpret_cast<const float4*>(a.G + idx);
+                st4[c] = *reinterpret_cast<const uint32_t*>(v.status + idx);
+                g4[c] = *reinterpret_cast<const float4*>(v.G + idx);
             }
         }
         float S[4] = {0.f, 0.f, 0.f, 0.f};
         if (do_update) {
-            const float4 xn4 = __ldg(reinterpret_cast<const float4*>(a.xnorm + li0));
+            const float4 xn4 = __ldg(reinterpret_cast<const float4*>(v.xnorm + li0));
             const float xn[4] = {xn4.x, xn4.y, xn4.z, xn4.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -406,7 +446,7 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
                 const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
                 if (do_update) g[j] = fmaf(yv, S[j], g[j]);
                 const float sc = -yv * g[j];
-                const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(a.row0 + li0 + j);
+                const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(v.row0 + li0 + j);
                 const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)gi);
                 const bool in = li0 + j < cta_end;
                 if (in && st_in_up(st)) ku[2 * j + c] = ((uint64_t)ord_f32(sc) << 32) | lo;
@@ -415,11 +455,11 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
             if (do_update) {
                 const int64_t idx = (int64_t)c * a.n_pad + li0;
                 if (full) {
-                    *reinterpret_cast<float4*>(a.G + idx) = make_float4(g[0], g[1], g[2], g[3]);
+                    *reinterpret_cast<float4*>(v.G + idx) = make_float4(g[0], g[1], g[2], g[3]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if (li0 + j < cta_end) a.G[idx + j] = g[j];
+                        if (li0 + j < cta_end) v.G[idx + j] = g[j];
                 }
             }
         }
@@ -431,15 +471,15 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
         const int64_t li = li0 + j;
-        xnv[j] = (do_update && li < cta_end) ? __ldg(a.xnorm + li) : 0.0f;
+        xnv[j] = (do_update && li < cta_end) ? __ldg(v.xnorm + li) : 0.0f;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             stv[j][c] = 0u;
             gv[j][c] = 0.0f;
             if (li < cta_end && c < a.ncopy) {
                 const int64_t idx = (int64_t)c * a.n_pad + li;
-                stv[j][c] = a.status[idx];
-                gv[j][c] = a.G[idx];
+                stv[j][c] = v.status[idx];
+                gv[j][c] = v.G[idx];
             }
         }
     }
@@ -473,10 +513,10 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const SmoShared& 
             float g = gv[j][c];
             if (do_update) {
                 g = fmaf(yv, S, g);
-                a.G[idx] = g;
+                v.G[idx] = g;
             }
             const float sc = -yv * g;
-            const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(a.row0 + li);
+            const uint64_t gi = (uint64_t)c * (uint64_t)a.n_global + (uint64_t)(v.row0 + li);
             const uint64_t lo = (uint64_t)(0xffffffffu - (uint32_t)gi);
             if (st_in_up(st)) ku[2 * j + c] = ((uint64_t)ord_f32(sc) << 32) | lo;
             if (st_in_low(st)) kl[2 * j + c] = ((uint64_t)ord_f32(-sc) << 32) | lo;
@@ -601,48 +641,6 @@ __device__ __forceinline__ void cta_merge(const uint64_t (*lists)[8], uint64_t* 
     }
 }
 
-// Global merge of L sorted 8-lists (staged in shared memory as keys[L][8]) into the top-8 (one
-// warp).  Lane l owns lists l, l + 32, ... (at most MAXK); current and next keys live in
-// registers.  src receives list * 8 + position of each winner.
-template <int MAXK>
-__device__ __forceinline__ void global_merge(const uint64_t* keys, int L, uint64_t* out,
-                                             int32_t* src, int lane)
-{
-    uint64_t cur[MAXK], nxt[MAXK];
-    int hd[MAXK];
-#pragma unroll
-    for (int k = 0; k < MAXK; ++k) {
-        int l = lane + 32 * k;
-        cur[k] = l < L ? lds_u64(keys + l * 8) : 0;
-        nxt[k] = l < L ? lds_u64(keys + l * 8 + 1) : 0;
-        hd[k] = 0;
-    }
-#pragma unroll 1
-    for (int r = 0; r < 8; ++r) {
-        uint64_t lb = cur[0];
-#pragma unroll
-        for (int k = 1; k < MAXK; ++k) lb = cur[k] > lb ? cur[k] : lb;
-        uint64_t best = warp_max_u64(lb);
-        if (best == 0) {
-            if (lane < 8 && lane >= r) { out[lane] = 0; src[lane] = -1; }
-            break;
-        }
-        if (lb == best) {  // unique owner
-#pragma unroll
-            for (int k = 0; k < MAXK; ++k) {
-                if (cur[k] == best) {
-                    int l = lane + 32 * k;
-                    out[r] = best;
-                    src[r] = l * 8 + hd[k];
-                    ++hd[k];
-                    cur[k] = nxt[k];
-                    nxt[k] = hd[k] + 1 < 8 ? lds_u64(keys + l * 8 + hd[k] + 1) : 0;
-                }
-            }
-        }
-    }
-}
-
 // One warp, one sorted 8-list per lane (heads in registers, the next key prefetched): the top-8
 // of the union in 8 rounds of a 64-bit warp max.  key(l, j) / src(l, j) read list l's j-th entry.
 template <class KeyF, class SrcF>
@@ -666,39 +664,6 @@ __device__ __forceinline__ void lane_list_merge(int nl, KeyF key, SrcF srcf, uin
             cur = nxt;
             nxt = hd + 1 < 8 ? key(lane, hd + 1) : 0ull;
         }
-    }
-}
-
-// Large-L variant (multi-rank runs): heads in shared memory, the winner rescans its lists.
-__device__ __noinline__ void global_merge_smem(const uint64_t* keys, uint8_t* head, int L,
-                                               uint64_t* out, int32_t* src, int lane)
-{
-    for (int l = lane; l < L; l += 32) head[l] = 0;
-    __syncwarp();
-    uint64_t lb = 0;
-    int ll = -1;
-    for (int l = lane; l < L; l += 32)
-        { const uint64_t kk = lds_u64(keys + l * 8); if (kk > lb) { lb = kk; ll = l; } }
-    for (int r = 0; r < 8; ++r) {
-        uint64_t best = warp_max_u64(lb);
-        if (best == 0) {
-            if (lane < 8 && lane >= r) { out[lane] = 0; src[lane] = -1; }
-            break;
-        }
-        if (lb == best) {
-            const int h = head[ll];
-            out[r] = best;
-            src[r] = ll * 8 + h;
-            head[ll] = (uint8_t)(h + 1);
-            lb = 0;
-            ll = -1;
-            for (int l = lane; l < L; l += 32) {
-                const int hh = head[l];
-                const uint64_t k = hh < 8 ? lds_u64(keys + l * 8 + hh) : 0;
-                if (k > lb) { lb = k; ll = l; }
-            }
-        }
-        __syncwarp();
     }
 }
 
@@ -826,7 +791,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ SmoShared sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int L = a.world * a.nblk;
+    const RankView v = rank_view(a);
+    const int L = a.nblk;      // this rank's CTA lists (local level of the exchange)
+    const int P = a.world;     // ranks (rank level of the exchange when > 1)
     const int d = (int)a.d;
     const int dp = (d + 3) & ~3;
     const int R = (int)a.rows_per_cta;
@@ -842,15 +809,16 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     float* sDot = sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
-    const int64_t cta_begin = (int64_t)blockIdx.x * a.rows_per_cta;
-    const int64_t cta_end = min(cta_begin + a.rows_per_cta, a.n_local);
+    const int64_t cta_begin = (int64_t)v.cta * a.rows_per_cta;
+    const int64_t cta_end = min(cta_begin + a.rows_per_cta, v.n_local);
     const int nvalid = cta_end > cta_begin ? (int)(cta_end - cta_begin) : 0;
     const int rows_per_chunk = 32 * RPT;
     const int nchunks = (nvalid + rows_per_chunk - 1) / rows_per_chunk;
-    const int slot = a.rank * a.nblk + blockIdx.x;
-    const bool sys = a.world > 1;
+    const int slot = v.cta;
+    const bool sys = a.world > 1 && !a.virt;   // peers across NVLink: system scope
     const bool reporter = blockIdx.x == 0;  // CTA 0 of every rank reports for its rank
-    uint64_t* rxw = a.peer_xw[a.rank];       // this rank's receive buffer
+    uint64_t* rxr = a.peer_xw[v.rank];      // this rank's exchange buffer: rank level ...
+    uint64_t* rxw = rxr + XW_RANK_WORDS;    // ... and local level (its own CTAs' lists)
 
 #ifdef SMO_POISON
     {
@@ -864,9 +832,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     if constexpr (XS) {
         for (int k = warp; k < d; k += SMO_WARPS)
             for (int r = lane; r < R; r += 32)
-                sX[(size_t)k * R + r] = a.XT[(int64_t)k * a.n_pad + cta_begin + r];
+                sX[(size_t)k * R + r] = v.XT[(int64_t)k * a.n_pad + cta_begin + r];
     }
-    const float* xbase = XS ? sX : a.XT + cta_begin;
+    const float* xbase = XS ? sX : v.XT + cta_begin;
     const int64_t xld = XS ? R : a.n_pad;
     // per-lane cp.async ring for streamed X (in the place of the resident slice)
     const uint32_t xring = (uint32_t)__cvta_generic_to_shared(sX) +
@@ -890,7 +858,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         mbar_arrive_tx(&sh.mb_full[s], (uint32_t)(kn * R * 4));
         float* dst = wring + (size_t)s * wkc * Rs;
         for (int q = 0; q < kn; ++q)
-            bulk_g2s(dst + (size_t)q * Rs, a.XT + (int64_t)(k0 + q) * a.n_pad + cta_begin,
+            bulk_g2s(dst + (size_t)q * Rs, v.XT + (int64_t)(k0 + q) * a.n_pad + cta_begin,
                      (uint32_t)(R * 4), &sh.mb_full[s]);
     };
     if (wide) {
@@ -928,23 +896,21 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             if (k) {
                 const uint64_t g = key_index(k);
                 const int c = g >= (uint64_t)a.n_global ? 1 : 0;
-                const int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - a.row0;
+                const int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - v.row0;
                 const int64_t idx = (int64_t)c * a.n_pad + li;
                 const uint64_t pos = (uint64_t)c * (uint64_t)R + (uint64_t)(li - cta_begin);
                 wkey = tg | ((k >> 32) << 16) | pos;
-                const uint64_t ab = (uint64_t)__double_as_longlong(a.alpha[idx]);
+                const uint64_t ab = (uint64_t)__double_as_longlong(v.alpha[idx]);
                 w0 = tg | (ab >> 16);
-                w1 = tg | ((ab & 0xffffull) << 32) | (uint64_t)__float_as_uint(a.G[idx]);
-                w2 = tg | (uint64_t)a.status[idx];
+                w1 = tg | ((ab & 0xffffull) << 32) | (uint64_t)__float_as_uint(v.G[idx]);
+                w2 = tg | (uint64_t)v.status[idx];
             }
-            const size_t base = ((size_t)par * L + slot) * XW_PER_SLOT;
-            for (int r = 0; r < a.world; ++r) {
-                uint64_t* dst = a.peer_xw[r] + base;
-                st_relaxed_u64(dst + 16 + 3 * tid, w0, sys);
-                st_relaxed_u64(dst + 17 + 3 * tid, w1, sys);
-                st_relaxed_u64(dst + 18 + 3 * tid, w2, sys);
-                st_relaxed_u64(dst + tid, wkey, sys);
-            }
+            // the rank's own local level only (payload words are read by other ranks over NVLink)
+            uint64_t* dst = rxw + ((size_t)par * L + slot) * XW_PER_SLOT;
+            st_relaxed_u64(dst + 16 + 3 * tid, w0, sys);
+            st_relaxed_u64(dst + 17 + 3 * tid, w1, sys);
+            st_relaxed_u64(dst + 18 + 3 * tid, w2, sys);
+            st_relaxed_u64(dst + tid, wkey, sys);
         }
     };
 
@@ -957,15 +923,17 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         for (int ch = warp; ch < nchunks; ch += SMO_WARPS) {
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             uint64_t ku[2 * RPT], kl[2 * RPT];
-            row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, false, acc, ku, kl);
+            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, false, acc, ku, kl);
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
         }
         finish_lists(wlu, wll);
     };
 
     // ---- prologue: scan the current (alpha, G) and publish tag0 + 1 ---------------------------
-    exact_select();
-    publish(a.tag0 + 1);
+    if (!a.pass_only) {
+        exact_select();
+        publish(a.tag0 + 1);
+    }
     // per-iteration exchange latency (CTA 0, thread 0): its publish -> every rank's slots staged.
     // Includes the wait for the slowest CTA of any rank, i.e. what the collective costs the loop.
     // One 32-bit register across the loop (differences mod 2^32); the sums go out as fire-and-
@@ -1007,7 +975,36 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         const uint32_t tag = a.tag0 + 1 + (uint32_t)t;
         const int par = tag & 1;
         const uint64_t tg = tag16_of(tag);
-        // ---- a1 (1/2): wait for + stage every slot's 16 key words (decoded to 64-bit keys) ----
+        // no bulk copy may outlive the CTA (wide mode): wait for the stages the producer issued
+        auto drain_wide = [&]() {
+            if (wide && warp == ncw && lane == 0)
+                for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
+                    mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
+        };
+        if (a.pass_only) {
+            // ---- pass-only diagnostic: fixed W (local rows of a single rank), fixed c ----------
+            if (t >= a.max_iter) {
+                drain_wide();
+                if (reporter && tid == 0) {
+                    a.info->iterations = t;
+                    atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->loop_cycles), (unsigned long long)clock64());
+                }
+                return;
+            }
+            if (tid == 0) {
+                sh.next_chunk = 0;
+                sh.next_chunk2 = 0;
+                sh.sub_done = 1;   // no subproblem: phase A buffers nothing, phase B streams all
+                sh.nr = a.pass_nr;
+                sh.nw = a.pass_nr;
+            }
+            if (t == 0 && tid < SVM_WS) {
+                sh.r_row[tid] = tid < a.pass_nr ? a.pass_rows[tid] : 0;
+                sh.c[tid] = tid < a.pass_nr ? a.pass_c[tid] : 0.0f;
+            }
+            __syncthreads();
+        } else {
+        // ---- a1 (1/3): wait for + stage this rank's CTA lists (16 key words each, decoded) -----
         if (tid == 0) sh.timeout = 0;
         {
             const uint64_t* src = rxw + (size_t)par * L * XW_PER_SLOT;
@@ -1040,12 +1037,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     uint64_t key = 0;
                     const uint32_t score = (uint32_t)(w[u] >> 16);
                     if (score) {
-                        int r = 0, blk = sl;
-                        if (a.world > 1) { r = sl / a.nblk; blk = sl - r * a.nblk; }
-                        const uint64_t Rr = (uint64_t)a.rank_rpc[r];
+                        const uint64_t Rr = (uint64_t)R;
                         const uint64_t pos = w[u] & 0xffffull;
                         const uint64_t c = pos >= Rr ? 1 : 0;
-                        const uint64_t row = (uint64_t)a.rank_row0[r] + (uint64_t)blk * Rr + pos - c * Rr;
+                        const uint64_t row = (uint64_t)v.row0 + (uint64_t)sl * Rr + pos - c * Rr;
                         const uint64_t g = c * (uint64_t)a.n_global + row;
                         key = ((uint64_t)score << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
                     }
@@ -1054,62 +1049,127 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
         }
         __syncthreads();
-        if (reporter && tid == 0) {   // a shared load first: the barrier is DEFER_BLOCKING
-            const int v = *reinterpret_cast<volatile int*>(&sh.timeout);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->exch_cycles),
-                      (unsigned long long)(uint32_t)((uint32_t)clock() - x_pub + (uint32_t)(v & 0)));
-        }
-        mark(0);
-        if (sh.timeout) {
+        auto report_exchange = [&]() {   // a shared load first: the barrier is DEFER_BLOCKING
+            if (reporter && tid == 0) {
+                const int vv = *reinterpret_cast<volatile int*>(&sh.timeout);
+                const uint32_t dt = (uint32_t)clock() - x_pub + (uint32_t)(vv & 0);
+                atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->exch_cycles), (unsigned long long)dt);
+                atomicAdd(&a.info->exch_hist[exch_bin(dt)], 1u);
+            }
+        };
+        auto timed_out = [&]() {
+            if (!sh.timeout) return false;
             if (reporter && tid == 0) a.info->error = 1;
-            if (wide && warp == ncw && lane == 0)   // no bulk copy may outlive the CTA
-                for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
-                    mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
-            return;
-        }
-        // ---- a1 (2/2): global merge (warp 0: I_up top-8, warp 1: I_low top-8) ----------------
+            drain_wide();
+            return true;
+        };
+        if (P == 1) report_exchange();
+        mark(0);
+        if (timed_out()) return;
+        // ---- a1 (2/3): merge of the rank's L <= 256 lists (warp 0: I_up top-8, warp 1: I_low
+        // top-8).  Two levels: 8 warps per side merge <= 32 lists each (one per lane), then one
+        // warp per side merges the 8 partial top-8 lists.  src = (rank << 24) | (CTA slot << 4) |
+        // candidate word (0-7 up, 8-15 low) throughout.
         wmark(-1);
-        if (L <= 8 * 32) {
-            // two levels: 8 warps per side merge <= 32 lists each (one per lane), then one warp per
-            // side merges the 8 partial top-8 lists (src = list * 8 + position throughout)
-            {
-                const int side = warp >> 3, part = warp & 7;
-                const uint64_t* keys = side == 0 ? sKU : sKL;
-                const int per = (L + 7) >> 3, l0 = part * per;
-                const int nl = max(0, min(per, L - l0));
+        {
+            const int side = warp >> 3, part = warp & 7;
+            const uint64_t* keys = side == 0 ? sKU : sKL;
+            const int per = (L + 7) >> 3, l0 = part * per;
+            const int nl = max(0, min(per, L - l0));
+            const int32_t sbase = (v.rank << 24) | (side << 3);
 #ifdef SMO_PROFILE
-                const long long c0 = clock64();
+            const long long c0 = clock64();
 #endif
+            lane_list_merge(nl, [&](int i, int j) { return lds_u64(keys + (l0 + i) * 8 + j); },
+                            [&](int i, int j) { return sbase | ((l0 + i) << 4) | j; },
+                            sh.gm_key[side][part], sh.gm_src[side][part], lane);
+#ifdef SMO_PROFILE
+            {   // I-cache probe: the same merge again (warm instructions), into scratch
+                uint64_t sk[8]; int32_t ss[8];
+                const int v0 = *reinterpret_cast<volatile int*>(&sh.nw);
+                const long long c1 = clock64() + (v0 & 0);
                 lane_list_merge(nl, [&](int i, int j) { return lds_u64(keys + (l0 + i) * 8 + j); },
-                                [&](int i, int j) { return (l0 + i) * 8 + j; },
-                                sh.gm_key[side][part], sh.gm_src[side][part], lane);
-#ifdef SMO_PROFILE
-                {   // I-cache probe: the same merge again (warm instructions), into scratch
-                    uint64_t sk[8]; int32_t ss[8];
-                    const int v0 = *reinterpret_cast<volatile int*>(&sh.nw);
-                    const long long c1 = clock64() + (v0 & 0);
-                    lane_list_merge(nl, [&](int i, int j) { return lds_u64(keys + (l0 + i) * 8 + j); },
-                                    [&](int i, int j) { return (l0 + i) * 8 + j; }, sk, ss, lane);
-                    const int v1 = *reinterpret_cast<volatile int*>(&sh.nw);
-                    const long long c2 = clock64() + (v1 & 0) + (long long)(sk[0] & 0);
-                    if (warp == 0) { wprof[6] += c1 - c0; wprof[7] += c2 - c1; }
-                }
+                                [&](int i, int j) { return sbase | ((l0 + i) << 4) | j; }, sk, ss, lane);
+                const int v1 = *reinterpret_cast<volatile int*>(&sh.nw);
+                const long long c2 = clock64() + (v1 & 0) + (long long)(sk[0] & 0);
+                if (warp == 0) { wprof[6] += c1 - c0; wprof[7] += c2 - c1; }
+            }
 #endif
+        }
+        __syncthreads();
+        if (warp < 2) {
+            uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
+            int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
+            lane_list_merge(8, [&](int i, int j) { return lds_u64(&sh.gm_key[warp][i][j]); },
+                            [&](int i, int j) { return sh.gm_src[warp][i][j]; }, out, srcs, lane);
+        }
+        __syncthreads();
+        if (P > 1) {
+            // ---- a1 (3/3), world > 1: CTA 0 of every rank publishes the rank's merged 8 + 8 list
+            // into every rank's rank level; every CTA stages the P lists and merges them.  The
+            // global top-8 is contained in the union of the per-rank top-8s, so this is exact.
+            if (v.cta == 0 && tid < 16) {
+                const uint64_t k = tid < 8 ? sh.win_up[tid] : sh.win_low[tid - 8];
+                const int32_t s = tid < 8 ? sh.win_up_src[tid] : sh.win_low_src[tid - 8];
+                uint64_t w0 = tg, w1 = tg;
+                if (k) {
+                    const uint64_t g = key_index(k);
+                    const int c = g >= (uint64_t)a.n_global ? 1 : 0;
+                    const int64_t li = (int64_t)(g - (uint64_t)c * a.n_global) - v.row0;
+                    const int blk = (s >> 4) & 0xfffff;
+                    const uint64_t pos = (uint64_t)c * (uint64_t)R + (uint64_t)(li - (int64_t)blk * R);
+                    w0 = tg | ((k >> 32) << 16) | (uint64_t)blk;
+                    w1 = tg | ((uint64_t)(s & 15) << 16) | pos;
+                }
+                const size_t base = ((size_t)par * SVM_MAX_RANKS + v.rank) * XW_RANK_SLOT + 2 * tid;
+                for (int r = 0; r < P; ++r) {
+                    uint64_t* dst = a.peer_xw[r] + base;
+                    st_relaxed_u64(dst + 1, w1, sys);
+                    st_relaxed_u64(dst, w0, sys);
+                }
+            }
+            if (tid < P * 16) {
+                const int o = tid >> 4, cnd = tid & 15;
+                const uint64_t* pw = rxr + ((size_t)par * SVM_MAX_RANKS + o) * XW_RANK_SLOT + 2 * cnd;
+                uint64_t w0 = ld_relaxed_u64(pw, sys), w1 = ld_relaxed_u64(pw + 1, sys);
+                uint64_t t0 = 0;
+                int spins = 0;
+                while ((w0 & 0xffff000000000000ull) != tg || (w1 & 0xffff000000000000ull) != tg) {
+                    if (++spins == 256) {
+                        spins = 0;
+                        const uint64_t now = globaltimer_ns();
+                        if (t0 == 0) t0 = now;
+                        else if (now - t0 > a.timeout_ns) { sh.timeout = 1; break; }
+                    }
+                    w0 = ld_relaxed_u64(pw, sys);
+                    w1 = ld_relaxed_u64(pw + 1, sys);
+                }
+                uint64_t key = 0;
+                int32_t src = -1;
+                const uint32_t score = (uint32_t)(w0 >> 16);
+                if (score) {
+                    const uint64_t blk = w0 & 0xffffull, pos = w1 & 0xffffull, q = (w1 >> 16) & 0xfull;
+                    const uint64_t Rr = (uint64_t)a.rank_rpc[o];
+                    const uint64_t c = pos >= Rr ? 1 : 0;
+                    const uint64_t row = (uint64_t)a.rank_row0[o] + blk * Rr + pos - c * Rr;
+                    const uint64_t g = c * (uint64_t)a.n_global + row;
+                    key = ((uint64_t)score << 32) | (uint64_t)(0xffffffffu - (uint32_t)g);
+                    src = (int32_t)(((uint32_t)o << 24) | ((uint32_t)blk << 4) | (uint32_t)q);
+                }
+                sh.rk_key[cnd >> 3][o * 8 + (cnd & 7)] = key;
+                sh.rk_src[cnd >> 3][o * 8 + (cnd & 7)] = src;
             }
             __syncthreads();
+            report_exchange();
+            if (timed_out()) return;
             if (warp < 2) {
                 uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
                 int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
-                lane_list_merge(8, [&](int i, int j) { return lds_u64(&sh.gm_key[warp][i][j]); },
-                                [&](int i, int j) { return sh.gm_src[warp][i][j]; }, out, srcs, lane);
+                lane_list_merge(P, [&](int i, int j) { return lds_u64(&sh.rk_key[warp][i * 8 + j]); },
+                                [&](int i, int j) { return sh.rk_src[warp][i * 8 + j]; }, out, srcs, lane);
             }
-        } else if (warp < 2) {
-            const uint64_t* keys = warp == 0 ? sKU : sKL;
-            uint64_t* out = warp == 0 ? sh.win_up : sh.win_low;
-            int32_t* srcs = warp == 0 ? sh.win_up_src : sh.win_low_src;
-            global_merge_smem(keys, reinterpret_cast<uint8_t*>(sh.qpart) + warp * 2048, L, out, srcs, lane);
+            __syncthreads();
         }
-        __syncthreads();
         if (warp == 0) {
             // W = sorted union of |W|/2 up winners and |W|/2 low winners, deduplicated
             const int half = a.q >> 1;
@@ -1117,11 +1177,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             int32_t src = -1;
             if (lane < 8 && lane < half) {
                 key = sh.win_up[lane];
-                if (key) src = (sh.win_up_src[lane] >> 3) * XW_PER_SLOT + (sh.win_up_src[lane] & 7);
+                if (key) src = sh.win_up_src[lane];
             } else if (lane >= 8 && lane < 16 && lane - 8 < half) {
                 key = sh.win_low[lane - 8];
-                if (key)
-                    src = (sh.win_low_src[lane - 8] >> 3) * XW_PER_SLOT + 8 + (sh.win_low_src[lane - 8] & 7);
+                if (key) src = sh.win_low_src[lane - 8];
             }
             const uint64_t g = key ? key_index(key) : ~0ull;
             bool valid = key != 0;
@@ -1180,9 +1239,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         __syncthreads();
         mark(1);
         if (sh.stop) {
-            if (wide && warp == ncw && lane == 0)   // no bulk copy may outlive the CTA
-                for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
-                    mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
+            drain_wide();
             if (reporter && tid == 0) {
                 a.info->iterations = t;
                 a.info->m_up = sh.m_up;
@@ -1198,9 +1255,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
 #endif
             return;
         }
+        }   // !pass_only
         // ---- a2 setup: X_W rows (fp32 [d][16], for the pass and for K_WW), their
         // norms and the W payloads; one warp per row, no integer division -------------------
         const int nw = sh.nw, nr = sh.nr;
+        if (!a.pass_only || t == 0) {
         if constexpr (CSR) {
             for (int i = tid; i < d * WS; i += SMO_THREADS) sXW[i] = 0.0f;
         } else {
@@ -1208,10 +1267,13 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 if ((i & 15) >= nr) sXW[i] = 0.0f;
         }
         if constexpr (CSR) __syncthreads();
-        if (warp == SMO_WARPS - 1 && lane < nw) {  // payloads of W (tagged words)
+        if (!a.pass_only && warp == SMO_WARPS - 1 && lane < nw) {  // payloads of W (tagged words,
+            // in the owner rank's local level: src = (rank << 24) | (CTA slot << 4) | candidate)
             const int p = lane;
-            const int q = sh.w_src[p] % XW_PER_SLOT;
-            const uint64_t* pl = rxw + (size_t)par * L * XW_PER_SLOT + sh.w_src[p] - q + 16 + 3 * q;
+            const int32_t s = sh.w_src[p];
+            const int o = s >> 24, blk = (s >> 4) & 0xfffff, q = s & 15;
+            const uint64_t* pl = a.peer_xw[o] + XW_RANK_WORDS +
+                                 ((size_t)par * a.rank_nblk[o] + blk) * XW_PER_SLOT + 16 + 3 * q;
             uint64_t w0 = ld_relaxed_u64(pl, sys), w1 = ld_relaxed_u64(pl + 1, sys),
                      w2 = ld_relaxed_u64(pl + 2, sys);
             while ((w0 & 0xffff000000000000ull) != tg) w0 = ld_relaxed_u64(pl, sys);
@@ -1230,35 +1292,36 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             if constexpr (!CSR) {
                 const float* src = a.peer_XR[o] + lr * a.d;
                 for (int k0 = 0; k0 < d; k0 += 8 * 32) {  // 8 loads in flight per lane
-                    float v[8];
+                    float xv[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int k = k0 + u * 32 + lane;
-                        v[u] = k < d ? __ldg(src + k) : 0.0f;
+                        xv[u] = k < d ? __ldg(src + k) : 0.0f;
                     }
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int k = k0 + u * 32 + lane;
-                        if (k < d) sXW[k * SVM_WS + r] = v[u];
+                        if (k < d) sXW[k * SVM_WS + r] = xv[u];
                     }
                 }
             } else {
                 const int64_t b = a.peer_indptr[o][lr], e = a.peer_indptr[o][lr + 1];
                 for (int64_t p = b + lane; p < e; p += 32) {
                     const int k = a.peer_indices[o][p];
-                    const float v = a.peer_vals[o][p];
-                    sXW[k * WS + r] = v;
-                    if (v != 0.0f) atomicOr(reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);   // group mask
+                    const float xv = a.peer_vals[o][p];
+                    sXW[k * WS + r] = xv;
+                    if (xv != 0.0f) atomicOr(reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);   // group mask
                 }
             }
             if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];
         }
         if (tid >= nr && tid < SVM_WS) sh.xn[tid] = 0.0f;
         __syncthreads();
+        }   // X_W staged (once in pass-only mode)
         mark(2);
         wmark(-1);
         // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
-        {
+        if (!a.pass_only) {
             const int npairs = nr * (nr + 1) / 2;
             const int kp = max(1, min(4, SMO_THREADS / max(npairs, 1)));
             const int klen = ((d + kp - 1) / kp + 3) & ~3;
@@ -1303,9 +1366,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 int r = 0, rem = tid;
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
                 const int sidx = r + rem;
-                double v = 0.0;
-                for (int part = 0; part < kp; ++part) v += sh.qpart[tid * 4 + part];
-                const double kv = kernel_fp64_from(v, a.kp);
+                double dsum = 0.0;
+                for (int part = 0; part < kp; ++part) dsum += sh.qpart[tid * 4 + part];
+                const double kv = kernel_fp64_from(dsum, a.kp);
                 sh.kr[r * SVM_WS + sidx] = kv;
                 sh.kr[sidx * SVM_WS + r] = kv;
             }
@@ -1347,7 +1410,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 const int k0 = sl * ks, kn = min(d, k0 + ks) - k0;
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
-                if constexpr (CSR) dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
                 else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, acc);
                 else dots_dense_async<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, xring, acc);
                 const int lr = (int)(li0 - cta_begin);
@@ -1360,7 +1423,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 }
             }
         };
-        if (warp == SOLVER_WARP) {
+        if (warp == SOLVER_WARP && !a.pass_only) {
             // ---- a2: the subproblem on the solver warp (the highest warp id: the SM's warp
             // arbiter favours high ids), overlapped with phase A on the other warps ------------
             const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
@@ -1378,11 +1441,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             if (lane < nw) {
                 const int64_t g = sh.w_gidx[lane];
                 const int c = g >= a.n_global ? 1 : 0;
-                const int64_t li = g - (int64_t)c * a.n_global - a.row0;
+                const int64_t li = g - (int64_t)c * a.n_global - v.row0;
                 if (li >= cta_begin && li < cta_end) {
                     const int64_t idx = (int64_t)c * a.n_pad + li;
-                    a.alpha[idx] = sh.w_anew[lane];
-                    a.status[idx] = make_status(sh.w_y[lane], sh.w_anew[lane], a.C);
+                    v.alpha[idx] = sh.w_anew[lane];
+                    v.status[idx] = make_status(sh.w_y[lane], sh.w_anew[lane], a.C);
                 }
             }
             if (reporter) {
@@ -1437,7 +1500,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             wmark(-1);
             if (warp < ncw) {
                 uint64_t ku[2 * RPT], kl[2 * RPT];
-                row_epilogue<RPT, RBFK>(a, sh, cta_begin + lr, cta_end, true, acc, ku, kl);
+                row_epilogue<RPT, RBFK>(a, v, sh, cta_begin + lr, cta_end, true, acc, ku, kl);
                 merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             }
         } else {
@@ -1484,7 +1547,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                             acc[j][r] += sDot[(size_t)(q * SVM_WS + r) * dbuf_rows + lr + j];
                 }
             } else if constexpr (CSR) {
-                dots_csr_staged(a.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
             } else if (XS || !a.x_ring) {
                 dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
             } else {
@@ -1492,7 +1555,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             }
             wmark(0);
             uint64_t ku[2 * RPT], kl[2 * RPT];
-            row_epilogue<RPT, RBFK>(a, sh, li0, cta_end, true, acc, ku, kl);
+            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, true, acc, ku, kl);
             wmark(2);
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             wmark(3);
@@ -1502,7 +1565,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         finish_lists(wlu, wll);
         mark(6);
         wmark(5);
-        publish(tag + 1);
+        if (!a.pass_only) publish(tag + 1);
         if (reporter && tid == 0) x_pub = (uint32_t)clock();
         mark(7);
     }
@@ -2176,8 +2239,24 @@ int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS))
 
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)
 {
-    int64_t L = (int64_t)world * nblk;
+    (void)world;   // the rank level (<= SVM_MAX_RANKS lists) lives in static shared memory
+    const int64_t L = nblk;
     return (int)(((d * 16 + 3) & ~3) * 4 + L * 8 * 8 * 2 + 4 * d * x_rows);  // + 64 B per buffered row
+}
+
+// persisting-L2 limit of the caller, saved by launch_smo and restored by smo_l2_restore (one
+// training at a time per thread; thread_local so concurrent trainings do not mix their values)
+static thread_local size_t g_l2_saved = 0;
+static thread_local bool g_l2_raised = false;
+void smo_l2_restore()
+{
+    if (!g_l2_raised) return;
+    g_l2_raised = false;
+    // demote this library's persisting lines only when nobody else had a set-aside (a reset
+    // would also demote the caller's); otherwise shrinking the set-aside back releases them
+    if (g_l2_saved == 0) cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved);
+    cudaGetLastError();
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
@@ -2196,7 +2275,7 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.nblk);
+    cfg.gridDim = dim3(a.virt ? a.nblk * a.world : a.nblk);   // virtual ranks: all in this launch
     cfg.blockDim = dim3(SMO_THREADS);
     cfg.dynamicSmemBytes = (size_t)smem_bytes;
     cfg.stream = st;
@@ -2208,21 +2287,28 @@ cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
     // X streamed from HBM every iteration (not resident in shared memory): an L2 access-policy
     // window marks this rank's X^T as persisting, so the part that fits the L2 set-aside stays
     // in L2 across iterations (c4: X = 108 MB against a 126 MB L2).  Arithmetic is unchanged.
-    static size_t persist_max = (size_t)-1, window_max = 0;
-    if (persist_max == (size_t)-1) {
+    size_t persist_max = 0, window_max = 0;
+    {
         int dev = 0, pm = 0, wm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&pm, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&wm, cudaDevAttrMaxAccessPolicyWindowSize, dev);
         persist_max = (size_t)pm;
         window_max = (size_t)wm;
-        if (persist_max > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_max) != cudaSuccess) {
-            cudaGetLastError();
-            persist_max = 0;
-        }
     }
     const size_t xbytes = a.XT ? (size_t)a.d * (size_t)a.n_pad * sizeof(float) : 0;
-    if (a.XT && !a.x_in_smem && persist_max > 0 && window_max > 0 && !getenv("SVMB200_NO_L2PERSIST")) {
+    const bool persist = a.XT && !a.x_in_smem && persist_max > 0 && window_max > 0 &&
+                         !getenv("SVMB200_NO_L2PERSIST");
+    // the L2 set-aside is raised for this launch only: smo_l2_restore (after the loop) puts the
+    // caller's limit back
+    if (persist) {
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        g_l2_saved = cur;
+        g_l2_raised = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_max) == cudaSuccess;
+        cudaGetLastError();
+    }
+    if (persist && g_l2_raised) {
         const size_t win = std::min(xbytes, window_max);
         attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[na].val.accessPolicyWindow.base_ptr = const_cast<float*>(a.XT);
@@ -2296,22 +2382,13 @@ int ovr_pass_smem(const OvrArgs& a)
 
 cudaError_t launch_ovr_pass(const OvrArgs& a0, cudaStream_t st)
 {
-    static int nsm = 0;
-    if (nsm == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-    }
+    const int nsm = svm_device_sms();
     OvrArgs a = a0;
     ovr_rings(a.NU, &a.na, &a.nb);
     const int smem = ovr_pass_smem_n(a.NU, a.na, a.nb);
-    static int smem_set = 0;   // the attribute is set outside stream capture (launch_ovr_pass_prepare)
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-    }
+    // (a per-launch attribute call: kernel attributes are per device, and this costs ~1 us)
+    cudaError_t e = cudaFuncSetAttribute(k_ovr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
     svm_note_launches(1);
     return ovr_launch(k_ovr_pass, std::min(nsm, a.nct), OVR_PASS_THREADS, smem, st, a);
 }
@@ -2344,14 +2421,9 @@ cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cuda
 }
 
 static int ovr_solve_smem(const OvrArgs& a) { return (int)(((a.d + 3) & ~3) * 24 * 8); }   // fp64 X_W
-static int g_solve_smem_set = 0;
 cudaError_t launch_ovr_solve_prepare(const OvrArgs& a)
 {
-    const int smem = ovr_solve_smem(a);
-    if (smem <= g_solve_smem_set) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) g_solve_smem_set = smem;
-    return e;
+    return cudaFuncSetAttribute(k_ovr_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, ovr_solve_smem(a));
 }
 cudaError_t launch_ovr_solve(const OvrArgs& a, cudaStream_t st)
 {

@@ -106,7 +106,29 @@ __device__ __forceinline__ uint64_t key_index(uint64_t key) { return 0xffffffffu
 // + local row, score 0 = no candidate) and 16 x 3 payload words carrying the candidate's alpha
 // (fp64), G (fp32) and status byte.
 #define XW_PER_SLOT 64
+// Per-rank exchange buffer = [rank level: 2 parities x SVM_MAX_RANKS x XW_RANK_SLOT words]
+// followed by [local level: 2 parities x nblk CTA slots x XW_PER_SLOT words].  The local level is
+// the all-to-all of the rank's own CTAs (every CTA merges the rank's nblk lists); with world > 1
+// CTA 0 of every rank then publishes the rank's merged 8 + 8 list into every rank's rank level
+// (2 words per candidate: [tag | ord(score) 32 | CTA slot 16] and [tag | candidate 16 | pos 16]),
+// so the lists a CTA stages and merges number nblk + world, not world x nblk (SURVEY 8(e):
+// one 8+8 list per rank).  Payload words stay in the owner's local level, read over NVLink.
+#define XW_RANK_SLOT 32
+#define XW_RANK_WORDS (2 * SVM_MAX_RANKS * XW_RANK_SLOT)
 __host__ __device__ __forceinline__ uint64_t tag16_of(uint32_t tag) { return (uint64_t)(tag % 65535u + 1u) << 48; }
+
+// Histogram of the per-iteration exchange latency (cycles): 64 bins of 512 cycles below 32768,
+// then 64 bins of 4096 cycles (the last one open) -- p50 / p99 for the scaling report.
+#define SMO_EXCH_BINS 128
+__host__ __device__ __forceinline__ int exch_bin(uint32_t c)
+{
+    const uint32_t hi = (c - 32768u) >> 12;
+    return c < 32768u ? (int)(c >> 9) : 64 + (int)(hi < 63u ? hi : 63u);
+}
+__host__ __device__ __forceinline__ double exch_bin_mid(int b)
+{
+    return b < 64 ? 512.0 * b + 256.0 : 32768.0 + 4096.0 * (b - 64) + 2048.0;
+}
 
 // Device-side result record of the persistent loop (written by CTA 0 of rank 0).
 struct SmoInfo {
@@ -122,6 +144,7 @@ struct SmoInfo {
     int64_t phase_cycles[16]; // CTA 0: clock64 per phase (solver [0,8), worker warp 0 [8,16))
     int64_t exch_cycles;      // CTA 0, thread 0: clock64 from its publish to all slots staged
     int64_t loop_cycles;      // CTA 0, thread 0: clock64 over the whole loop (prologue excluded)
+    uint32_t exch_hist[SMO_EXCH_BINS];   // per-iteration exchange cycles (exch_bin)
 };
 
 // All arguments of the persistent working-set kernel (passed by value).
@@ -144,8 +167,12 @@ struct SmoArgs {
     int32_t inner_max;
     int32_t q;                // |W| requested (even, <= 16)
     KParams kp;
-    // ranks (world = 1 for single-GPU training)
-    int32_t rank, world, nblk;
+    // ranks (world = 1 for single-GPU training).  virt = 1: all `world` ranks run inside this
+    // one launch (virtual ranks on one GPU, `nblk` CTAs each; rank r = blockIdx.x / nblk owns rows
+    // [rank_row0[r], rank_row0[r + 1]) of the arrays above, which then hold ALL rows) -- the
+    // multi-rank exchange, owner and peer-gather code runs exactly as across GPUs.
+    int32_t rank, world, nblk, virt;
+    int32_t rank_nblk[SVM_MAX_RANKS];         // CTAs of each rank
     int64_t rank_row0[SVM_MAX_RANKS + 1];
     const float* peer_XR[SVM_MAX_RANKS];      // dense row-major rows of each rank
     const float* peer_xnorm[SVM_MAX_RANKS];   // squared norms of each rank's rows
@@ -153,7 +180,7 @@ struct SmoArgs {
     const int32_t* peer_indices[SVM_MAX_RANKS];
     const float* peer_vals[SVM_MAX_RANKS];
     int64_t rank_rpc[SVM_MAX_RANKS];          // rows_per_cta of each rank
-    uint64_t* peer_xw[SVM_MAX_RANKS];         // receive buffers: [2][world*nblk][XW_PER_SLOT]
+    uint64_t* peer_xw[SVM_MAX_RANKS];         // exchange buffers (XW_RANK_WORDS + 2 nblk XW_PER_SLOT)
     uint32_t tag0;            // epoch: this launch publishes tags tag0+1, tag0+2, ...
     int64_t max_iter;         // iterations allowed in this launch
     uint64_t timeout_ns;
@@ -167,6 +194,12 @@ struct SmoArgs {
     int32_t nslice;           // > 1: phase A splits the features of each chunk into nslice items
                               //      (partials [nslice][16][dbuf_rows], summed in slice order)
     int32_t x_ring;           // streamed X through a per-lane cp.async ring (RPT >= 2)
+    // pass-only diagnostic (svm_solver_pass_bench): max_iter repetitions of the fused a3 pass +
+    // CTA selection with a FIXED working set (local rows pass_rows[0..pass_nr), coefficients
+    // pass_c), no exchange and no subproblem -- the same device code, timed in isolation
+    int32_t pass_only, pass_nr;
+    const int64_t* pass_rows;
+    const float* pass_c;
 };
 
 // Batched one-vs-rest: P <= 16 binary problems on the same dense X, one X pass per
@@ -214,8 +247,25 @@ cudaError_t launch_absmax(const float* X, int64_t count, unsigned int* out, cuda
 
 // Count of CUDA kernels launched by this library (svm_launch_count in the C ABI).
 void svm_note_launches(int k);
+// The library's private stream-ordered memory pool of the current device (capi.cu): every
+// scratch buffer is allocated from it on the caller's stream and freed on that stream at the end
+// of the call -- no scratch is shared between calls, threads or devices.
+cudaMemPool_t svm_mem_pool();
+inline cudaError_t svm_scratch_alloc(void** p, size_t bytes, cudaStream_t st)
+{
+    cudaMemPool_t pool = svm_mem_pool();
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
+inline int svm_device_sms()
+{
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
+void smo_l2_restore();   // after the launch's loop: the caller's persisting-L2 limit back
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
 int smo_ring_bytes(int rpt);
 int smo_csr_stage_bytes();

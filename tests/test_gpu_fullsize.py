@@ -1,12 +1,11 @@
-"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+"""GPU parity for C5 (CSR), whose full-size oracle run does not finish on the host.
 
-The oracle cannot train these problems in test time, so (task ③) the GPU model is
-checked on SAMPLED outputs the oracle computes one by one in fp64, and through properties that
-hold at any size:
+C1-C4 are compared at full size against the oracle's own solutions (tests/test_gpu_golden.py).
+For the CSR config the GPU model is checked on SAMPLED outputs the oracle computes one by one in
+fp64, and through properties that hold at any size:
   * KKT on a sample: for sampled training duals, G_i is recomputed by the oracle in fp64 from the
     GPU model's support vectors (G = Q alpha + p); the sampled violation
-    max_{I_up} s - min_{I_low} s over the sample must be <= tol (1e-3) plus the fp32-kernel
-    margin the survey measured (2e-5);
+    max_{I_up} s - min_{I_low} s over the sample must be <= tol (1e-3);
   * predict on a sample: decision values of held-out rows by the oracle (fp64) from the GPU
     model's SVs and coefficients vs svm_predict, within 1e-5 sum_s |coef_s K_s| + 1e-6 (fp32
     kernel values) and within north_star's 1e-3;
@@ -77,7 +76,7 @@ def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=
                 up.append(s)
             if (y[k] > 0 and a > 0) or (y[k] < 0 and a < C):
                 low.append(s)
-    assert max(up) - min(low) <= tol + 2e-5, (max(up), min(low))
+    assert max(up) - min(low) <= tol, (max(up), min(low))
     # sampled held-out decision values vs the oracle's fp64 decision of the same model
     H = synth.make(ds.name, n=2000, heldout=True)
     Xh = H.dense() if H.is_csr else H.X
@@ -97,51 +96,6 @@ def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=
     assert (err <= 1e-5 * mass + 1e-6).all(), (err.max(), (err / (mass + 1e-12)).max())
     assert err.max() <= 1e-3
     return dec, fo
-
-
-def test_c2_full_size():
-    """configs[1] (the bench workload): eps-SVR 50,000 x 100."""
-    ds = synth.make("c2")
-    import torch
-    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(),
-                  svm_type="eps-regression", gamma=1.0 / ds.d, epsilon=0.1)
-    _sample_checks(ds, m, True, np.random.default_rng(0))
-
-
-def test_c4_full_size():
-    """configs[3]: covertype-shaped C-SVC 500,000 x 54 (X streamed from HBM)."""
-    ds = synth.make("c4")
-    import torch
-    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d)
-    _sample_checks(ds, m, False, np.random.default_rng(1))
-
-
-def test_c3_full_size_ovr():
-    """configs[2]: 10-class one-vs-rest C-SVC, MNIST-shaped 60,000 x 784 (the batched tcgen05
-    passes bench.py times).  Every class problem is checked on its own sample (y = +1 iff the
-    label is that class, S:325 / BASELINE config 3), and the one-vs-rest label is the argmax of
-    the decision values (ties -> lowest class)."""
-    ds = synth.make("c3")
-    import torch
-    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d)
-    info = m.info
-    assert info.n_problem == 10 and info.n_class == 10
-    labels = np.array(info.labels[:10])
-    assert sorted(labels.tolist()) == sorted(set(ds.y.astype(np.float64).tolist()))
-    H = synth.make("c3", n=2000, heldout=True)
-    hr = np.random.default_rng(30).choice(H.n, size=60, replace=False)
-    fo_all = np.empty((60, 10))
-    for p in range(10):
-        ybin = np.where(ds.y.astype(np.float64) == labels[p], 1.0, -1.0)
-        _, fo_all[:, p] = _sample_checks(ds, m, False, np.random.default_rng(30), n_sample=100,
-                                         prob=p, ybin=ybin, held_rows=hr)
-    out, dec = m.predict(H.X[hr], decision=True)
-    assert np.array_equal(out, labels[np.argmax(dec, axis=1)].astype(np.float32))
-    # labels agree with the oracle's argmax wherever the oracle's top-2 gap exceeds the
-    # decision tolerance (1e-3); north_star asks >= 99.9% agreement overall
-    srt = np.sort(fo_all, axis=1)
-    clear = srt[:, -1] - srt[:, -2] > 2e-3
-    assert np.array_equal(out[clear], labels[np.argmax(fo_all, axis=1)][clear].astype(np.float32))
 
 
 def test_c5_csr_sample_size():

@@ -185,7 +185,8 @@ def test_one_step_from_identical_state(kname, svm_type, csr):
 def _labels_agree(out, f_ref, pred_ref, tol=1e-3):
     """Labels must agree wherever the oracle's decision is unique at the decision tolerance:
     binary |f| > 2 tol, one-vs-rest top-1 minus top-2 > 2 tol (a row closer to the boundary may
-    legitimately take either label).  Returns the overall agreement for reporting."""
+    legitimately take either label).  Returns the overall agreement, which the callers hold to
+    north_star's >= 99.9% on >= 2,000 rows."""
     f_ref = np.asarray(f_ref)
     if f_ref.ndim == 1 or f_ref.shape[1] == 1:
         margin = np.abs(f_ref.reshape(-1))
@@ -231,12 +232,12 @@ def test_end_to_end(cfg, n):
     assert info.converged == 1
     assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
     Xh = synth.make(cfg, n=min(ds.n, 1000), heldout=True).X
-    for Xq in (ds.X[:1500], Xh):
-        out, dec = model.predict(Xq, decision=True)
-        f_ora = om.decision_function(Xq)[:, 0]
-        assert np.abs(dec[:, 0] - f_ora).max() <= 1e-3
-        if not reg:
-            assert _labels_agree(out, f_ora, om.predict(Xq)) >= 0.99
+    Xq = np.concatenate([ds.X[:1500], Xh])
+    out, dec = model.predict(Xq, decision=True)
+    f_ora = om.decision_function(Xq)[:, 0]
+    assert np.abs(dec[:, 0] - f_ora).max() <= 1e-3
+    if not reg:   # north_star: >= 99.9% label agreement (2,500 rows: at most 2 boundary flips)
+        assert _labels_agree(out, f_ora, om.predict(Xq)) >= 0.999
     prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION,
                        ds.y if reg else ora.binary_labels(ds.y)[0], ds.n, 0.1)
     alpha = _alpha_from_model(model, prob, ds.n, 1.0)
@@ -280,11 +281,11 @@ def test_ovr_multiclass():
     info = model.info
     assert info.n_problem == 10 and info.n_class == 10
     om = ora.train(ds.X, ds.y, gamma=1.0 / 40)
-    Xh = synth.make("c3", n=400, d=40, heldout=True).X
+    Xh = synth.make("c3", n=2000, d=40, heldout=True).X
     out, dec = model.predict(Xh, decision=True)
     f = om.decision_function(Xh)
     assert np.abs(dec - f).max() <= 1e-3
-    assert _labels_agree(out, f, om.predict(Xh)) >= 0.99
+    assert _labels_agree(out, f, om.predict(Xh)) >= 0.999
     d_ora = sum(r["dual"] for r in om.results)
     assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
 
@@ -299,11 +300,11 @@ def test_ovr_batched_vs_oracle(n, d, k):
     info = model.info
     assert info.n_problem == k and info.batched == 1
     om = ora.train(ds.X, ds.y, gamma=1.0 / d)
-    Xh = synth.mnist_like(n=300, d=d, k=k, seed=103).X
+    Xh = synth.mnist_like(n=2000, d=d, k=k, seed=103).X
     out, dec = model.predict(Xh, decision=True)
     f = om.decision_function(Xh)
     assert np.abs(dec - f).max() <= 1e-3
-    assert _labels_agree(out, f, om.predict(Xh)) >= 0.99
+    assert _labels_agree(out, f, om.predict(Xh)) >= 0.999
     d_ora = sum(r["dual"] for r in om.results)
     assert abs(info.dual_objective - d_ora) <= 1e-4 * abs(d_ora)
     assert info.passes >= max(r["iterations"] for r in om.results) // 2 and info.pass_ms > 0

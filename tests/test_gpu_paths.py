@@ -1,0 +1,195 @@
+"""GPU parity of every launch configuration a BASELINE config takes, and of the multi-rank path.
+
+* One step from identical state (SURVEY 8(c) "Parity criteria"; north_star: "kernel rows and
+  gradient within 1e-5 relative") through each production variant of the persistent kernel:
+  X resident in shared memory, X streamed with 1 / 2 / 4 rows per thread (with and without the
+  per-lane cp.async ring), wide rows through the bulk-copy pipeline (d >= 256), feature slices,
+  CSR, and virtual ranks.  W must equal the oracle's exactly; G must equal the oracle's step 6
+  ("calculating the gradient for all dual space coefficients") applied to the GPU's own
+  dalpha within 1e-5 max(1, |G|).
+* The pass-only diagnostic (svm_solver_pass_bench) against the same step 6: one pass with a fixed
+  W through every row of the production launch.
+* Virtual ranks (SURVEY 8(e) invariant): P ranks inside one launch run the
+  multi-rank exchange (local merge, one 8+8 list per rank, owner-rank payload and row gathers)
+  and must reproduce the one-rank alpha, G and iteration count bit for bit.
+"""
+import os
+from contextlib import contextmanager
+
+import numpy as np
+import pytest
+
+import oracle as ora
+import paper_1706_05544_b200 as pkg
+from paper_1706_05544_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    pkg.lib()
+
+
+@contextmanager
+def env(**kw):
+    old = {k: os.environ.get(k) for k in kw}
+    try:
+        for k, v in kw.items():
+            os.environ[k] = str(v)
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _csr(X):
+    ip = np.concatenate([[0], np.cumsum((X != 0).sum(1))]).astype(np.int64)
+    return ip, np.nonzero(X)[1].astype(np.int32), X[X != 0].astype(np.float32)
+
+
+# (config, n, env, csr): every launch variant of smo_persistent that a BASELINE config takes
+PATHS = {
+    "xsmem": ("c1", 900, {}, False),                                   # c1 / c2: X in SMEM
+    "stream_rpt1": ("c1", 1300, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=1), False),
+    "stream_rpt2": ("c1", 1300, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=2), False),
+    "stream_rpt4": ("c4", 2600, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=4), False),  # c4
+    "stream_rpt4_noring": ("c4", 2600, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=4, SVMB200_XRING=0), False),
+    "stream_rpt4_nodbuf": ("c4", 2600, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=4, SVMB200_NO_DBUF=1), False),
+    "wide": ("c3", 1500, {}, False),                                   # c3 per class: bulk-copy ring
+    "slices": ("c3", 1500, dict(SVMB200_NO_WIDE=1), False),           # feature-slice fallback
+    "csr": ("c5", 3000, {}, True),                                     # c5: CSR staged pass
+    "svr_stream_rpt2": ("c2", 1300, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=2), False),
+}
+
+
+def _problem(cfg, n):
+    ds = synth.make(cfg, n=n)
+    X = ds.dense()
+    reg = ds.svm_type == synth.EPS_REGRESSION
+    y = ds.y if reg or cfg != "c3" else np.where(ds.y == ds.y[0], 1.0, -1.0).astype(np.float32)
+    svm_type = "eps-regression" if reg else "C-classification"
+    prob = ora.Problem(ora.EPS_REGRESSION if reg else ora.C_CLASSIFICATION, y, n, 0.1)
+    return ds, X, y, svm_type, prob
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_one_step_launch_paths(path):
+    cfg, n, ev, csr = PATHS[path]
+    ds, X, y, svm_type, prob = _problem(cfg, n)
+    gamma, C, tol = 1.0 / ds.d, 1.0, 1e-3
+    ks = ora.kspec("rbf", gamma, d=ds.d)
+    alpha, G = np.zeros(prob.m), prob.p.copy()
+    with env(**ev):
+        s = (pkg.Solver(csr=_csr(X), y=y, d=ds.d, svm_type=svm_type, gamma=gamma)
+             if csr else pkg.Solver(X, y, svm_type=svm_type, gamma=gamma))
+        done = 0
+        for steps in (0, 5, 30):
+            for _ in range(steps - done):
+                _, _, alpha, G = ora.step(X, prob, ks, alpha, G, C, q=16, tol=tol)
+            done = steps
+            G32 = G.astype(np.float32)
+            W = ora.select(prob, alpha, G32.astype(np.float64), C, 16)
+            s.set_state(alpha, G32)
+            st = s.run(1)
+            assert st.iterations == 1
+            np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+            dg = np.array(st.last_dalpha[:st.last_nw])
+            _, Gg = s.get_state()
+            Gref = ora.gradient_update(X, prob, ks, W, dg, G32.astype(np.float64))
+            err = np.abs(Gg - Gref) / np.maximum(1.0, np.abs(Gref))
+            assert err.max() <= 1e-5, (path, steps, err.max())
+
+
+@pytest.mark.parametrize("path", ["xsmem", "stream_rpt4", "stream_rpt2", "wide", "csr",
+                                  "svr_stream_rpt2"])
+def test_pass_only_diagnostic_matches_step6(path):
+    """svm_solver_pass_bench (the a3 diagnostic bench.py times) computes the oracle's step 6."""
+    cfg, n, ev, csr = PATHS[path]
+    ds, X, y, svm_type, prob = _problem(cfg, n)
+    gamma = 1.0 / ds.d
+    ks = ora.kspec("rbf", gamma, d=ds.d)
+    rows = np.array([3, 0, n - 1, n // 2, 17, 5, 11, n // 3, 40, 41, 42, 7, 8, 9, 99, 100])
+    coef = np.linspace(-0.9, 0.8, len(rows)).astype(np.float32)
+    with env(**ev):
+        s = (pkg.Solver(csr=_csr(X), y=y, d=ds.d, svm_type=svm_type, gamma=gamma)
+             if csr else pkg.Solver(X, y, svm_type=svm_type, gamma=gamma))
+        _, G0 = s.get_state()
+        ms = s.pass_bench(rows, coef, 1)
+        assert ms > 0
+        _, G1 = s.get_state()
+    # step 6 with W = the rows' positive copies (y_w = prob.y) and y_w dalpha_w = coef_w
+    W = rows.astype(np.int64)
+    dalpha = coef.astype(np.float64) * prob.y[W]
+    Gref = ora.gradient_update(X, prob, ks, W, dalpha, G0.astype(np.float64))
+    err = np.abs(G1 - Gref) / np.maximum(1.0, np.abs(Gref))
+    assert err.max() <= 1e-5, err.max()
+
+
+@pytest.mark.parametrize("case", [("c4", 36864, {}, False, "C-classification"),
+                                  ("c4", 36864, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=2), False,
+                                   "C-classification"),
+                                  ("c2", 18432, {}, False, "eps-regression"),
+                                  ("c5", 36864, {}, True, "C-classification")])
+def test_virtual_ranks_bit_identical(case):
+    """P in {2, 4, 8} virtual ranks (144 CTAs) == one rank with the same 144 CTAs, bit for bit."""
+    cfg, n, ev, csr, svm_type = case
+    ds = synth.make(cfg, n=n)
+    X = ds.dense()
+    with env(SVMB200_NBLK=144, **ev):
+        def solver():
+            kw = dict(svm_type=svm_type, gamma=1.0 / ds.d)
+            return (pkg.Solver(csr=(ds.indptr, ds.indices, ds.data), y=ds.y, d=ds.d, **kw)
+                    if csr else pkg.Solver(X, ds.y, **kw))
+        ref = solver()
+        assert ref.geometry()[0] == 144
+        r1 = ref.run(1000000)
+        assert r1.converged
+        a1, g1 = ref.get_state()
+        for P in (2, 4, 8):
+            s = solver()
+            s.set_ranks(P)
+            rp = s.run(1000000)
+            ap, gp = s.get_state()
+            assert rp.iterations == r1.iterations, (P, rp.iterations, r1.iterations)
+            np.testing.assert_array_equal(ap, a1)
+            np.testing.assert_array_equal(gp, g1)
+            assert (rp.m_up, rp.M_low) == (r1.m_up, r1.M_low)
+
+
+def test_virtual_ranks_one_step_vs_oracle():
+    """One step through the multi-rank exchange (virtual ranks) against the oracle's step."""
+    ds, X, y, svm_type, prob = _problem("c1", 2000)
+    gamma, C = 1.0 / ds.d, 1.0
+    ks = ora.kspec("rbf", gamma, d=ds.d)
+    alpha, G = np.zeros(prob.m), prob.p.copy()
+    for _ in range(9):
+        _, _, alpha, G = ora.step(X, prob, ks, alpha, G, C)
+    G32 = G.astype(np.float32)
+    W = ora.select(prob, alpha, G32.astype(np.float64), C, 16)
+    with env(SVMB200_NBLK=8):
+        for P in (2, 4, 8):
+            s = pkg.Solver(X, y, gamma=gamma)
+            s.set_ranks(P)
+            s.set_state(alpha, G32)
+            st = s.run(1)
+            np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+            _, Gg = s.get_state()
+            Gref = ora.gradient_update(X, prob, ks, W, np.array(st.last_dalpha[:st.last_nw]),
+                                       G32.astype(np.float64))
+            assert (np.abs(Gg - Gref) <= 1e-5 * np.maximum(1.0, np.abs(Gref))).all()
+
+
+def test_set_ranks_rejects_bad_counts():
+    ds = synth.make("c1", n=900)
+    with env(SVMB200_NBLK=4):
+        s = pkg.Solver(ds.X, ds.y, gamma=1.0 / ds.d)
+        for bad in (0, 3, 9):
+            with pytest.raises(pkg.SvmError):
+                s.set_ranks(bad)
