@@ -45,6 +45,7 @@ extern "C" {
 #define SVM_ECUDA (-5)        /* a CUDA runtime error (message carries cudaGetErrorString)     */
 #define SVM_EPEER (-6)        /* sharded run: peer-memory mapping / rank exchange failed       */
 #define SVM_ETIMEOUT (-7)     /* sharded run: a rank stopped publishing working-set candidates */
+#define SVM_ENCCL (-8)        /* svm_train_sharded*: NCCL could not be loaded or a call failed  */
 
 /* ---- enums (e1071 numbering) ------------------------------------------------------------- */
 #define SVM_C_CLASSIFICATION 0 /* e1071 type = "C-classification"  (P:75 item 1)            */
@@ -75,7 +76,7 @@ typedef struct svm_params {
     int32_t layout;      /* SVM_ROW_MAJOR | SVM_COL_MAJOR for dense X                           */
     int32_t certify;     /* after the loop, recompute G = Q a + p from the support vectors with
                             fp64 accumulation and resume if the violation exceeds tolerance:
-                            1 = always, 0 = never, -1 = auto (when n * n_SV * d <= 4e13)  */
+                            1 = always, 0 = never, -1 = auto (when n * n_SV * d <= 2e15)  */
     void* stream;        /* cudaStream_t, or NULL for the legacy default stream                 */
 } svm_params;
 
@@ -256,6 +257,22 @@ int svm_shard_handle(const svm_shard* sh, void* handle /* SVM_SHARD_HANDLE_BYTES
 int svm_shard_connect(svm_shard* sh, const void* all_handles /* world * HANDLE_BYTES */);
 int svm_shard_train(svm_shard* sh, svm_model** out);
 void svm_shard_free(svm_shard* sh);
+
+/* One-call sharded training: create + handle exchange + connect + train + free.
+ * nccl_unique_id: the 128-byte ncclUniqueId rank 0 obtained (svm_nccl_unique_id) and shared with
+ * every rank by the caller (e.g. torch.distributed.broadcast_object_list).  All `world` ranks call
+ * it collectively with the same id; the handles are all-gathered over a communicator created from
+ * the id (NCCL is loaded at first use: libnccl.so.2, the host framework's when one is loaded) and
+ * destroyed before returning.  Arguments and results as svm_shard_create* / svm_shard_train:
+ * every rank returns the identical model.  Errors: those of the shard API, SVM_ENCCL. */
+int svm_nccl_unique_id(void* id /* 128 bytes, out */);
+int svm_train_sharded(const float* X_local, int64_t n_local, int64_t d, int64_t row0,
+                      const float* y_global, int64_t n_global, int32_t rank, int32_t world,
+                      const void* nccl_unique_id, const svm_params* params, svm_model** out);
+int svm_train_sharded_csr(const int64_t* indptr, const int32_t* indices, const float* data,
+                          int64_t n_local, int64_t d, int64_t row0, const float* y_global,
+                          int64_t n_global, int32_t rank, int32_t world, const void* nccl_unique_id,
+                          const svm_params* params, svm_model** out);
 
 #ifdef __cplusplus
 }

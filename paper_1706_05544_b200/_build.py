@@ -13,8 +13,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build")
-LIB = os.path.join(PKG, "libsvmb200.so")
+# SVMB200_BUILD_TAG (diagnostic builds, e.g. the SMO_PROFILE one) puts objects and the library
+# under separate names (build_<tag>/, libsvmb200_<tag>.so) next to the product build;
+# binding.py loads it only when SVMB200_LIB names it
+_TAG = os.environ.get("SVMB200_BUILD_TAG", "")
+BUILD = os.path.join(ROOT, "build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, "libsvmb200" + (f"_{_TAG}" if _TAG else "") + ".so")
 SOURCES = ["smo.cu", "layout.cu", "predict.cu", "capi.cu"]
 HEADERS = ["svm_internal.cuh", "layout.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -14,10 +14,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsvmb200.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("SVMB200_LIB", "libsvmb200.so"))
 
 SVM_OK, SVM_EINVAL, SVM_EDEGENERATE, SVM_ENONFINITE = 0, -1, -2, -3
-SVM_ENOMEM, SVM_ECUDA, SVM_EPEER, SVM_ETIMEOUT = -4, -5, -6, -7
+SVM_ENOMEM, SVM_ECUDA, SVM_EPEER, SVM_ETIMEOUT, SVM_ENCCL = -4, -5, -6, -7, -8
 C_CLASSIFICATION, EPS_REGRESSION = 0, 3
 LINEAR, POLYNOMIAL, RADIAL, SIGMOID = 0, 1, 2, 3
 ROW_MAJOR, COL_MAJOR = 0, 1
@@ -103,6 +103,11 @@ SIGNATURES = {
     "svm_shard_connect": (ctypes.c_int, [_P, _P]),
     "svm_shard_train": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "svm_shard_free": (None, [_P]),
+    "svm_nccl_unique_id": (ctypes.c_int, [_P]),
+    "svm_train_sharded": (ctypes.c_int, [_P, _i64, _i64, _i64, _P, _i64, _i32, _i32, _P,
+                                         ctypes.POINTER(svm_params), ctypes.POINTER(_P)]),
+    "svm_train_sharded_csr": (ctypes.c_int, [_P, _P, _P, _i64, _i64, _i64, _P, _i64, _i32, _i32,
+                                             _P, ctypes.POINTER(svm_params), ctypes.POINTER(_P)]),
 }
 
 _lib = None
@@ -375,3 +380,38 @@ def train_sharded(X_local, row0: int, y_global, rank: int, world: int, all_gathe
     _check(lib().svm_shard_create(x.p, n_local, d, int(row0), yy.p, n_global, int(rank),
                                   int(world), ctypes.byref(p), ctypes.byref(sh)))
     return _shard_run(sh, world, all_gather_bytes)
+
+
+def nccl_unique_id() -> bytes:
+    """svm_nccl_unique_id: a fresh 128-byte ncclUniqueId (call on rank 0, share with all ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().svm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def train_sharded_nccl(X_local, row0: int, y_global, rank: int, world: int, nccl_id: bytes,
+                       layout=ROW_MAJOR, **kw) -> Model:
+    """svm_train_sharded: the one-call sharded training (handles exchanged over NCCL inside)."""
+    n_local, d = (int(X_local.shape[0]), int(X_local.shape[1])) if layout == ROW_MAJOR else \
+        (int(X_local.shape[1]), int(X_local.shape[0]))
+    p = params(d, layout=layout, **kw)
+    x, yy = _Arr(X_local, np.float32), _Arr(y_global, np.float32)
+    idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    h = ctypes.c_void_p()
+    _check(lib().svm_train_sharded(x.p, n_local, d, int(row0), yy.p, int(len(y_global)), int(rank),
+                                   int(world), idb, ctypes.byref(p), ctypes.byref(h)))
+    return Model(h.value)
+
+
+def train_sharded_nccl_csr(indptr, indices, data, d: int, row0: int, y_global, rank: int,
+                           world: int, nccl_id: bytes, **kw) -> Model:
+    """svm_train_sharded_csr: as train_sharded_nccl for this rank's CSR rows."""
+    p = params(int(d), **kw)
+    a, b, c = _Arr(indptr, np.int64), _Arr(indices, np.int32), _Arr(data, np.float32)
+    yy = _Arr(y_global, np.float32)
+    idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    h = ctypes.c_void_p()
+    _check(lib().svm_train_sharded_csr(a.p, b.p, c.p, int(len(indptr)) - 1, int(d), int(row0), yy.p,
+                                       int(len(y_global)), int(rank), int(world), idb,
+                                       ctypes.byref(p), ctypes.byref(h)))
+    return Model(h.value)

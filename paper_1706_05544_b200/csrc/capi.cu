@@ -7,6 +7,8 @@
 #include "../../include/svmb200.h"
 #include "layout.cuh"
 
+#include <dlfcn.h>
+
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -522,6 +524,40 @@ struct LoopMode {
     double* pass_ms = nullptr;          // out: device time of the pass-only launch
 };
 
+// TMA descriptor of X^T [d][n_pad] for the streamed dense pass: dim 0 = rows (contiguous), dim 1
+// = features; box = {32 rpt rows, d features} -- one chunk of a CTA per tensor copy.  The encoder
+// is the driver's cuTensorMapEncodeTiled, reached through the runtime (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled()
+{
+    static std::once_flag once;
+    static EncodeTiledFn fn = nullptr;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+static bool encode_x_map(CUtensorMap* map, const float* XT, int64_t n_pad, int64_t d, int rows)
+{
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn || d > 256 || rows > 256 || (n_pad * 4) % 16 != 0) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)n_pad, (cuuint64_t)d};
+    cuuint64_t strides[1] = {(cuuint64_t)n_pad * 4};
+    cuuint32_t box[2] = {(cuuint32_t)rows, (cuuint32_t)d};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(XT), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Virtual ranks (LoopMode::vranks = P): the launch's D.nblk CTAs form P ranks of D.nblk / P CTAs;
 // rank r owns rows [r nblk_r R, (r + 1) nblk_r R) (clipped to n) -- the same rows its CTAs own in a
 // one-rank launch, so alpha, G and the iteration count must be bit-identical to it.  Each virtual
@@ -586,6 +622,22 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         smem = smo_smem_bytes(D.d, a.world, a.nblk, 0) +
                (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
+        // dense rows of <= 256 features: the TMA ring (one tensor copy per 32 rpt-row chunk)
+        // (opt-in, SVMB200_TMA=1: measured slower than the per-lane ring on c4)
+        if (!D.csr && D.d < 256 && getenv("SVMB200_TMA") && atoi(getenv("SVMB200_TMA"))) {
+            const int64_t stage = D.d * 32 * a.rpt * 4;
+            const int base = smo_smem_bytes(D.d, a.world, a.nblk, 0) + 128;
+            int ns = 4;
+            if (const char* e = getenv("SVMB200_TMA_STAGES")) ns = std::max(2, std::min(8, atoi(e)));
+            while (ns > 2 && base + ns * stage > 150 * 1024) --ns;
+            if (base + ns * stage <= 200 * 1024 &&
+                encode_x_map(&a.xmap, D.XT.as<float>(), D.n_pad, D.d, 32 * a.rpt)) {
+                a.x_tma = 1;
+                a.tma_ns = ns;
+                a.x_ring = 0;
+                smem = base + (int)(ns * stage);
+            }
+        }
     }
     if (!a.x_in_smem && !D.csr && D.d >= 256 && a.rpt == 1 && D.rows_per_cta <= 14 * 32 &&
         !getenv("SVMB200_NO_WIDE")) {
@@ -614,7 +666,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         rows = rows / chunk * chunk;
         if (getenv("SVMB200_NO_DBUF") || a.wide) rows = 0;
         a.nslice = 1;
-        if (!a.x_in_smem && !D.csr && D.d >= 256 && rows == all_rows) {
+        if (!a.x_in_smem && !D.csr && !a.x_tma && D.d >= 256 && rows == all_rows) {
             // feature slices: as many as the partial buffers allow, >= 64 features each, aiming
             // at >= 4 items per warp
             const int64_t nch = all_rows / chunk;
@@ -654,6 +706,13 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     E.epoch += (uint32_t)info.iterations + 1;
     if (a.pass_only) {   // a diagnostic: the solver's iteration bookkeeping is not advanced
         if (M.pass_ms) *M.pass_ms = ms;
+        if (getenv("SVMB200_PROFILE")) {
+            const double it = (double)std::max<int64_t>(1, info.iterations);
+            fprintf(stderr, "[svmb200] pass-only %lld passes, %.3f ms: worker warp 0 (cycles/pass): B-dots %.0f "
+                    "B-epilogue %.0f B-merge %.0f B-tail %.0f finish %.0f\n", (long long)info.iterations, ms,
+                    info.phase_cycles[8] / it, info.phase_cycles[10] / it, info.phase_cycles[11] / it,
+                    info.phase_cycles[12] / it, info.phase_cycles[13] / it);
+        }
         if (info_out) *info_out = info;
         return SVM_OK;
     }
@@ -834,7 +893,9 @@ static bool want_certify(const svm_params* prm, int64_t n, int64_t nsv, int64_t 
 {
     if (prm->certify == 0) return false;
     if (prm->certify > 0) return true;
-    return (double)n * (double)nsv * (double)d <= 4e13;
+    // auto: every BASELINE config (c5: 2e6 x 9.4e5 SVs x 400 = 7.5e14, one fp16-split tcgen05
+    // decision pass of a few seconds against a ~100 s training); only far larger problems skip it
+    return (double)n * (double)nsv * (double)d <= 2e15;
 }
 
 // Certification (a4): recompute G = Q a + p from the support vectors with fp64 accumulation and
@@ -2011,11 +2072,25 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         P.max_iter = prm->max_iter > 0 ? prm->max_iter
                                        : std::max<int64_t>(10 * S->n_global * P.ncopy, 10000);
         TRY(run_loop(D, P, S->E, P.max_iter, S->st, nullptr, &S->sc));
-        for (int round = 0; round < 4 && P.converged && prm->certify != 0; ++round) {
+        for (int round = 0; P.converged && prm->certify != 0; ++round) {
+            if (prm->certify < 0) {   // auto rule of svm_train, on the global SV count
+                DBuf cf, fl, ix;
+                TRY(fl.alloc(D.n));
+                CK(cudaMemsetAsync(fl.p, 0, D.n, S->st));
+                TRY(problem_coef(D, P, cf, fl, S->st));
+                int64_t nloc = 0;
+                TRY(compact(fl, D.n, ix, &nloc, S->st));
+                std::vector<double> all;
+                TRY(shard_xchg(S, {(double)nloc}, all));
+                double nsv_g = 0;
+                for (double v : all) nsv_g += v;
+                if (!want_certify(prm, S->n_global, (int64_t)nsv_g, D.d)) break;
+            }
             double viol = 0;
             TRY(shard_certify(S, P, &viol));
-            if (viol <= P.tol) break;
+            if (viol <= P.tol) { P.converged = true; break; }
             P.converged = false;
+            if (round == SVM_MAX_RESUMES) break;
             P.tol_loop = std::min(P.tol_loop - 0.01 * P.tol, P.tol - resume_factor() * (viol - P.tol));
             int64_t left = P.max_iter - P.iterations;
             if (left <= 0) break;
@@ -2108,3 +2183,114 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
 }
 
 extern "C" void svm_shard_free(svm_shard* S) { delete S; }
+
+// ---- one-call sharded training over an NCCL communicator (SURVEY 8(b) svm_train_sharded) -----
+// NCCL is loaded on first use (dlopen of libnccl.so.2: the one the host framework already loaded
+// when there is one), so the library has no link-time NCCL dependency.  The communicator carries
+// the one setup exchange (the peer-mapping handles); the per-iteration exchange stays inside the
+// persistent kernel over NVLink peer memory.
+namespace {
+struct NcclApi {
+    typedef int (*GetUniqueId)(void*);
+    typedef int (*CommInitRank)(void**, int, const void* /* ncclUniqueId by value, 128 B */, int);
+    typedef int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t);
+    typedef int (*CommDestroy)(void*);
+    typedef const char* (*GetErrorString)(int);
+    bool ok = false;
+    GetUniqueId get_unique_id = nullptr;
+    void* comm_init_rank = nullptr;   // called through a by-value 128-byte struct signature
+    AllGather all_gather = nullptr;
+    CommDestroy comm_destroy = nullptr;
+    GetErrorString err = nullptr;
+};
+struct NcclId { char internal[128]; };
+typedef int (*CommInitRankFn)(void**, int, NcclId, int);
+const NcclApi& nccl_api()
+{
+    static std::once_flag once;
+    static NcclApi api;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.get_unique_id = (NcclApi::GetUniqueId)dlsym(h, "ncclGetUniqueId");
+        api.comm_init_rank = dlsym(h, "ncclCommInitRank");
+        api.all_gather = (NcclApi::AllGather)dlsym(h, "ncclAllGather");
+        api.comm_destroy = (NcclApi::CommDestroy)dlsym(h, "ncclCommDestroy");
+        api.err = (NcclApi::GetErrorString)dlsym(h, "ncclGetErrorString");
+        api.ok = api.get_unique_id && api.comm_init_rank && api.all_gather && api.comm_destroy && api.err;
+    });
+    return api;
+}
+constexpr int NCCL_INT8 = 0;   // ncclDataType_t ncclInt8 / ncclChar
+}  // namespace
+
+extern "C" int svm_nccl_unique_id(void* id)
+{
+    if (!id) return fail(SVM_EINVAL, "id is NULL");
+    const NcclApi& A = nccl_api();
+    if (!A.ok) return fail(SVM_ENCCL, "libnccl.so.2 could not be loaded");
+    int r = A.get_unique_id(id);
+    if (r != 0) return fail(SVM_ENCCL, "ncclGetUniqueId: %s", A.err(r));
+    return SVM_OK;
+}
+
+// All-gather of the SVM_SHARD_HANDLE_BYTES handle blobs over a fresh communicator, then
+// connect + train; the communicator is destroyed before returning.
+static int shard_run_nccl(svm_shard* S, const void* nccl_unique_id, svm_model** out)
+{
+    const NcclApi& A = nccl_api();
+    if (!A.ok) return fail(SVM_ENCCL, "libnccl.so.2 could not be loaded");
+    std::vector<char> mine(SVM_SHARD_HANDLE_BYTES), all((size_t)SVM_SHARD_HANDLE_BYTES * S->world);
+    TRY(svm_shard_handle(S, mine.data()));
+    NcclId id;
+    memcpy(id.internal, nccl_unique_id, sizeof id.internal);
+    void* comm = nullptr;
+    int r = reinterpret_cast<CommInitRankFn>(A.comm_init_rank)(&comm, S->world, id, S->rank);
+    if (r != 0) return fail(SVM_ENCCL, "ncclCommInitRank(rank %d of %d): %s", S->rank, S->world, A.err(r));
+    DBuf dsend, drecv;
+    int rc = SVM_OK;
+    if ((rc = dsend.alloc(mine.size())) == SVM_OK && (rc = drecv.alloc(all.size())) == SVM_OK) {
+        cudaMemcpyAsync(dsend.p, mine.data(), mine.size(), cudaMemcpyHostToDevice, S->st);
+        r = A.all_gather(dsend.p, drecv.p, mine.size(), NCCL_INT8, comm, S->st);
+        if (r != 0) rc = fail(SVM_ENCCL, "ncclAllGather: %s", A.err(r));
+        else {
+            cudaMemcpyAsync(all.data(), drecv.p, all.size(), cudaMemcpyDeviceToHost, S->st);
+            if (cudaStreamSynchronize(S->st) != cudaSuccess) rc = fail(SVM_ECUDA, "handle exchange failed");
+        }
+    }
+    A.comm_destroy(comm);
+    if (rc != SVM_OK) return rc;
+    TRY(svm_shard_connect(S, all.data()));
+    return svm_shard_train(S, out);
+}
+
+extern "C" int svm_train_sharded(const float* X_local, int64_t n_local, int64_t d, int64_t row0,
+                                 const float* y_global, int64_t n_global, int32_t rank,
+                                 int32_t world, const void* nccl_unique_id,
+                                 const svm_params* params, svm_model** out)
+{
+    if (!out || !nccl_unique_id) return fail(SVM_EINVAL, "out or nccl_unique_id is NULL");
+    *out = nullptr;
+    svm_shard* S = nullptr;
+    TRY(svm_shard_create(X_local, n_local, d, row0, y_global, n_global, rank, world, params, &S));
+    const int rc = shard_run_nccl(S, nccl_unique_id, out);
+    svm_shard_free(S);
+    return rc;
+}
+
+extern "C" int svm_train_sharded_csr(const int64_t* indptr, const int32_t* indices,
+                                     const float* data, int64_t n_local, int64_t d, int64_t row0,
+                                     const float* y_global, int64_t n_global, int32_t rank,
+                                     int32_t world, const void* nccl_unique_id,
+                                     const svm_params* params, svm_model** out)
+{
+    if (!out || !nccl_unique_id) return fail(SVM_EINVAL, "out or nccl_unique_id is NULL");
+    *out = nullptr;
+    svm_shard* S = nullptr;
+    TRY(svm_shard_create_csr(indptr, indices, data, n_local, d, row0, y_global, n_global, rank,
+                             world, params, &S));
+    const int rc = shard_run_nccl(S, nccl_unique_id, out);
+    svm_shard_free(S);
+    return rc;
+}

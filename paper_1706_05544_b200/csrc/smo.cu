@@ -151,6 +151,29 @@ __device__ __forceinline__ void fma_row16_masked(float x, const float4* w4k, uin
     }
 }
 
+// Four rows at once with packed FFMA2, W loaded one float4 (4 columns) at a time so that only 4 W
+// registers are live: acc[j][c] += x_j * w_c for j < 4, c < 16.  Per lane each FFMA2 half rounds
+// exactly like fmaf, so the sums are bit-identical to fma_row16_scalar / fma_row16.
+__device__ __forceinline__ void fma_rows4_x16(const float (&x)[4], const float4* w4k, float (&acc)[4][SVM_WS])
+{
+    float2 xx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xx[j] = make_float2(x[j], x[j]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 w = w4k[q];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 lo = __ffma2_rn(xx[j], make_float2(w.x, w.y), make_float2(acc[j][4 * q], acc[j][4 * q + 1]));
+            const float2 hi = __ffma2_rn(xx[j], make_float2(w.z, w.w), make_float2(acc[j][4 * q + 2], acc[j][4 * q + 3]));
+            acc[j][4 * q] = lo.x;
+            acc[j][4 * q + 1] = lo.y;
+            acc[j][4 * q + 2] = hi.x;
+            acc[j][4 * q + 3] = hi.y;
+        }
+    }
+}
+
 template <int RPT>
 __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64_t ld, int d,
                                            bool active, const float* sXW,
@@ -182,12 +205,15 @@ __device__ __forceinline__ void dots_dense(const float* __restrict__ xcol, int64
     }
 }
 
+#ifndef SMO_PF4
+#define SMO_PF4 8    // features in flight per lane at 4 rows per thread (64 B each; 16 measured slower)
+#endif
 // Streamed X (global): each lane keeps a private ring of PF_X feature slots in shared memory,
 // filled by cp.async (one commit group per feature), so PF_X features of its rows are in flight
 // without holding registers -- with 64 accumulators per thread ptxas keeps only ~2 plain loads
 // in flight, which left the streamed pass latency-bound.
 template <int RPT>
-__host__ __device__ constexpr int pf_x() { return RPT == 1 ? 16 : 8; }  // ~1-2 KB of X in flight per warp
+__host__ __device__ constexpr int pf_x() { return RPT == 1 ? 16 : (RPT == 4 ? SMO_PF4 : 8); }  // X in flight per warp: 2-8 KB
 template <int RPT>
 __device__ __forceinline__ void cp_async_x(uint32_t dst, const float* src)
 {
@@ -203,6 +229,35 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int RPT>
+__device__ __forceinline__ void x_fma_slot(uint32_t sa, const float4* w4k, float (&acc)[RPT][SVM_WS])
+{
+    float x[RPT];
+    if constexpr (RPT == 4) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sa) : "memory");
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else if constexpr (RPT == 2) {
+        float2 v;
+        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sa) : "memory");
+        x[0] = v.x; x[1] = v.y;
+    } else {
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(sa) : "memory");
+    }
+    if constexpr (RPT == 4) {
+        fma_rows4_x16(x, w4k, acc);
+    } else {
+        float4 wv[4] = {w4k[0], w4k[1], w4k[2], w4k[3]};
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) fma_row16(x[j], wv, acc[j]);
+    }
+}
+
+// Streamed X: feature k of the lane's rows sits in ring slot k mod PF_X (one cp.async commit group
+// per feature, PF_X features in flight).  Features [0, d - PF_X) refill their slot with feature
+// k + PF_X; the main part runs in blocks of PF_X with compile-time slot offsets and the source
+// pointer advanced by ld (no index arithmetic on the FMA path).
+template <int RPT>
 __device__ __forceinline__ void dots_dense_async(const float* __restrict__ xcol, int64_t ld, int d,
                                                  bool active, const float* sXW, uint32_t ring,
                                                  float (&acc)[RPT][SVM_WS])
@@ -212,39 +267,68 @@ __device__ __forceinline__ void dots_dense_async(const float* __restrict__ xcol,
     constexpr uint32_t SLOT = 32u * 4u * RPT;  // bytes per slot across the warp
     constexpr int PF_X = pf_x<RPT>();
     const float4* w4 = reinterpret_cast<const float4*>(sXW);
+    const float* src = xcol;
 #pragma unroll
     for (int f = 0; f < PF_X; ++f) {
-        if (f < d) cp_async_x<RPT>(ring + f * SLOT, xcol + (int64_t)f * ld);
+        if (f < d) cp_async_x<RPT>(ring + f * SLOT, src);
+        src += ld;
         cp_async_commit();
     }
+    int k = 0;
+    for (; k + 2 * PF_X <= d; k += PF_X) {   // every feature of the block refills its slot
+#pragma unroll
+        for (int u = 0; u < PF_X; ++u) {
+            cp_async_wait<PF_X - 1>();
+            x_fma_slot<RPT>(ring + u * SLOT, w4 + 4 * (k + u), acc);
+            cp_async_x<RPT>(ring + u * SLOT, src);
+            src += ld;
+            cp_async_commit();
+        }
+    }
 #pragma unroll 2
-    for (int k = 0; k < d; ++k) {
+    for (; k < d; ++k) {   // the last < 2 PF_X features: refill while features remain
         cp_async_wait<PF_X - 1>();
         const uint32_t sa = ring + (uint32_t)(k & (PF_X - 1)) * SLOT;
+        x_fma_slot<RPT>(sa, w4 + 4 * k, acc);
+        if (k + PF_X < d) {
+            cp_async_x<RPT>(sa, src);
+            src += ld;
+        }
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+}
+
+// Dense kernel-row dot products from a TMA-staged chunk tile [d][CH] (CH = 32 RPT rows, lane l
+// owns rows RPT l .. RPT l + RPT - 1): one conflict-free LDS per feature for the lane's rows plus
+// the 4 broadcast LDS.128 of X_W, then 16 RPT FMAs (the same order as dots_dense: bit-identical).
+template <int RPT>
+__device__ __forceinline__ void dots_tile(const float* tile, int d, int lane, const float* sXW,
+                                          float (&acc)[RPT][SVM_WS])
+{
+    zero_acc<RPT>(acc);
+    constexpr int CH = 32 * RPT;
+    const float* p = tile + lane * RPT;
+    const float4* w4 = reinterpret_cast<const float4*>(sXW);
+#pragma unroll 4
+    for (int k = 0; k < d; ++k) {
         float x[RPT];
         if constexpr (RPT == 4) {
-            float4 v;
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sa) : "memory");
+            const float4 v = *reinterpret_cast<const float4*>(p + k * CH);
             x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
         } else if constexpr (RPT == 2) {
-            float2 v;
-            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sa) : "memory");
+            const float2 v = *reinterpret_cast<const float2*>(p + k * CH);
             x[0] = v.x; x[1] = v.y;
         } else {
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(sa) : "memory");
+            x[0] = p[k * CH];
         }
         float4 wv[4] = {w4[4 * k], w4[4 * k + 1], w4[4 * k + 2], w4[4 * k + 3]};
 #pragma unroll
         for (int j = 0; j < RPT; ++j) {
-            if constexpr (RPT == 4) fma_row16_scalar(x[j], wv, acc[j]);   // pairs would spill
+            if constexpr (RPT == 4) fma_row16_scalar(x[j], wv, acc[j]);
             else fma_row16(x[j], wv, acc[j]);
         }
-        // refill the slot just consumed with feature k + PF_X
-        if (k + PF_X < d) cp_async_x<RPT>(sa, xcol + (int64_t)(k + PF_X) * ld);
-        cp_async_commit();
     }
-    cp_async_wait<0>();
 }
 
 // CSR kernel-row dot products for one row: sum over its nnz of v * X_W^T[col][r].
@@ -344,7 +428,8 @@ struct SmoShared {
     uint64_t rk_key[2][SVM_MAX_RANKS * 8];   // rank level: [side][rank * 8 + position]
     int32_t rk_src[2][SVM_MAX_RANKS * 8];
     int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
-    alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode pipeline barriers
+    alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode / TMA-ring pipeline barriers
+    uint64_t tma_seq[8];                 // TMA ring: chunk sequence number last issued into each slot
     double m_up, M_low;
 };
 
@@ -785,8 +870,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// 2D tensor copy (TMA) of one box of the map into shared memory, completing on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+                   "r"(smem_u32(bar)) : "memory");
+}
+
 template <bool CSR, int RPT, bool XS, bool RBFK>
-__global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a)
+__global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_constant__ SmoArgs a)
 {
     extern __shared__ __align__(16) unsigned char dyn_smem[];
     __shared__ SmoShared sh;
@@ -806,7 +900,15 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
     // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
     float* csr_val = sX + (size_t)warp * CSR_CAP;                                   // CSR only
     uint16_t* csr_idx = reinterpret_cast<uint16_t*>(sX + (size_t)SMO_WARPS * CSR_CAP) + (size_t)warp * CSR_CAP;
-    float* sDot = sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
+    // TMA ring (streamed dense X, a.x_tma): tma_ns slots of [d][32 RPT] fp32, 128-byte aligned
+    constexpr bool TMA_OK = !CSR && !XS;
+    const bool tma = TMA_OK && a.x_tma != 0;
+    const int NS = tma ? a.tma_ns : 1;
+    constexpr int CH = 32 * RPT;
+    float* tring = reinterpret_cast<float*>(dyn_smem + ((smem_u32(sX) + 127u) & ~127u) - smem_u32(dyn_smem));
+    const uint32_t stage_floats = (uint32_t)d * CH;
+    float* sDot = tma ? tring + (size_t)NS * stage_floats
+                      : sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
     const int64_t cta_begin = (int64_t)v.cta * a.rows_per_cta;
@@ -872,6 +974,46 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         __syncthreads();
         if (warp == ncw && lane == 0)
             for (int T = 0; T < WIDE_STAGES; ++T) wide_issue((uint64_t)T);
+    }
+
+    // ---- TMA ring for streamed dense X (a.x_tma): chunk sequence T = t * nchunks + j -----------
+    // slot T % NS holds chunk j = T % nchunks ([d][CH] rows cta_begin + j CH ..).  The consumer of
+    // T refills the slot with T + NS once its warp has read it; a consumer of T first waits until
+    // the slot's sequence number says T was issued (so the mbarrier is in T's phase), then on the
+    // phase parity (T / NS) & 1.  Chunks are consumed in increasing j within each iteration
+    // (phase A hands out 0, 1, ..; phase B the rest), so the ring runs ahead across iterations.
+    const uint32_t stage_bytes = stage_floats * 4u;
+    const int map_row0 = (int)((a.virt ? v.row0 : 0) + cta_begin);
+    auto tma_issue = [&](uint64_t T) {      // one thread
+        const int s = (int)(T % (uint64_t)NS);
+        const int j = (int)(T % (uint64_t)nchunks);
+        mbar_arrive_tx(&sh.mb_full[s], stage_bytes);
+        tma_load_2d(tring + (size_t)s * stage_floats, &a.xmap, map_row0 + j * CH, 0, &sh.mb_full[s]);
+        *reinterpret_cast<volatile uint64_t*>(&sh.tma_seq[s]) = T;
+    };
+    auto tma_acquire = [&](uint64_t T) -> const float* {   // whole warp
+        const int s = (int)(T % (uint64_t)NS);
+        if (lane == 0)
+            while (*reinterpret_cast<volatile uint64_t*>(&sh.tma_seq[s]) != T) {}
+        __syncwarp();
+        mbar_wait(&sh.mb_full[s], (uint32_t)((T / (uint64_t)NS) & 1));
+        return tring + (size_t)s * stage_floats;
+    };
+    auto tma_release = [&](uint64_t T) {   // whole warp, after its reads of T's slot
+        __syncwarp();
+        if (lane == 0) tma_issue(T + (uint64_t)NS);
+    };
+    if (tma) {
+        if (tid == 0) {
+            for (int s = 0; s < NS; ++s) {
+                mbar_init(&sh.mb_full[s], 1);
+                sh.tma_seq[s] = ~0ull;
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0 && nchunks > 0)
+            for (int T = 0; T < NS; ++T) tma_issue((uint64_t)T);
     }
 
     // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
@@ -980,6 +1122,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
             if (wide && warp == ncw && lane == 0)
                 for (uint64_t T = (uint64_t)t * nst; T < (uint64_t)t * nst + WIDE_STAGES; ++T)
                     mbar_wait(&sh.mb_full[T % WIDE_STAGES], (uint32_t)((T / WIDE_STAGES) & 1));
+            if (tma && tid == 0 && nchunks > 0)   // the NS chunks issued ahead for iteration t
+                for (uint64_t T = (uint64_t)t * nchunks; T < (uint64_t)t * nchunks + NS; ++T) {
+                    const int s = (int)(T % (uint64_t)NS);
+                    while (*reinterpret_cast<volatile uint64_t*>(&sh.tma_seq[s]) != T) {}
+                    mbar_wait(&sh.mb_full[s], (uint32_t)((T / (uint64_t)NS) & 1));
+                }
         };
         if (a.pass_only) {
             // ---- pass-only diagnostic: fixed W (local rows of a single rank), fixed c ----------
@@ -989,6 +1137,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                     a.info->iterations = t;
                     atomicAdd(reinterpret_cast<unsigned long long*>(&a.info->loop_cycles), (unsigned long long)clock64());
                 }
+#ifdef SMO_PROFILE
+                if (reporter && tid == SOLVER_WARP * 32)
+                    for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[ph] = prof[ph];
+                if (reporter && tid == 0)
+                    for (int ph = 0; ph < 8; ++ph) a.info->phase_cycles[8 + ph] = wprof[ph];
+#endif
                 return;
             }
             if (tid == 0) {
@@ -1411,6 +1565,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                else if (tma) {
+                    const uint64_t T = (uint64_t)t * nchunks + ch;
+                    dots_tile<RPT>(tma_acquire(T), d, lane, sXW, acc);
+                    tma_release(T);
+                }
                 else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, acc);
                 else dots_dense_async<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, xring, acc);
                 const int lr = (int)(li0 - cta_begin);
@@ -1517,11 +1676,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
         const int nA = nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf);
         const int nS = nchunks - nA;
         for (;;) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(&sh.next_chunk2, 1);
-            t = __shfl_sync(FULL, t, 0);
-            if (t >= nchunks) break;
-            const int ch = t < nS ? nA + t : t - nS;
+            int tk = 0;
+            if (lane == 0) tk = atomicAdd(&sh.next_chunk2, 1);
+            tk = __shfl_sync(FULL, tk, 0);
+            if (tk >= nchunks) break;
+            const int ch = tk < nS ? nA + tk : tk - nS;
             const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             float acc[RPT][SVM_WS];
             if (ch < nA) {
@@ -1548,6 +1707,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const SmoArgs a
                 }
             } else if constexpr (CSR) {
                 dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+            } else if (tma) {
+                const uint64_t T = (uint64_t)t * nchunks + ch;
+                dots_tile<RPT>(tma_acquire(T), d, lane, sXW, acc);
+                tma_release(T);
             } else if (XS || !a.x_ring) {
                 dots_dense<RPT>(xbase + (li0 - cta_begin), xld, d, li0 < cta_end, sXW, acc);
             } else {

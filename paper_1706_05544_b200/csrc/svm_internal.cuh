@@ -6,6 +6,7 @@
 // (P:59-69).  Layout and kernel design are in DESIGN.md.
 #pragma once
 
+#include <cuda.h>   // CUtensorMap (the TMA descriptor type; encoded through the runtime's driver entry point)
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -200,6 +201,13 @@ struct SmoArgs {
     int32_t pass_only, pass_nr;
     const int64_t* pass_rows;
     const float* pass_c;
+    // streamed dense X through the TMA engine (x_tma = 1): chunk j of a CTA (32 RPT rows x all d
+    // features of X^T) is one 2D tensor copy (boxes of <= 256 features) into a tma_ns-slot
+    // mbarrier ring; the warp that consumes chunk T refills its slot with chunk T + tma_ns (the ring
+    // runs ahead across iterations: X does not depend on W).  xmap: 2D map over X^T [d][n_pad]
+    // (dim 0 = rows, contiguous), box {32 RPT, min(d, 256)}.
+    int32_t x_tma, tma_ns;
+    alignas(64) CUtensorMap xmap;
 };
 
 // Batched one-vs-rest: P <= 16 binary problems on the same dense X, one X pass per

@@ -193,3 +193,24 @@ def test_set_ranks_rejects_bad_counts():
         for bad in (0, 3, 9):
             with pytest.raises(pkg.SvmError):
                 s.set_ranks(bad)
+
+
+def test_train_sharded_one_call_world1():
+    """svm_train_sharded: the handle exchange over a one-rank NCCL communicator,
+    then the shard path -- the same model as svm_train (same CTA partition: bit-identical)."""
+    from paper_1706_05544_b200 import binding
+    ds = synth.make("c1", n=3000)
+    m1 = pkg.train(ds.X, ds.y, gamma=1.0 / ds.d)
+    uid = binding.nccl_unique_id()
+    assert len(uid) == 128
+    ms = binding.train_sharded_nccl(ds.X, 0, ds.y, 0, 1, uid, gamma=1.0 / ds.d)
+    i1, c1 = m1.support()
+    i2, c2 = ms.support()
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(c1, c2)
+    assert ms.info.iterations == m1.info.iterations
+    dsc = synth.make("c5", n=4000)
+    mc1 = pkg.train_csr(dsc.indptr, dsc.indices, dsc.data, dsc.y, dsc.d, gamma=1.0 / dsc.d)
+    mc2 = binding.train_sharded_nccl_csr(dsc.indptr, dsc.indices, dsc.data, dsc.d, 0, dsc.y, 0, 1,
+                                         binding.nccl_unique_id(), gamma=1.0 / dsc.d)
+    np.testing.assert_array_equal(mc1.support()[1], mc2.support()[1])
