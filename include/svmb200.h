@@ -166,6 +166,37 @@ const char* svm_last_error(void);
  * reports the launches inside its timed region from the difference of two calls). */
 int64_t svm_launch_count(void);
 
+/* ---- K-fold cross validation over a (gamma, C) grid ---------
+ * For every grid cell g (gammas[g], costs[g]; NULL arrays = params' value) and fold f, the model of
+ * the training split (rows with fold[i] != f) is trained exactly as svm_train would train it on
+ * those rows (same label map from ALL of y, same one-vs-rest split for k > 2 classes) and
+ * evaluated on the held-out rows.  All problems share one device copy of X: held-out rows leave a
+ * problem through their status, classification problems run 16 at a time through the batched
+ * tcgen05 pass (one X pass per iteration for all of them, per-problem gamma and C), eps-SVR ones
+ * on the persistent kernel.  The held-out decision values come from the certified G (recomputed
+ * from the fold model's support vectors, fp64 sums).
+ *   fold: int32[n] fold id in [0, nfold) per row (host or device), or NULL for i mod nfold.
+ *   results: [ngrid] -- metric = mean accuracy (classification) or mean MSE (regression) over the
+ *            folds that did not fail (a training split with one class fails), pearson =
+ *            mean Pearson correlation (regression; NaN when undefined), plus the cell's gamma, C,
+ *            total iterations and whether every fold problem converged.
+ *   cv_decision: optional fp64 [ngrid][n][n_problem] (host or device): each row's decision value
+ *            from the model of the fold that held it out (n_problem = k for one-vs-rest, else 1).
+ * Errors: those of svm_train, SVM_EINVAL (nfold outside [2, n], a fold id out of range, an empty
+ * fold, ngrid < 1, a non-positive gamma or C). */
+typedef struct svm_cv_result {
+    int32_t nfold, failed;   /* folds; folds whose training split had a single class            */
+    double metric;           /* mean accuracy (classification) or MSE (regression)              */
+    double pearson;          /* regression: mean Pearson correlation; 0 for classification       */
+    double gamma, cost;      /* the grid cell                                                     */
+    int64_t iterations;      /* outer iterations summed over the cell's problems                  */
+    int32_t converged;       /* 1 if every problem of the cell converged                          */
+} svm_cv_result;
+int svm_cross_validate(const float* X, const float* y, int64_t n, int64_t d,
+                       const svm_params* params, int32_t nfold, const int32_t* fold,
+                       int32_t ngrid, const double* gammas, const double* costs,
+                       svm_cv_result* results, double* cv_decision);
+
 /* ---- solver-state API: one binary problem, stepwise (parity tests and drivers) -------------
  * A solver owns the device state of one Eq. 2 instance built from (X, y, params) exactly as
  * svm_train builds it (labels: binary only -- exactly two classes, mapped as svm_train maps them).

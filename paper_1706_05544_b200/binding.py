@@ -66,6 +66,12 @@ class svm_solver_stats(ctypes.Structure):
                 ("loop_ms", ctypes.c_double)]
 
 
+class svm_cv_result(ctypes.Structure):
+    _fields_ = [("nfold", ctypes.c_int32), ("failed", ctypes.c_int32), ("metric", ctypes.c_double),
+                ("pearson", ctypes.c_double), ("gamma", ctypes.c_double), ("cost", ctypes.c_double),
+                ("iterations", ctypes.c_int64), ("converged", ctypes.c_int32)]
+
+
 # name -> (restype, argtypes); the names are exactly those of include/svmb200.h
 _P = ctypes.c_void_p
 _i64, _i32 = ctypes.c_int64, ctypes.c_int32
@@ -104,6 +110,8 @@ SIGNATURES = {
     "svm_shard_train": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "svm_shard_free": (None, [_P]),
     "svm_nccl_unique_id": (ctypes.c_int, [_P]),
+    "svm_cross_validate": (ctypes.c_int, [_P, _P, _i64, _i64, ctypes.POINTER(svm_params), _i32, _P,
+                                          _i32, _P, _P, ctypes.POINTER(svm_cv_result), _P]),
     "svm_train_sharded": (ctypes.c_int, [_P, _i64, _i64, _i64, _P, _i64, _i32, _i32, _P,
                                          ctypes.POINTER(svm_params), ctypes.POINTER(_P)]),
     "svm_train_sharded_csr": (ctypes.c_int, [_P, _P, _P, _i64, _i64, _i64, _P, _i64, _i32, _i32,
@@ -415,3 +423,51 @@ def train_sharded_nccl_csr(indptr, indices, data, d: int, row0: int, y_global, r
                                        int(len(y_global)), int(rank), int(world), idb,
                                        ctypes.byref(p), ctypes.byref(h)))
     return Model(h.value)
+
+
+def kfold_split(n: int, k: int, seed: int = 0, labels=None) -> np.ndarray:
+    """Fold id per row (host plumbing, SPEC kfold_split): a seeded shuffle, then round-robin
+    assignment; with labels, the round robin runs per class (stratified)."""
+    if not (2 <= k <= n):
+        raise ValueError("need 2 <= k <= n")
+    rng = np.random.default_rng(seed)
+    fold = np.empty(n, np.int32)
+    if labels is None:
+        perm = rng.permutation(n)
+        fold[perm] = np.arange(n) % k
+        return fold
+    labels = np.asarray(labels)
+    start = 0
+    for c in dict.fromkeys(labels.tolist()):
+        idx = np.nonzero(labels == c)[0]
+        perm = idx[rng.permutation(idx.size)]
+        fold[perm] = (np.arange(idx.size) + start) % k
+        start += idx.size
+    return fold
+
+
+def cross_validate(X, y, nfold: int, fold=None, gammas=None, costs=None, decision=False, **kw):
+    """svm_cross_validate: K-fold CV over a (gamma, C) grid on one device copy of X.
+    Returns a list of per-cell dicts and, if decision, the held-out decision values
+    [ngrid, n, n_problem]."""
+    n, d = int(X.shape[0]), int(X.shape[1])
+    p = params(d, **kw)
+    ng = max(len(gammas) if gammas is not None else 1, len(costs) if costs is not None else 1)
+    g = None if gammas is None else np.ascontiguousarray(np.broadcast_to(gammas, (ng,)), np.float64)
+    c = None if costs is None else np.ascontiguousarray(np.broadcast_to(costs, (ng,)), np.float64)
+    x, yy = _Arr(X, np.float32), _Arr(y, np.float32)
+    fo = None if fold is None else _Arr(fold, np.int32)
+    res = (svm_cv_result * ng)()
+    yv = np.asarray(y.cpu().numpy() if hasattr(y, "cpu") else y)
+    nprob = 1
+    if p.type == C_CLASSIFICATION:
+        ncls = len(set(yv.tolist()))
+        nprob = ncls if ncls > 2 else 1
+    dec = np.empty((ng, n, nprob), np.float64) if decision else None
+    _check(lib().svm_cross_validate(x.p, yy.p, n, d, ctypes.byref(p), int(nfold),
+                                    fo.p if fo is not None else None, ng,
+                                    g.ctypes.data_as(_P) if g is not None else None,
+                                    c.ctypes.data_as(_P) if c is not None else None, res,
+                                    dec.ctypes.data_as(_P) if dec is not None else None))
+    out = [{f: getattr(r, f) for f, _ in svm_cv_result._fields_} for r in res]
+    return (out, dec) if decision else out

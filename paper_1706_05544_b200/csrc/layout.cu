@@ -145,6 +145,23 @@ __global__ void k_status_from_alpha(const double* __restrict__ alpha, int64_t n,
     }
 }
 
+// Cross-validation folds: rows whose fold id equals `held` leave the problem.
+// Their status gets both bound bits (alpha = 0 and alpha = C at once, which no live variable can
+// have), so they are in neither I_up nor I_low: never selected, alpha stays 0, and they add
+// nothing to Q alpha, the bias, the dual or the model -- the Eq. 2 instance of the training split.
+// G keeps being updated for them, so after certification y_i (G_i - p_i) is the fold model's
+// decision value (without b) on the held-out row.
+__global__ void k_exclude_fold(const int32_t* __restrict__ fold, int32_t held, int64_t n,
+                               int64_t n_pad, int ncopy, uint8_t* __restrict__ status)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || fold[i] != held) return;
+    for (int c = 0; c < ncopy; ++c) {
+        const int64_t idx = (int64_t)c * n_pad + i;
+        status[idx] = (uint8_t)((status[idx] & ST_YPOS) | ST_LOW | ST_UPP);
+    }
+}
+
 // copy-major device state <-> dual-indexed host order (dual (c,i) <-> c*n + i)
 __global__ void k_pack_state(const double* __restrict__ alpha, const float* __restrict__ G,
                              int64_t n, int64_t n_pad, int ncopy, double* __restrict__ a_out,
@@ -455,6 +472,13 @@ cudaError_t lay_status_from_alpha(const double* alpha, int64_t n, int64_t n_pad,
 {
     svm_note_launches(1);
     k_status_from_alpha<<<nblocks(n, 256), 256, 0, st>>>(alpha, n, n_pad, ncopy, C, status);
+    return cudaGetLastError();
+}
+cudaError_t lay_exclude_fold(const int32_t* fold, int32_t held, int64_t n, int64_t n_pad,
+                             int ncopy, uint8_t* status, cudaStream_t st)
+{
+    svm_note_launches(1);
+    k_exclude_fold<<<nblocks(n, 256), 256, 0, st>>>(fold, held, n, n_pad, ncopy, status);
     return cudaGetLastError();
 }
 cudaError_t lay_pack_state(const double* alpha, const float* G, int64_t n, int64_t n_pad,

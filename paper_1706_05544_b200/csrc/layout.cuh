@@ -20,6 +20,8 @@ cudaError_t lay_norms_csr(const int64_t* indptr, const float* vals, int64_t n, i
                           float* xnorm, cudaStream_t st);
 cudaError_t lay_init_state(const float* yv, int64_t n, int64_t n_pad, int ncopy, double eps,
                            double C, double* alpha, float* G, uint8_t* status, cudaStream_t st);
+cudaError_t lay_exclude_fold(const int32_t* fold, int32_t held, int64_t n, int64_t n_pad,
+                             int ncopy, uint8_t* status, cudaStream_t st);
 cudaError_t lay_status_from_alpha(const double* alpha, int64_t n, int64_t n_pad, int ncopy,
                                   double C, uint8_t* status, cudaStream_t st);
 cudaError_t lay_pack_state(const double* alpha, const float* G, int64_t n, int64_t n_pad,

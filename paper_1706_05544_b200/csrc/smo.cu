@@ -914,8 +914,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     const int64_t cta_begin = (int64_t)v.cta * a.rows_per_cta;
     const int64_t cta_end = min(cta_begin + a.rows_per_cta, v.n_local);
     const int nvalid = cta_end > cta_begin ? (int)(cta_end - cta_begin) : 0;
-    const int rows_per_chunk = 32 * RPT;
+    // rows per chunk (work item of one warp): 32 RPT, or fewer (a.chunk_rows, a multiple of 4)
+    // so that the chunk count is a multiple of the warp count and every warp gets the same
+    // number of chunks; lanes beyond the chunk's rows idle (lane_on)
+    const int rows_per_chunk = (a.chunk_rows > 0 && a.chunk_rows < 32 * RPT) ? a.chunk_rows : 32 * RPT;
     const int nchunks = (nvalid + rows_per_chunk - 1) / rows_per_chunk;
+    const bool lane_on = lane * RPT < rows_per_chunk;
     const int slot = v.cta;
     const bool sys = a.world > 1 && !a.virt;   // peers across NVLink: system scope
     const bool reporter = blockIdx.x == 0;  // CTA 0 of every rank reports for its rank
@@ -1063,7 +1067,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         float acc[RPT][SVM_WS];
         zero_acc<RPT>(acc);
         for (int ch = warp; ch < nchunks; ch += SMO_WARPS) {
-            const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+            const int64_t li0 = lane_on ? cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT : cta_end;
             uint64_t ku[2 * RPT], kl[2 * RPT];
             row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, false, acc, ku, kl);
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
@@ -1391,6 +1395,35 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             }
         }
         __syncthreads();
+        if (a.cache_slots > 0 && reporter && tid == 0 && !sh.stop) {   // cache dry run (stats)
+            const int nsets = a.cache_slots / 4;
+            int hits = 0;
+            bool used[4 * SVM_WS];
+            for (int q = 0; q < 4 * SVM_WS; ++q) used[q] = false;
+            int way_of[SVM_WS];
+            for (int r = 0; r < sh.nr; ++r) {
+                const int64_t row = sh.r_row[r];
+                const int set = (int)(row % nsets);
+                way_of[r] = -1;
+                for (int w = 0; w < 4; ++w)
+                    if (a.cache_tag[set * 4 + w] == (int32_t)row) way_of[r] = w;
+                if (way_of[r] >= 0) { ++hits; a.cache_stamp[set * 4 + way_of[r]] = (uint32_t)(t + 1); }
+            }
+            for (int r = 0; r < sh.nr; ++r) {
+                if (way_of[r] >= 0) continue;
+                const int64_t row = sh.r_row[r];
+                const int set = (int)(row % nsets);
+                int best = 0;
+                for (int w = 1; w < 4; ++w)
+                    if (a.cache_stamp[set * 4 + w] < a.cache_stamp[set * 4 + best]) best = w;
+                a.cache_tag[set * 4 + best] = (int32_t)row;
+                a.cache_stamp[set * 4 + best] = (uint32_t)(t + 1);
+            }
+            a.info->cache_lookups += sh.nr;
+            a.info->cache_hits += hits;
+            a.info->cache_allhit += (hits == sh.nr) ? 1 : 0;
+            (void)used;
+        }
         mark(1);
         if (sh.stop) {
             drain_wide();
@@ -1562,7 +1595,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 if (it >= nitems) break;
                 const int ch = nsl > 1 ? it / nsl : it, sl = nsl > 1 ? it - ch * nsl : 0;
                 const int k0 = sl * ks, kn = min(d, k0 + ks) - k0;
-                const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                const int64_t lrow = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+                const int64_t li0 = lane_on ? lrow : cta_end;   // idle lanes: past the CTA's rows
                 float acc[RPT][SVM_WS];
                 if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
                 else if (tma) {
@@ -1572,9 +1606,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 }
                 else if (XS || !a.x_ring) dots_dense<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, acc);
                 else dots_dense_async<RPT>(xbase + (li0 - cta_begin) + (int64_t)k0 * xld, xld, kn, li0 < cta_end, sXW + k0 * SVM_WS, xring, acc);
-                const int lr = (int)(li0 - cta_begin);
+                const int lr = (int)(lrow - cta_begin);
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {
+                    if (!lane_on) break;
                     float* dst = sDot + (size_t)(sl * SVM_WS + r) * dbuf_rows + lr;
                     if constexpr (RPT == 4) *reinterpret_cast<float4*>(dst) = make_float4(acc[0][r], acc[1][r], acc[2][r], acc[3][r]);
                     else if constexpr (RPT == 2) *reinterpret_cast<float2*>(dst) = make_float2(acc[0][r], acc[1][r]);
@@ -1681,19 +1716,20 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             tk = __shfl_sync(FULL, tk, 0);
             if (tk >= nchunks) break;
             const int ch = tk < nS ? nA + tk : tk - nS;
-            const int64_t li0 = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+            const int64_t lrow = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
+            const int64_t li0 = lane_on ? lrow : cta_end;   // idle lanes: past the CTA's rows
             float acc[RPT][SVM_WS];
             if (ch < nA) {
-                const int lr = (int)(li0 - cta_begin);
+                const int lr = lane_on ? (int)(lrow - cta_begin) : 0;
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {
                     const float* src = sDot + (size_t)r * dbuf_rows + lr;
                     if constexpr (RPT == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(src);
-                        acc[0][r] = v.x; acc[1][r] = v.y; acc[2][r] = v.z; acc[3][r] = v.w;
+                        const float4 dv = *reinterpret_cast<const float4*>(src);
+                        acc[0][r] = dv.x; acc[1][r] = dv.y; acc[2][r] = dv.z; acc[3][r] = dv.w;
                     } else if constexpr (RPT == 2) {
-                        const float2 v = *reinterpret_cast<const float2*>(src);
-                        acc[0][r] = v.x; acc[1][r] = v.y;
+                        const float2 dv = *reinterpret_cast<const float2*>(src);
+                        acc[0][r] = dv.x; acc[1][r] = dv.y;
                     } else {
                         acc[0][r] = *src;
                     }
@@ -2090,7 +2126,7 @@ __global__ void __launch_bounds__(OVR_PASS_THREADS, 1) k_ovr_pass(const OvrArgs 
                     float S = 0.0f;
 #pragma unroll
                     for (int r = 0; r < 16; ++r)
-                        S = fmaf(sCoef[p * 16 + r], kernel_from_dot(a.kp, __uint_as_float(v[k][r]) * isg, xn, sNorm[p * 16 + r]), S);
+                        S = fmaf(sCoef[p * 16 + r], kernel_from_dot(a.kpp[p], __uint_as_float(v[k][r]) * isg, xn, sNorm[p * 16 + r]), S);
                     const uint32_t st = st0[k];
                     const float yv = (st & ST_YPOS) ? 1.0f : -1.0f;
                     const float gn = fmaf(yv, S, g0[k]);
@@ -2331,11 +2367,11 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
             const int ra = tid >> 4, rb = tid & 15;
             if (ra < nr && rb < nr) {
                 double v = gram[tid];
-                if (a.kp.kernel == 2) {
+                if (a.kpp[p].kernel == 2) {
                     v = ra == rb ? 0.0 : gram[ra * 17] + gram[rb * 17] - 2.0 * gram[tid];
                     v = v > 0.0 ? v : 0.0;
                 }
-                sh.kr[tid] = kernel_fp64_from(v, a.kp);
+                sh.kr[tid] = kernel_fp64_from(v, a.kpp[p]);
             }
         }
         __syncthreads();
@@ -2356,7 +2392,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
     SOLVE_MARK(2)
     // ---- a2: the subproblem (one warp), then alpha / status of W and the coefficients --------
     if (warp == 0) {
-        const int steps = solve_subproblem(sh, nw, a.C, a.inner_tol, a.inner_max, lane);
+        const int steps = solve_subproblem(sh, nw, a.Cp[p], a.inner_tol, a.inner_max, lane);
         if (lane == 0) SOLVE_MARK(3)
         __syncwarp();
         if (lane < SVM_WS) {
@@ -2366,7 +2402,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
                 c = (float)((double)sh.w_y[lane] * da);
                 const int64_t g = sh.w_gidx[lane];
                 a.alpha[p][g] = sh.w_anew[lane];
-                a.status[p][g] = make_status(sh.w_y[lane], sh.w_anew[lane], a.C);
+                a.status[p][g] = make_status(sh.w_y[lane], sh.w_anew[lane], a.Cp[p]);
             }
             a.ucoef[p * 16 + lane] = c;
             a.unorm[p * 16 + lane] = sh.xn[lane];

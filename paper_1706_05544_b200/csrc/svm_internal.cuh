@@ -142,6 +142,7 @@ struct SmoInfo {
     int64_t last_w[SVM_WS];
     double last_dalpha[SVM_WS];
     int64_t inner_total;
+    int64_t cache_lookups, cache_hits, cache_allhit;   // kernel-column cache dry run (statistics)
     int64_t phase_cycles[16]; // CTA 0: clock64 per phase (solver [0,8), worker warp 0 [8,16))
     int64_t exch_cycles;      // CTA 0, thread 0: clock64 from its publish to all slots staged
     int64_t loop_cycles;      // CTA 0, thread 0: clock64 over the whole loop (prologue excluded)
@@ -207,6 +208,12 @@ struct SmoArgs {
     // runs ahead across iterations: X does not depend on W).  xmap: 2D map over X^T [d][n_pad]
     // (dim 0 = rows, contiguous), box {32 RPT, min(d, 256)}.
     int32_t x_tma, tma_ns;
+    int32_t chunk_rows;       // rows per warp work item (multiple of 4, <= 32 rpt; 0 = 32 rpt)
+    // kernel-column cache dry run (SVMB200_CACHE_STATS = slots): CTA 0 tracks a 4-way set-associative
+    // LRU of W rows (tags / stamps in global scratch) and counts hits; the pass is unchanged
+    int32_t cache_slots;
+    int32_t* cache_tag;
+    uint32_t* cache_stamp;
     alignas(64) CUtensorMap xmap;
 };
 
@@ -224,10 +231,11 @@ struct OvrArgs {
     double* alpha[OVR_MAXP];   // per problem [n_pad]
     float* G[OVR_MAXP];
     uint8_t* status[OVR_MAXP];
-    double C, tol, inner_tol;
+    double tol, inner_tol;
     int inner_max;
     int64_t max_iter;
-    KParams kp;
+    KParams kpp[OVR_MAXP];     // per problem: kernel parameters (gamma grids share the X pass)
+    double Cp[OVR_MAXP];       // per problem: box bound C
     int NU;                    // 16 * P (MMA N)
     int kch, nkc;              // features per K-chunk (multiple of 8), number of chunks
     uint16_t* Uh;              // [nkc][hi | lo][NU x KCH] fp16 K-major core tiles (k_ovr_solve)

@@ -59,3 +59,17 @@ def test_handle_exchange_gloo_world2():
         assert heads == [bytes([0]) * 4, bytes([1]) * 4]
         assert total == 2 * 1024
     assert res[0][3] == (0, 500) and res[1][3] == (500, 1001)
+
+
+def test_kfold_split_sizes_and_stratification():
+    """SPEC kfold_split: union = all rows, sizes differ by at most one, stratified per class."""
+    import numpy as np
+    from paper_1706_05544_b200 import binding
+    f = binding.kfold_split(10, 5, seed=1)
+    assert sorted(np.bincount(f).tolist()) == [2, 2, 2, 2, 2]
+    f = binding.kfold_split(7, 3, seed=2)
+    assert sorted(np.bincount(f).tolist()) == [2, 2, 3]
+    lab = np.array([0] * 6 + [1] * 4)
+    f = binding.kfold_split(10, 2, seed=3, labels=lab)
+    for k in range(2):
+        assert (lab[f == k] == 0).sum() == 3 and (lab[f == k] == 1).sum() == 2

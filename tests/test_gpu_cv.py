@@ -1,0 +1,98 @@
+"""K-fold cross validation over a (gamma, C) grid against
+independent oracle solves: for every grid cell and fold the oracle trains on the training split
+alone (the Eq. 2 instance of those rows) and evaluates its decision function on the
+held-out rows; the GPU's held-out decision values (one device X, held-out rows excluded through
+their status, classification problems batched 16 at a time) must match within north_star's
+1e-3, labels wherever the oracle's decision is unique at that tolerance, and the per-cell
+metrics must follow from those decisions (accuracy / MSE / Pearson)."""
+import numpy as np
+import pytest
+
+import oracle as ora
+import paper_1706_05544_b200 as pkg
+from paper_1706_05544_b200 import binding, synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    pkg.lib()
+
+
+def _oracle_fold(X, y, train, held, reg, gamma, C, classes=None):
+    if reg:
+        m = ora.train(X[train], y[train], svm_type=ora.EPS_REGRESSION, gamma=gamma, C=C)
+        return m.decision_function(X[held])
+    if classes is None:   # binary, labels exactly +-1 (used as-is)
+        m = ora.train(X[train], y[train], gamma=gamma, C=C)
+        return m.decision_function(X[held])
+    cols = []
+    for c in classes:    # one-vs-rest in the label order of the FULL y
+        yb = np.where(y[train] == c, 1.0, -1.0).astype(np.float32)
+        m = ora.train(X[train], yb, gamma=gamma, C=C)
+        cols.append(m.decision_function(X[held])[:, 0])
+    return np.stack(cols, axis=1)
+
+
+@pytest.mark.parametrize("case", ["binary_grid", "regression", "one_vs_rest"])
+def test_cross_validate_vs_oracle(case):
+    if case == "binary_grid":
+        ds = synth.make("c1", n=1200)
+        reg, nfold = False, 4
+        gammas, costs = [0.05, 0.2, 0.05], [1.0, 1.0, 3.0]
+    elif case == "regression":
+        ds = synth.make("c2", n=900, d=20)
+        reg, nfold = True, 3
+        gammas, costs = [0.05], [1.0]
+    else:
+        ds = synth.mnist_like(n=900, d=40, k=4)
+        reg, nfold = False, 3
+        gammas, costs = [1.0 / 40, 0.05], [1.0, 1.0]
+    X, y = ds.X, ds.y
+    fold = binding.kfold_split(ds.n, nfold, seed=7, labels=None if reg else y)
+    kw = dict(svm_type="eps-regression" if reg else "C-classification", epsilon=0.1)
+    res, dec = binding.cross_validate(X, y, nfold, fold=fold, gammas=gammas, costs=costs,
+                                      decision=True, **kw)
+    classes = None
+    if not reg and len(set(y.tolist())) > 2:
+        classes = list(dict.fromkeys(y.tolist()))
+    for g, (gm, C) in enumerate(zip(gammas, costs)):
+        assert res[g]["nfold"] == nfold and res[g]["failed"] == 0 and res[g]["converged"] == 1
+        assert abs(res[g]["gamma"] - gm) < 1e-15 and res[g]["cost"] == C
+        metrics = []
+        for f in range(nfold):
+            train, held = np.nonzero(fold != f)[0], np.nonzero(fold == f)[0]
+            fo = _oracle_fold(X, y, train, held, reg, gm, C, classes)
+            fg = dec[g, held, :]
+            assert np.abs(fg - fo).max() <= 1e-3, (case, g, f, np.abs(fg - fo).max())
+            if reg:
+                metrics.append(np.mean((fg[:, 0] - y[held]) ** 2))
+            else:
+                if classes is None:
+                    lab_o = np.where(fo[:, 0] > 0, 1.0, -1.0)
+                    lab_g = np.where(fg[:, 0] > 0, 1.0, -1.0)
+                    margin = np.abs(fo[:, 0])
+                else:
+                    lab_o = np.asarray(classes)[np.argmax(fo, axis=1)]
+                    lab_g = np.asarray(classes)[np.argmax(fg, axis=1)]
+                    srt = np.sort(fo, axis=1)
+                    margin = srt[:, -1] - srt[:, -2]
+                sure = margin > 2e-3
+                assert (lab_o[sure] == lab_g[sure]).all()
+                metrics.append(np.mean(lab_g == y[held]))
+        # the reported metric is the mean of the per-fold metrics of these decisions
+        assert abs(res[g]["metric"] - np.mean(metrics)) <= 1e-9, (res[g]["metric"], np.mean(metrics))
+
+
+def test_cross_validate_errors():
+    ds = synth.make("c1", n=300)
+    with pytest.raises(pkg.SvmError):
+        binding.cross_validate(ds.X, ds.y, 1)
+    with pytest.raises(pkg.SvmError):
+        binding.cross_validate(ds.X, ds.y, 3, fold=np.full(ds.n, 5, np.int32))
+    with pytest.raises(pkg.SvmError):
+        binding.cross_validate(ds.X, ds.y, 3, costs=[-1.0])
