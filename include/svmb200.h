@@ -117,6 +117,8 @@ typedef struct svm_model_info {
                           /* 0 for the batched one-vs-rest passes.                               */
     double exchange_p50_us; /* median and 99th percentile of that per-iteration exchange latency */
     double exchange_p99_us; /* (histogram of 512-cycle bins, converted at the loop's clock)       */
+    int64_t cache_passes;   /* iterations whose W rows were all in the kernel-column cache (SURVEY */
+                            /* 8(f) #3): their pass read K columns instead of X                  */
 } svm_model_info;
 
 /*
@@ -213,6 +215,7 @@ typedef struct svm_solver_stats {
     double last_dalpha[16]; /* alpha change of each last_w entry                               */
     int32_t last_inner;   /* inner pair steps of the last subproblem                           */
     double loop_ms;       /* device time of the last run                                       */
+    int64_t cache_passes; /* iterations of the last run served by the kernel-column cache       */
 } svm_solver_stats;
 
 int svm_solver_create(const float* X, const float* y, int64_t n, int64_t d,

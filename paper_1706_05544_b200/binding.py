@@ -55,7 +55,8 @@ class svm_model_info(ctypes.Structure):
                 ("setup_ms", ctypes.c_double), ("certify_ms", ctypes.c_double),
                 ("passes", ctypes.c_int64), ("pass_ms", ctypes.c_double),
                 ("batched", ctypes.c_int32), ("exchange_ms", ctypes.c_double),
-                ("exchange_p50_us", ctypes.c_double), ("exchange_p99_us", ctypes.c_double)]
+                ("exchange_p50_us", ctypes.c_double), ("exchange_p99_us", ctypes.c_double),
+                ("cache_passes", ctypes.c_int64)]
 
 
 class svm_solver_stats(ctypes.Structure):
@@ -63,7 +64,7 @@ class svm_solver_stats(ctypes.Structure):
                 ("M_low", ctypes.c_double), ("converged", ctypes.c_int32),
                 ("last_nw", ctypes.c_int32), ("last_w", ctypes.c_int64 * 16),
                 ("last_dalpha", ctypes.c_double * 16), ("last_inner", ctypes.c_int32),
-                ("loop_ms", ctypes.c_double)]
+                ("loop_ms", ctypes.c_double), ("cache_passes", ctypes.c_int64)]
 
 
 class svm_cv_result(ctypes.Structure):

@@ -63,7 +63,8 @@ static int fail(int code, const char* fmt, ...)
 // point synchronises its stream before returning, so pool reuse never races user work.
 // The library's device buffers come from a PRIVATE stream-ordered pool per device (the default
 // pool and the caller's allocators are left alone).  Its release threshold keeps up to
-// min(8 GiB, 1/16 of the device) of freed memory cached for the next training: with threshold 0
+// min(16 GiB, 1/8 of the device) of freed memory cached for the next training (the kernel-column
+// cache alone takes up to 12 GiB): with threshold 0
 // every synchronize returned it to the OS and the next training re-mapped it, which made single
 // trainings 10-30% slower at random (c2: +40 ms, c4: +1.2 s measured); beyond the bound, freed
 // memory goes back to the device at the next synchronize, so a host framework sharing the GPU
@@ -85,7 +86,7 @@ cudaMemPool_t svm_mem_pool()
         if (cudaMemPoolCreate(&pool, &pp) != cudaSuccess) { cudaGetLastError(); return nullptr; }
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        uint64_t thr = std::min<uint64_t>(8ull << 30, (uint64_t)tot / 16);
+        uint64_t thr = std::min<uint64_t>(16ull << 30, (uint64_t)tot / 8);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         cudaGetLastError();
         pools[dev] = pool;
@@ -413,6 +414,7 @@ struct Problem {
     double exch_hist[SMO_EXCH_BINS] = {};   // per-iteration exchange latency histogram (us units
                                             // after scaling: see exch_percentile)
     double us_per_cycle = 0;                // loop_ms / loop_cycles of the last launch
+    int64_t cache_allhit = 0;               // iterations run as kernel-column-cache passes
     int64_t passes = 0;    // X passes of the dominant pass kernel (batched one-vs-rest: k_ovr_pass)
     double pass_ms = 0;    // their device time (CUDA event pairs around each launch)
     SmoInfo last_info;
@@ -614,17 +616,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     }
     a.tag0 = E.epoch;
     a.max_iter = max_iter;
-    DBuf ctag, cstamp;   // kernel-column cache dry run (statistics only)
-    if (const char* e = getenv("SVMB200_CACHE_STATS")) {
-        const int slots = std::max(4, atoi(e) / 4 * 4);
-        TRY(ctag.alloc(sizeof(int32_t) * slots));
-        TRY(cstamp.alloc(sizeof(uint32_t) * slots));
-        CK(cudaMemsetAsync(ctag.p, 0xff, ctag.bytes, st));
-        CK(cudaMemsetAsync(cstamp.p, 0, cstamp.bytes, st));
-        a.cache_slots = slots;
-        a.cache_tag = ctag.as<int32_t>();
-        a.cache_stamp = cstamp.as<uint32_t>();
-    }
+
     CK(cudaMemsetAsync(E.info.p, 0, sizeof(SmoInfo), st));
     const int64_t pos_elems = D.rows_per_cta * P.ncopy;
     const int64_t smem_cap = 200 * 1024;
@@ -683,6 +675,33 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         if (const char* e = getenv("SVMB200_CHUNK_ROWS")) {
             const int64_t c = 32 * a.rpt, v = atoll(e) / 4 * 4;
             if (v >= 4 && v < c) a.chunk_rows = (int32_t)v;
+        }
+    }
+    // kernel-column cache: streamed X only (X resident in shared memory costs no
+    // HBM; the wide and TMA pipelines consume every chunk of every iteration); up to 4096 columns
+    // within min(12 GiB, 20% of the free device memory) -- inside the pool's retained bound, so
+    // repeated trainings do not re-map it (c4, 16384 columns = 33 GB: +1.2-3 s of mapping per
+    // training, measured).  SVMB200_CACHE = slots (0 = off).
+    DBuf cdata, ctag, cstamp;
+    if (!a.x_in_smem && !a.wide && !a.x_tma && !a.pass_only) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const int64_t col = D.n_pad * (int64_t)sizeof(float);
+        const double budget = std::min(12.0 * (1ull << 30), 0.2 * (double)fr);
+        int64_t slots = std::min<int64_t>(4096, (int64_t)budget / std::max<int64_t>(col, 1));
+        if (const char* e = getenv("SVMB200_CACHE")) slots = std::min<int64_t>(atoll(e), 65536);
+        slots = slots / 4 * 4;
+        const int nctas = a.virt ? a.nblk * a.world : a.nblk;
+        if (slots >= 16) {
+            TRY(cdata.alloc((size_t)col * slots));
+            TRY(ctag.alloc(sizeof(int32_t) * slots * nctas));
+            TRY(cstamp.alloc(sizeof(uint32_t) * slots * nctas));
+            CK(cudaMemsetAsync(ctag.p, 0xff, ctag.bytes, st));
+            CK(cudaMemsetAsync(cstamp.p, 0, cstamp.bytes, st));
+            a.cache_slots = (int32_t)slots;
+            a.cache_data = cdata.as<float>();
+            a.cache_tag = ctag.as<int32_t>();
+            a.cache_stamp = cstamp.as<uint32_t>();
         }
     }
     {   // buffer the dot products of as many rows as fit (64 B per row), whole chunks only
@@ -755,9 +774,10 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         P.us_per_cycle = ms * 1e3 / (double)info.loop_cycles;
         for (int b = 0; b < SMO_EXCH_BINS; ++b) P.exch_hist[b] += (double)info.exch_hist[b];
     }
-    if (a.cache_slots > 0)
-        fprintf(stderr, "[svmb200] column-cache dry run, %d slots: %lld iterations, row hit rate %.3f, "
-                "all-|W| hits %.3f\n", a.cache_slots, (long long)info.iterations,
+    P.cache_allhit += info.cache_allhit;
+    if (a.cache_slots > 0 && getenv("SVMB200_PROFILE"))
+        fprintf(stderr, "[svmb200] column cache, %d slots: %lld iterations, row hit rate %.3f, "
+                "cache-pass iterations %.3f\n", a.cache_slots, (long long)info.iterations,
                 info.cache_lookups ? (double)info.cache_hits / (double)info.cache_lookups : 0.0,
                 info.iterations ? (double)info.cache_allhit / (double)info.iterations : 0.0);
     if (getenv("SVMB200_PROFILE")) {
@@ -1318,6 +1338,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     std::vector<double> bs(ys.size());
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, pass_ms = 0, exch_ms = 0;
     double xh[SMO_EXCH_BINS] = {}, upc = 0;
+    int64_t cache_passes = 0;
     int64_t iters = 0, passes = 0;
     bool conv = true, cert = true;
     for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
@@ -1339,6 +1360,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
         exch_ms += P.exch_ms;
+        cache_passes += P.cache_allhit;
         for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
         if (P.us_per_cycle > 0) upc = P.us_per_cycle;
         cert_ms += P.cert_ms;
@@ -1380,6 +1402,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     I.exchange_ms = exch_ms;
     I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
     I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
+    I.cache_passes = cache_passes;
     I.certify_ms = cert_ms;
     I.setup_ms = t_setup;
     I.passes = passes;
@@ -1862,6 +1885,7 @@ extern "C" int svm_solver_run(svm_solver* s, int64_t max_iter, svm_solver_stats*
         }
         stats->last_inner = info.last_inner;
         stats->loop_ms = s->P.loop_ms;
+        stats->cache_passes = info.cache_allhit;
     }
     return SVM_OK;
 }
@@ -2285,6 +2309,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     std::vector<double> bs(S->nprob);
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, exch_ms = 0;
     double xh[SMO_EXCH_BINS] = {}, upc = 0;
+    int64_t cache_passes = 0;
     int64_t iters = 0;
     bool conv = true, cert = true;
     for (int p = 0; p < S->nprob; ++p) {
@@ -2329,6 +2354,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         cert = cert && P.certified;
         loop_ms += P.loop_ms;
         exch_ms += P.exch_ms;
+        cache_passes += P.cache_allhit;
         for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
         if (P.us_per_cycle > 0) upc = P.us_per_cycle;
         cert_ms += P.cert_ms;
@@ -2396,6 +2422,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     I.exchange_ms = exch_ms;
     I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
     I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
+    I.cache_passes = cache_passes;
     I.certify_ms = cert_ms;
     I.passes = iters;
     I.pass_ms = loop_ms;

@@ -353,7 +353,7 @@ __device__ __forceinline__ void dots_csr(const int64_t* __restrict__ indptr,
 // [indptr[r0], indptr[r0 + 32]); the warp loads it coalesced into shared memory, then every
 // lane walks its own row from there (no dependent global loads on the FMA chain).  Ranges
 // larger than the buffer fall back to direct loads.
-constexpr int CSR_CAP = 1600;  // nonzeros per warp stage (c5: 32 rows x ~40 nnz)
+constexpr int CSR_CAP = 1472;  // nonzeros per warp stage (c5: 32 rows x 40 +- 6 nnz: 1280 +- 34; beyond -> direct loads)
 __device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indptr,
                                                 const int32_t* __restrict__ indices,
                                                 const float* __restrict__ vals, int64_t li0_warp,
@@ -428,6 +428,7 @@ struct SmoShared {
     uint64_t rk_key[2][SVM_MAX_RANKS * 8];   // rank level: [side][rank * 8 + position]
     int32_t rk_src[2][SVM_MAX_RANKS * 8];
     int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
+    int32_t c_slot[SVM_WS], c_ins[SVM_WS], c_mode;   // kernel-column cache (8(f) #3): per W row
     alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode / TMA-ring pipeline barriers
     uint64_t tma_seq[8];                 // TMA ring: chunk sequence number last issued into each slot
     double m_up, M_low;
@@ -478,8 +479,14 @@ template <int RPT, bool RBFK>
 __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v, const SmoShared& sh, int64_t li0,
                                              int64_t cta_end, bool do_update,
                                              const float (&acc)[RPT][SVM_WS],
-                                             uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT])
+                                             uint64_t (&ku)[2 * RPT], uint64_t (&kl)[2 * RPT],
+                                             int kmode = 0, float* kc = nullptr)
 {
+    // kmode (kernel-column cache): 0 = K from the dot products; 1 = the same, and
+    // the columns of the W rows newly cached this iteration (sh.c_ins[r] >= 0) are stored into
+    // kc[slot][row]; 2 = every W row is cached: K read from kc[sh.c_slot[r]][row] (no X, no dots).
+    // The stored values are exactly the ones the computing path uses, and S sums over r in the
+    // same order either way, so all three modes give bit-identical G.
     if constexpr (RPT == 4) {
         // A lane's 4 rows are consecutive and li0 is a multiple of 4 (rows_per_cta and n_pad are):
         // the norms, G and status of all 4 rows (both copies) are loaded up front as one 16-byte /
@@ -501,26 +508,48 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
             }
         }
         float S[4] = {0.f, 0.f, 0.f, 0.f};
-        if (do_update) {
+        const bool full = li0 + 4 <= cta_end;
+        if (do_update && kmode == 2) {
+#pragma unroll
+            for (int r = 0; r < SVM_WS; ++r) {
+                const int sl = sh.c_slot[r];
+                const float4 K = sl >= 0 ? *reinterpret_cast<const float4*>(kc + (int64_t)sl * a.n_pad + li0)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                S[0] = fmaf(sh.c[r], K.x, S[0]);
+                S[1] = fmaf(sh.c[r], K.y, S[1]);
+                S[2] = fmaf(sh.c[r], K.z, S[2]);
+                S[3] = fmaf(sh.c[r], K.w, S[3]);
+            }
+        } else if (do_update) {
             const float4 xn4 = __ldg(reinterpret_cast<const float4*>(v.xnorm + li0));
             const float xn[4] = {xn4.x, xn4.y, xn4.z, xn4.w};
+            const float ng = -a.kp.gamma * 1.4426950408889634f;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if constexpr (RBFK) {
-                    const float ng = -a.kp.gamma * 1.4426950408889634f;
+            for (int r = 0; r < SVM_WS; ++r) {
+                float K[4];
 #pragma unroll
-                    for (int r = 0; r < SVM_WS; ++r) {
+                for (int j = 0; j < 4; ++j) {
+                    if constexpr (RBFK) {
                         const float d2 = fmaxf(fmaf(-2.0f, acc[j][r], xn[j] + sh.xn[r]), 0.0f);
-                        S[j] = fmaf(sh.c[r], exp2f_approx(ng * d2), S[j]);
+                        K[j] = exp2f_approx(ng * d2);
+                    } else {
+                        K[j] = kernel_from_dot(a.kp, acc[j][r], xn[j], sh.xn[r]);
                     }
-                } else {
+                    S[j] = fmaf(sh.c[r], K[j], S[j]);
+                }
+                if (kmode == 1) {
+                    const int ins = sh.c_ins[r];
+                    if (ins >= 0) {
+                        float* dst = kc + (int64_t)ins * a.n_pad + li0;
+                        if (full) *reinterpret_cast<float4*>(dst) = make_float4(K[0], K[1], K[2], K[3]);
+                        else
 #pragma unroll
-                    for (int r = 0; r < SVM_WS; ++r)
-                        S[j] = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn[j], sh.xn[r]), S[j]);
+                            for (int j = 0; j < 4; ++j)
+                                if (li0 + j < cta_end) dst[j] = K[j];
+                    }
                 }
             }
         }
-        const bool full = li0 + 4 <= cta_end;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             if (c >= a.ncopy) break;
@@ -574,19 +603,26 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
         ku[2 * j] = ku[2 * j + 1] = kl[2 * j] = kl[2 * j + 1] = 0ull;
         if (li >= cta_end) continue;
         float S = 0.0f;
-        if (do_update) {
+        if (do_update && kmode == 2) {
+#pragma unroll
+            for (int r = 0; r < SVM_WS; ++r) {
+                const int sl = sh.c_slot[r];
+                S = fmaf(sh.c[r], sl >= 0 ? kc[(int64_t)sl * a.n_pad + li] : 0.0f, S);
+            }
+        } else if (do_update) {
             const float xn = xnv[j];
-            if constexpr (RBFK) {  // exp(-gamma |x_i - x_r|^2) with the distance from the norms
-                const float ng = -a.kp.gamma * 1.4426950408889634f;  // exp(z) = 2^(z log2 e)
+            const float ng = -a.kp.gamma * 1.4426950408889634f;  // exp(z) = 2^(z log2 e)
 #pragma unroll
-                for (int r = 0; r < SVM_WS; ++r) {
+            for (int r = 0; r < SVM_WS; ++r) {
+                float K;
+                if constexpr (RBFK) {  // exp(-gamma |x_i - x_r|^2) with the distance from the norms
                     const float d2 = fmaxf(fmaf(-2.0f, acc[j][r], xn + sh.xn[r]), 0.0f);
-                    S = fmaf(sh.c[r], exp2f_approx(ng * d2), S);
+                    K = exp2f_approx(ng * d2);
+                } else {
+                    K = kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]);
                 }
-            } else {
-#pragma unroll
-                for (int r = 0; r < SVM_WS; ++r)
-                    S = fmaf(sh.c[r], kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]), S);
+                S = fmaf(sh.c[r], K, S);
+                if (kmode == 1 && sh.c_ins[r] >= 0) kc[(int64_t)sh.c_ins[r] * a.n_pad + li] = K;
             }
         }
 #pragma unroll
@@ -1393,37 +1429,72 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 sh.next_chunk2 = 0;
                 sh.sub_done = 0;
             }
+            if (a.cache_slots > 0) {
+                // ---- kernel-column cache: this CTA's 4-way set-associative LRU of
+                // K(x_i, x_r) columns over its rows.  Every CTA takes the same decisions from the
+                // same W sequence; tags and stamps are per CTA (global, L1-resident).  A hit
+                // refreshes the stamp; a miss takes its set's least recently used way that no W row
+                // of this iteration uses (not when an earlier missing W row has the same set), and
+                // its column is written by this iteration's pass.  All W rows hit -> cache pass.
+                __syncwarp();
+                const int nrr = __popc(firsts);
+                const int nsets = a.cache_slots >> 2;
+                int32_t* ctag = a.cache_tag + (size_t)blockIdx.x * a.cache_slots;
+                uint32_t* cstamp = a.cache_stamp + (size_t)blockIdx.x * a.cache_slots;
+                const uint32_t now = (uint32_t)(t + 1);
+                const bool mine = lane < nrr;
+                const int64_t crow = mine ? sh.r_row[lane] : 0;
+                const int cset = mine ? (int)(crow % nsets) : -1;
+                int hitw = -1;
+                if (mine) {
+                    const int4 tg = *reinterpret_cast<const int4*>(ctag + cset * 4);
+                    const int cr = (int)crow;
+                    hitw = tg.x == cr ? 0 : tg.y == cr ? 1 : tg.z == cr ? 2 : tg.w == cr ? 3 : -1;
+                    if (hitw >= 0) cstamp[cset * 4 + hitw] = now;
+                }
+                const uint32_t hm = __ballot_sync(FULL, hitw >= 0);
+                const uint32_t all = nrr >= 32 ? FULL : ((1u << nrr) - 1u);
+                const bool allhit = nrr > 0 && hm == all;
+                const uint32_t mm = all & ~hm;
+                int sets[SVM_WS];
+#pragma unroll
+                for (int q = 0; q < SVM_WS; ++q) sets[q] = __shfl_sync(FULL, cset, q);
+                __syncwarp();
+                int ins = -1;
+                if (mine && hitw < 0 && !allhit) {
+                    bool first = true;
+#pragma unroll
+                    for (int q = 0; q < SVM_WS; ++q)
+                        if (q < lane && ((mm >> q) & 1u) && sets[q] == cset) first = false;
+                    if (first) {
+                        const uint4 sp = *reinterpret_cast<const uint4*>(cstamp + cset * 4);
+                        const uint32_t s4[4] = {sp.x, sp.y, sp.z, sp.w};
+                        int best = -1;
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            if (s4[w] != now && (best < 0 || s4[w] < s4[best])) best = w;
+                        if (best >= 0) {
+                            ctag[cset * 4 + best] = (int32_t)crow;
+                            cstamp[cset * 4 + best] = now;
+                            ins = cset * 4 + best;
+                        }
+                    }
+                }
+                if (lane < SVM_WS) {
+                    sh.c_slot[lane] = hitw >= 0 ? cset * 4 + hitw : -1;
+                    sh.c_ins[lane] = ins;
+                }
+                if (lane == 0) {
+                    sh.c_mode = allhit ? 2 : 1;
+                    if (reporter) {
+                        a.info->cache_lookups += nrr;
+                        a.info->cache_hits += __popc(hm);
+                        a.info->cache_allhit += allhit ? 1 : 0;
+                    }
+                }
+            }
         }
         __syncthreads();
-        if (a.cache_slots > 0 && reporter && tid == 0 && !sh.stop) {   // cache dry run (stats)
-            const int nsets = a.cache_slots / 4;
-            int hits = 0;
-            bool used[4 * SVM_WS];
-            for (int q = 0; q < 4 * SVM_WS; ++q) used[q] = false;
-            int way_of[SVM_WS];
-            for (int r = 0; r < sh.nr; ++r) {
-                const int64_t row = sh.r_row[r];
-                const int set = (int)(row % nsets);
-                way_of[r] = -1;
-                for (int w = 0; w < 4; ++w)
-                    if (a.cache_tag[set * 4 + w] == (int32_t)row) way_of[r] = w;
-                if (way_of[r] >= 0) { ++hits; a.cache_stamp[set * 4 + way_of[r]] = (uint32_t)(t + 1); }
-            }
-            for (int r = 0; r < sh.nr; ++r) {
-                if (way_of[r] >= 0) continue;
-                const int64_t row = sh.r_row[r];
-                const int set = (int)(row % nsets);
-                int best = 0;
-                for (int w = 1; w < 4; ++w)
-                    if (a.cache_stamp[set * 4 + w] < a.cache_stamp[set * 4 + best]) best = w;
-                a.cache_tag[set * 4 + best] = (int32_t)row;
-                a.cache_stamp[set * 4 + best] = (uint32_t)(t + 1);
-            }
-            a.info->cache_lookups += sh.nr;
-            a.info->cache_hits += hits;
-            a.info->cache_allhit += (hits == sh.nr) ? 1 : 0;
-            (void)used;
-        }
         mark(1);
         if (sh.stop) {
             drain_wide();
@@ -1582,7 +1653,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         // feature slicing (wide d, streamed X): every (chunk, slice) item is buffered in phase A
         const int nsl = a.nslice > 1 ? a.nslice : 1;
         const int ks = nsl > 1 ? (d + nsl - 1) / nsl : d;
-        const int nitems = nsl > 1 ? nchunks * nsl : nbuf;
+        const int kmode = a.cache_slots > 0 ? sh.c_mode : 0;   // kernel-column cache mode
+        float* kcache = a.cache_data ? a.cache_data + (a.virt ? v.row0 : 0) : nullptr;
+        const int nitems = kmode == 2 ? 0 : (nsl > 1 ? nchunks * nsl : nbuf);   // cache pass: no dots
         // ---- phase A: dot products x_i . X_W of the buffered chunks into shared memory --------
         auto phase_a = [&]() {
             for (;;) {
@@ -1708,7 +1781,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         // ---- phase B / a3: epilogue of every chunk (buffered dots, or computed now) ----------
         // chunks [0, nA) have buffered dots; the streamed ones [nA, nchunks) are handed out
         // first so that their X reads start together and no streamed chunk forms the tail
-        const int nA = nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf);
+        const int nA = kmode == 2 ? 0 : (nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf));
         const int nS = nchunks - nA;
         for (;;) {
             int tk = 0;
@@ -1719,7 +1792,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             const int64_t lrow = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             const int64_t li0 = lane_on ? lrow : cta_end;   // idle lanes: past the CTA's rows
             float acc[RPT][SVM_WS];
-            if (ch < nA) {
+            if (kmode == 2) {
+                zero_acc<RPT>(acc);   // (unused: K comes from the cache)
+            } else if (ch < nA) {
                 const int lr = lane_on ? (int)(lrow - cta_begin) : 0;
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {
@@ -1754,7 +1829,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             }
             wmark(0);
             uint64_t ku[2 * RPT], kl[2 * RPT];
-            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, true, acc, ku, kl);
+            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, true, acc, ku, kl, kmode, kcache);
             wmark(2);
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             wmark(3);

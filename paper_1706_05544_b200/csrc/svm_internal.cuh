@@ -209,9 +209,11 @@ struct SmoArgs {
     // (dim 0 = rows, contiguous), box {32 RPT, min(d, 256)}.
     int32_t x_tma, tma_ns;
     int32_t chunk_rows;       // rows per warp work item (multiple of 4, <= 32 rpt; 0 = 32 rpt)
-    // kernel-column cache dry run (SVMB200_CACHE_STATS = slots): CTA 0 tracks a 4-way set-associative
-    // LRU of W rows (tags / stamps in global scratch) and counts hits; the pass is unchanged
+    // kernel-column cache (SPEC KernelRowCache S:105-110): cache_slots columns of
+    // K(x_i, x_r) over the local rows ([slot][n_pad] fp32), per-CTA 4-way set-associative LRU tags
+    // and stamps ([nblk][cache_slots]); 0 slots = off
     int32_t cache_slots;
+    float* cache_data;
     int32_t* cache_tag;
     uint32_t* cache_stamp;
     alignas(64) CUtensorMap xmap;

@@ -214,3 +214,32 @@ def test_train_sharded_one_call_world1():
     mc2 = binding.train_sharded_nccl_csr(dsc.indptr, dsc.indices, dsc.data, dsc.d, 0, dsc.y, 0, 1,
                                          binding.nccl_unique_id(), gamma=1.0 / dsc.d)
     np.testing.assert_array_equal(mc1.support()[1], mc2.support()[1])
+
+
+@pytest.mark.parametrize("case", [("c4", 36864, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=4), False),
+                                  ("c4", 20000, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=2), False),
+                                  ("c2", 9000, dict(SVMB200_NO_XSMEM=1, SVMB200_RPT=1), False),
+                                  ("c4", 36864, {}, True)])
+def test_column_cache_bit_identical(case):
+    """SURVEY 8(f) #3 / SPEC KernelRowCache ("a cached row equals a fresh recomputation
+    exactly"): training with the kernel-column cache (cache passes read K columns instead of X)
+    gives bit-identical alpha, G and iteration count to training without it."""
+    cfg, n, ev, csr = case
+    ds = synth.make(cfg, n=n)
+    kw = dict(svm_type="eps-regression" if ds.svm_type == synth.EPS_REGRESSION else "C-classification",
+              gamma=1.0 / ds.d)
+    sp = _csr(ds.X) if csr else None   # c4's rows as CSR (one-hot blocks: 12 of 54 nonzero)
+
+    def run(slots):
+        with env(SVMB200_CACHE=slots, **ev):
+            s = (pkg.Solver(csr=sp, y=ds.y, d=ds.d, **kw) if csr else pkg.Solver(ds.X, ds.y, **kw))
+            st = s.run(10 ** 7)
+            return st, s.get_state()
+    st0, (a0, g0) = run(0)
+    st1, (a1, g1) = run(1024)
+    assert st0.converged and st0.cache_passes == 0
+    assert st1.iterations == st0.iterations
+    np.testing.assert_array_equal(a1, a0)
+    np.testing.assert_array_equal(g1, g0)
+    if cfg != "c2":   # (eps-SVR working sets rarely repeat all 16 rows: no cache passes needed)
+        assert st1.cache_passes > 0
