@@ -436,7 +436,10 @@ def main():
     bpi = fused_bytes_per_iter(args.config, n_rows_local, d, ncopy,
                                nnz=int(ds.indptr[r1] - ds.indptr[r0]) if csr else None)
     loop_s = info.loop_ms / 1e3
-    achieved = bpi * info.iterations / loop_s / 1e9 if loop_s > 0 else 0.0
+    # kernel-column cache passes read 16 cached K values per row instead of X
+    cpi = n_rows_local * (4 * 16 + 4 + 9 * ncopy) if not csr else n_rows_local * (4 * 16 + 8 + 4 + 9 * ncopy)
+    alg_bytes = bpi * (info.iterations - info.cache_passes) + cpi * info.cache_passes
+    achieved = alg_bytes / loop_s / 1e9 if loop_s > 0 else 0.0
     traffic = None
     tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}.json")
     if os.path.exists(tf):
@@ -451,7 +454,9 @@ def main():
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                   "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                  "algorithmic_bytes_per_launch": bpi * info.iterations,
+                  "algorithmic_bytes_per_launch": alg_bytes,
+                  "algorithmic_bytes_per_iteration": {"pass": bpi, "cache_pass": cpi},
+                  "cache_passes": info.cache_passes, "iterations": info.iterations,
                   "kernel": "smo_persistent (a1+a2+a3 fused, one cooperative launch per training)",
                   "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
                   "note": ROOF_NOTES.get(args.config, "")}

@@ -257,6 +257,23 @@ int svm_solver_pass_bench(svm_solver* s, const int64_t* rows, int32_t nr, const 
                           int64_t passes, double* ms);
 void svm_solver_free(svm_solver* s);
 
+/* ---- batched solver: P binary C-SVC problems on one dense X, stepwise -------
+ * The machinery svm_train uses for one-vs-rest (and svm_cross_validate for folds / grids): each
+ * iteration is one k_ovr_solve launch (per problem: selection, stop test, fp64 subproblem, its 16
+ * U columns) and one k_ovr_pass launch (tcgen05 D = X X_U^T for all problems at once, kernel
+ * values, G update, candidates).  Y: fp32 [nprob][n] labels +-1 (host or device); 2 <= nprob <=
+ * 16.  Dual variables indexed by row (as svm_solver).  svm_batch_run executes up to max_iter
+ * iterations per problem from the current state (a problem stops early at tolerance) and writes
+ * each problem's iteration count (may be NULL).  SVM_EINVAL when d or the shared-memory plan is
+ * not covered by the batched pass. */
+typedef struct svm_batch svm_batch;
+int svm_batch_create(const float* X, const float* Y, int32_t nprob, int64_t n, int64_t d,
+                     const svm_params* params, svm_batch** out);
+int svm_batch_set_state(svm_batch* b, int32_t p, const double* alpha, const float* G);
+int svm_batch_get_state(const svm_batch* b, int32_t p, double* alpha, float* G);
+int svm_batch_run(svm_batch* b, int64_t max_iter, int64_t* iterations);
+void svm_batch_free(svm_batch* b);
+
 /* ---- row-sharded training over several GPUs (one process per GPU) --------------------------
  * Rank r holds training rows [row0, row0 + n_local) of an n_global-row problem (contiguous
  * blocks).  Every iteration each CTA of a rank publishes its 8+8 working-set

@@ -111,6 +111,12 @@ SIGNATURES = {
     "svm_shard_train": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "svm_shard_free": (None, [_P]),
     "svm_nccl_unique_id": (ctypes.c_int, [_P]),
+    "svm_batch_create": (ctypes.c_int, [_P, _P, _i32, _i64, _i64, ctypes.POINTER(svm_params),
+                                        ctypes.POINTER(_P)]),
+    "svm_batch_set_state": (ctypes.c_int, [_P, _i32, _P, _P]),
+    "svm_batch_get_state": (ctypes.c_int, [_P, _i32, _P, _P]),
+    "svm_batch_run": (ctypes.c_int, [_P, _i64, _P]),
+    "svm_batch_free": (None, [_P]),
     "svm_cross_validate": (ctypes.c_int, [_P, _P, _i64, _i64, ctypes.POINTER(svm_params), _i32, _P,
                                           _i32, _P, _P, ctypes.POINTER(svm_cv_result), _P]),
     "svm_train_sharded": (ctypes.c_int, [_P, _i64, _i64, _i64, _P, _i64, _i32, _i32, _P,
@@ -472,3 +478,39 @@ def cross_validate(X, y, nfold: int, fold=None, gammas=None, costs=None, decisio
                                     dec.ctypes.data_as(_P) if dec is not None else None))
     out = [{f: getattr(r, f) for f, _ in svm_cv_result._fields_} for r in res]
     return (out, dec) if decision else out
+
+
+class BatchSolver:
+    """svm_batch_*: P binary C-SVC problems on one dense X, stepwise (the batched tcgen05 pass)."""
+
+    def __init__(self, X, Y, **kw):
+        n, d = int(X.shape[0]), int(X.shape[1])
+        Y = np.ascontiguousarray(Y, np.float32)
+        self.P, self.n = int(Y.shape[0]), n
+        p = params(d, **kw)
+        x = _Arr(X, np.float32)
+        h = ctypes.c_void_p()
+        _check(lib().svm_batch_create(x.p, Y.ctypes.data_as(_P), self.P, n, d, ctypes.byref(p),
+                                      ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value and _lib is not None:
+            _lib.svm_batch_free(self._h)
+            self._h = ctypes.c_void_p(None)
+
+    def set_state(self, p, alpha, G):
+        a, g = _Arr(alpha, np.float64), _Arr(G, np.float32)
+        _check(lib().svm_batch_set_state(self._h, int(p), a.p, g.p))
+
+    def get_state(self, p):
+        alpha = np.empty(self.n, np.float64)
+        G = np.empty(self.n, np.float32)
+        _check(lib().svm_batch_get_state(self._h, int(p), alpha.ctypes.data_as(_P),
+                                         G.ctypes.data_as(_P)))
+        return alpha, G
+
+    def run(self, max_iter: int):
+        it = np.zeros(self.P, np.int64)
+        _check(lib().svm_batch_run(self._h, int(max_iter), it.ctypes.data_as(_P)))
+        return it

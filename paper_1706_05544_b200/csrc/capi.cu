@@ -1755,6 +1755,100 @@ extern "C" int svm_cross_validate(const float* X, const float* y, int64_t n, int
     return SVM_OK;
 }
 
+// ================================================================ batched solver (8(f) #1)
+// Stepwise access to the batched one-vs-rest machinery: P binary problems on one dense X, each
+// iteration = one k_ovr_solve (selection, subproblem) + one k_ovr_pass (tcgen05 X X_U^T, G update,
+// candidates) for all problems (parity tests of the batched pass; drivers).
+struct svm_batch {
+    Data D;
+    std::vector<Problem> probs;
+    svm_params prm;
+    cudaStream_t st = nullptr;
+};
+
+extern "C" int svm_batch_create(const float* X, const float* Y, int32_t nprob, int64_t n,
+                                int64_t d, const svm_params* params, svm_batch** out)
+{
+    if (!out) return fail(SVM_EINVAL, "out is NULL");
+    *out = nullptr;
+    TRY(check_params(params, n, d));
+    if (!X || !Y) return fail(SVM_EINVAL, "X or Y is NULL");
+    if (params->type != SVM_C_CLASSIFICATION) return fail(SVM_EINVAL, "batched problems are C-SVC");
+    if (nprob < 2 || nprob > OVR_MAXP) return fail(SVM_EINVAL, "nprob must be in [2, %d]", OVR_MAXP);
+    svm_batch* B = new (std::nothrow) svm_batch();
+    if (!B) return fail(SVM_ENOMEM, "batch allocation failed");
+    B->prm = *params;
+    B->st = (cudaStream_t)params->stream;
+    int rc = build_dense(B->D, X, n, d, params->layout, pick_nblk(n), B->st);
+    std::vector<float> yh;
+    if (rc == SVM_OK) rc = to_host(yh, Y, (int64_t)nprob * n, B->st);
+    if (rc == SVM_OK) {
+        for (int64_t i = 0; i < (int64_t)nprob * n; ++i)
+            if (yh[i] != 1.0f && yh[i] != -1.0f) { rc = fail(SVM_EINVAL, "Y must hold +-1 labels"); break; }
+    }
+    {
+        std::vector<Problem> tmp(nprob);   // (Problem owns device buffers: not copyable)
+        B->probs.swap(tmp);
+    }
+    for (int p = 0; p < nprob && rc == SVM_OK; ++p)
+        rc = problem_init(B->probs[p], B->D, yh.data() + (size_t)p * n, params, B->st);
+    if (rc == SVM_OK && cudaStreamSynchronize(B->st) != cudaSuccess) rc = fail(SVM_ECUDA, "setup failed");
+    if (rc != SVM_OK) { delete B; return rc; }
+    *out = B;
+    return SVM_OK;
+}
+
+extern "C" int svm_batch_set_state(svm_batch* B, int32_t p, const double* alpha, const float* G)
+{
+    if (!B || !alpha || !G || p < 0 || p >= (int)B->probs.size()) return fail(SVM_EINVAL, "bad argument");
+    Problem& P = B->probs[p];
+    const int64_t n = B->D.n;
+    std::vector<double> ah;
+    TRY(to_host(ah, alpha, n, B->st));
+    for (int64_t i = 0; i < n; ++i)
+        if (!(ah[i] >= 0.0 && ah[i] <= P.C)) return fail(SVM_EINVAL, "alpha[%lld] outside [0, C]", (long long)i);
+    DBuf da, dg;
+    TRY(to_device(da, alpha, n, B->st));
+    TRY(to_device(dg, G, n, B->st));
+    CK(lay_unpack_state(da.as<double>(), dg.as<float>(), n, B->D.n_pad, 1, P.alpha.as<double>(),
+                        P.G.as<float>(), B->st));
+    CK(lay_status_from_alpha(P.alpha.as<double>(), n, B->D.n_pad, 1, P.C, P.status.as<uint8_t>(), B->st));
+    CK(cudaStreamSynchronize(B->st));
+    return SVM_OK;
+}
+
+extern "C" int svm_batch_get_state(const svm_batch* B, int32_t p, double* alpha, float* G)
+{
+    if (!B || p < 0 || p >= (int)B->probs.size()) return fail(SVM_EINVAL, "bad argument");
+    const Problem& P = B->probs[p];
+    const int64_t n = B->D.n;
+    DBuf da, dg;
+    TRY(da.alloc(sizeof(double) * n));
+    TRY(dg.alloc(sizeof(float) * n));
+    CK(lay_pack_state(P.alpha.as<double>(), P.G.as<float>(), n, B->D.n_pad, 1, da.as<double>(),
+                      dg.as<float>(), B->st));
+    if (alpha) CK(cudaMemcpyAsync(alpha, da.p, sizeof(double) * n,
+                                  is_device_ptr(alpha) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, B->st));
+    if (G) CK(cudaMemcpyAsync(G, dg.p, sizeof(float) * n,
+                              is_device_ptr(G) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, B->st));
+    CK(cudaStreamSynchronize(B->st));
+    return SVM_OK;
+}
+
+extern "C" int svm_batch_run(svm_batch* B, int64_t max_iter, int64_t* iterations)
+{
+    if (!B || max_iter < 1) return fail(SVM_EINVAL, "NULL batch or max_iter < 1");
+    for (size_t p = 0; p < B->probs.size(); ++p) B->probs[p].max_iter = max_iter;
+    bool handled = false;
+    TRY(solve_batched(B->D, B->probs, &B->prm, B->st, &handled));
+    if (!handled) return fail(SVM_EINVAL, "configuration not covered by the batched pass");
+    if (iterations)
+        for (size_t p = 0; p < B->probs.size(); ++p) iterations[p] = B->probs[p].iterations;   // (this run's)
+    return SVM_OK;
+}
+
+extern "C" void svm_batch_free(svm_batch* B) { delete B; }
+
 // ================================================================ solver-state API
 struct svm_solver {
     Data D;

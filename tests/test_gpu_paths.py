@@ -243,3 +243,38 @@ def test_column_cache_bit_identical(case):
     np.testing.assert_array_equal(g1, g0)
     if cfg != "c2":   # (eps-SVR working sets rarely repeat all 16 rows: no cache passes needed)
         assert st1.cache_passes > 0
+
+
+@pytest.mark.parametrize("n,d,P", [(1100, 40, 3), (700, 200, 4)])
+def test_batched_pass_one_step_vs_oracle(n, d, P):
+    """one batched iteration (k_ovr_solve + the tcgen05 k_ovr_pass with 3 fp16-split
+    MMAs) from the same fp32-representable state as the oracle, for every problem: W exact and the
+    new G within 1e-5 max(1, |G|) of the oracle's step 6 applied to the GPU's dalpha."""
+    from paper_1706_05544_b200 import binding
+    ds = synth.mnist_like(n=n, d=d, k=P)
+    classes = list(dict.fromkeys(ds.y.tolist()))
+    Y = np.stack([np.where(ds.y == c, 1.0, -1.0) for c in classes]).astype(np.float32)
+    gamma, C = 1.0 / d, 1.0
+    ks = ora.kspec("rbf", gamma, d=d)
+    b = binding.BatchSolver(ds.X, Y, gamma=gamma)
+    probs = [ora.Problem(ora.C_CLASSIFICATION, Y[p], n) for p in range(P)]
+    states = []
+    for p in range(P):   # a different number of oracle steps per problem
+        alpha, G = np.zeros(n), probs[p].p.copy()
+        for _ in range(3 * p):
+            _, _, alpha, G = ora.step(ds.X, probs[p], ks, alpha, G, C)
+        G32 = G.astype(np.float32)
+        b.set_state(p, alpha, G32)
+        states.append((alpha, G32))
+    it = b.run(1)
+    assert (it == 1).all(), it
+    for p in range(P):
+        alpha, G32 = states[p]
+        W = ora.select(probs[p], alpha, G32.astype(np.float64), C, 16)
+        ag, Gg = b.get_state(p)
+        dA = ag - alpha
+        Wg = np.nonzero(dA)[0]
+        assert set(Wg.tolist()) <= set(W.tolist())        # only W moved (a1)
+        Gref = ora.gradient_update(ds.X, probs[p], ks, W, dA[W], G32.astype(np.float64))
+        err = np.abs(Gg - Gref) / np.maximum(1.0, np.abs(Gref))
+        assert err.max() <= 1e-5, (p, err.max())
