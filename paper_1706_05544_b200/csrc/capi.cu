@@ -371,6 +371,36 @@ static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, con
     return SVM_OK;
 }
 
+// Handles that outlive the call (svm_solver, svm_batch) must not keep the caller's device arrays
+// (the header's rule: inputs are borrowed for the call only): copy every borrowed pointer of D
+// into a buffer D owns.
+static int own_inputs(Data& D, cudaStream_t st)
+{
+    if (!D.csr && D.XR && !D.XR_own.p) {
+        TRY(D.XR_own.alloc(sizeof(float) * D.n * D.d));
+        CK(cudaMemcpyAsync(D.XR_own.p, D.XR, sizeof(float) * D.n * D.d, cudaMemcpyDeviceToDevice, st));
+        D.XR = D.XR_own.as<float>();
+    }
+    if (D.csr) {
+        if (!D.indptr_own.p) {
+            TRY(D.indptr_own.alloc(sizeof(int64_t) * (D.n + 1)));
+            CK(cudaMemcpyAsync(D.indptr_own.p, D.indptr, sizeof(int64_t) * (D.n + 1), cudaMemcpyDeviceToDevice, st));
+            D.indptr = D.indptr_own.as<int64_t>();
+        }
+        if (!D.indices_own.p) {
+            TRY(D.indices_own.alloc(sizeof(int32_t) * std::max<int64_t>(D.nnz, 1)));
+            CK(cudaMemcpyAsync(D.indices_own.p, D.indices, sizeof(int32_t) * D.nnz, cudaMemcpyDeviceToDevice, st));
+            D.indices = D.indices_own.as<int32_t>();
+        }
+        if (!D.vals_own.p) {
+            TRY(D.vals_own.alloc(sizeof(float) * std::max<int64_t>(D.nnz, 1)));
+            CK(cudaMemcpyAsync(D.vals_own.p, D.vals, sizeof(float) * D.nnz, cudaMemcpyDeviceToDevice, st));
+            D.vals = D.vals_own.as<float>();
+        }
+    }
+    return SVM_OK;
+}
+
 // ================================================================ one binary problem (Eq. 2)
 struct Exchange {
     int L = 0, nbuf = 0;         // CTA lists per rank; buffers (1, or the virtual ranks of a launch)
@@ -1780,6 +1810,7 @@ extern "C" int svm_batch_create(const float* X, const float* Y, int32_t nprob, i
     B->prm = *params;
     B->st = (cudaStream_t)params->stream;
     int rc = build_dense(B->D, X, n, d, params->layout, pick_nblk(n), B->st);
+    if (rc == SVM_OK) rc = own_inputs(B->D, B->st);
     std::vector<float> yh;
     if (rc == SVM_OK) rc = to_host(yh, Y, (int64_t)nprob * n, B->st);
     if (rc == SVM_OK) {
@@ -1887,6 +1918,7 @@ extern "C" int svm_solver_create(const float* X, const float* y, int64_t n, int6
     S->prm = *params;
     S->st = (cudaStream_t)params->stream;
     int rc = build_dense(S->D, X, n, d, params->layout, pick_nblk(n), S->st);
+    if (rc == SVM_OK) rc = own_inputs(S->D, S->st);
     if (rc == SVM_OK) rc = solver_create_common(S, y, params);
     if (rc != SVM_OK) { delete S; return rc; }
     *out = S;
@@ -1906,6 +1938,7 @@ extern "C" int svm_solver_create_csr(const int64_t* indptr, const int32_t* indic
     S->prm = *params;
     S->st = (cudaStream_t)params->stream;
     int rc = build_csr(S->D, indptr, indices, data, n, d, pick_nblk(n), S->st);
+    if (rc == SVM_OK) rc = own_inputs(S->D, S->st);
     if (rc == SVM_OK) rc = solver_create_common(S, y, params);
     if (rc != SVM_OK) { delete S; return rc; }
     *out = S;

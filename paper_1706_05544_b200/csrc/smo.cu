@@ -429,6 +429,8 @@ struct SmoShared {
     int32_t rk_src[2][SVM_MAX_RANKS * 8];
     int32_t nw, nr, stop, timeout, next_chunk, next_chunk2, inner_steps, sub_done;
     int32_t c_slot[SVM_WS], c_ins[SVM_WS], c_mode;   // kernel-column cache (8(f) #3): per W row
+    int32_t c_off, c_wh, c_rh, c_rl;     // cache switched off; cache passes, row hits and lookups
+                                         // in the current window
     alignas(8) uint64_t mb_full[8], mb_empty[8];   // wide-mode / TMA-ring pipeline barriers
     uint64_t tma_seq[8];                 // TMA ring: chunk sequence number last issued into each slot
     double m_up, M_low;
@@ -1056,6 +1058,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             for (int T = 0; T < NS; ++T) tma_issue((uint64_t)T);
     }
 
+    if (tid == 0) { sh.c_off = 0; sh.c_wh = 0; sh.c_rh = 0; sh.c_rl = 0; sh.c_mode = 0; }   // (read after the prologue's barriers)
+
     // ---- end of a pass: warp lists -> CTA top-8 up / low ---------------------------------------
     auto finish_lists = [&](uint64_t wlu, uint64_t wll) {
         if (lane < 8) {
@@ -1429,7 +1433,10 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 sh.next_chunk2 = 0;
                 sh.sub_done = 0;
             }
-            if (a.cache_slots > 0) {
+            if (a.cache_slots > 0 && sh.c_off) {   // switched off: plain passes, no inserts
+                if (lane < SVM_WS) { sh.c_slot[lane] = -1; sh.c_ins[lane] = -1; }
+                if (lane == 0) sh.c_mode = 0;
+            } else if (a.cache_slots > 0) {
                 // ---- kernel-column cache: this CTA's 4-way set-associative LRU of
                 // K(x_i, x_r) columns over its rows.  Every CTA takes the same decisions from the
                 // same W sequence; tags and stamps are per CTA (global, L1-resident).  A hit
@@ -1486,6 +1493,18 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 }
                 if (lane == 0) {
                     sh.c_mode = allhit ? 2 : 1;
+                    // the cache switches itself off when it does not pay: a row hit rate below 20%
+                    // in a window of 2048 iterations, or fewer than 1% cache passes in a window
+                    // from iteration 8192 on (c5: a 940k-SV active set, 1,600 affordable columns,
+                    // 0.5% row hits, no cache pass) -- the same decision in every CTA (the same W
+                    // history)
+                    sh.c_wh += allhit ? 1 : 0;
+                    sh.c_rh += __popc(hm);
+                    sh.c_rl += nrr;
+                    if (((t + 1) & 2047) == 0) {
+                        if (sh.c_rh * 5 < sh.c_rl || (t + 1 >= 8192 && sh.c_wh * 100 < 2048)) sh.c_off = 1;
+                        sh.c_wh = sh.c_rh = sh.c_rl = 0;
+                    }
                     if (reporter) {
                         a.info->cache_lookups += nrr;
                         a.info->cache_hits += __popc(hm);
