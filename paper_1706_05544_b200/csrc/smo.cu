@@ -1493,16 +1493,17 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 }
                 if (lane == 0) {
                     sh.c_mode = allhit ? 2 : 1;
-                    // the cache switches itself off when it does not pay: a row hit rate below 20%
-                    // in a window of 2048 iterations, or fewer than 1% cache passes in a window
-                    // from iteration 8192 on (c5: a 940k-SV active set, 1,600 affordable columns,
-                    // 0.5% row hits, no cache pass) -- the same decision in every CTA (the same W
-                    // history)
+                    // the cache switches itself off when it cannot pay: from iteration 8192 on,
+                    // a 2048-iteration window with a row hit rate below 5% (c5: a 940k-SV active
+                    // set, 1,600 affordable columns, 0.5% row hits; c4: > 20% already while the
+                    // cache fills, 72% overall -- its cache passes only start once the active set
+                    // shrinks, so their rate is no early criterion) -- the same decision in every
+                    // CTA (the same W history)
                     sh.c_wh += allhit ? 1 : 0;
                     sh.c_rh += __popc(hm);
                     sh.c_rl += nrr;
                     if (((t + 1) & 2047) == 0) {
-                        if (sh.c_rh * 5 < sh.c_rl || (t + 1 >= 8192 && sh.c_wh * 100 < 2048)) sh.c_off = 1;
+                        if (t + 1 >= 8192 && sh.c_rh * 20 < sh.c_rl) sh.c_off = 1;
                         sh.c_wh = sh.c_rh = sh.c_rl = 0;
                     }
                     if (reporter) {
