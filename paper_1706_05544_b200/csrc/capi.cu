@@ -694,7 +694,8 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
             smem = base + (int)(8 * 4 * kc * Rs);
         }
     }
-    if (smem > 220 * 1024)
+    const int dyn_cap = smo_dyn_smem_cap(a);   // (opt-in maximum - this variant's static SmoShared)
+    if (smem > dyn_cap)
         return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d + %d lists)",
                     smem, (long long)D.d, a.nblk, a.world);
     // dense (non-wide, non-TMA) chunks of fewer than 32 rpt rows (SVMB200_CHUNK_ROWS = rows, a
@@ -737,7 +738,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     {   // buffer the dot products of as many rows as fit (64 B per row), whole chunks only
         const int64_t chunk = 32 * a.rpt;
         const int64_t all_rows = (D.rows_per_cta + chunk - 1) / chunk * chunk;
-        const int64_t avail = 210 * 1024 - smem;
+        const int64_t avail = std::min<int64_t>(210 * 1024, dyn_cap) - smem;
         int64_t rows = avail / 64;
         rows = std::min<int64_t>(rows, all_rows);
         rows = rows / chunk * chunk;
@@ -1290,28 +1291,84 @@ static int solve_batched(const Data& D, std::vector<Problem>& probs, const svm_p
     };
     CK(cudaEventRecord(e0, st));
     TRY(timed_pass());   // candidates of the initial state (all coefficients 0)
-    std::vector<int32_t> dh(P);
+    // Active-problem compaction: at every host poll, problems that stopped leave the batch -- their
+    // final counters are kept on the host, the others move to the leading slots (per-slot state,
+    // candidate lists, pointers, gamma / C), and the next launches run with N = 16 x active MMA
+    // columns and only the active problems' epilogues.  Each problem's arithmetic is unchanged.
+    std::vector<int> orig(P);          // original problem of each slot
+    for (int p = 0; p < P; ++p) orig[p] = p;
+    std::vector<int32_t> dh(P), fin_done(P, 0);
+    std::vector<int64_t> ih(P), fin_iters(P, 0), inh(P), fin_inner(P, 0);
+    std::vector<double> uh(P), lh(P), fin_up(P, 0.0), fin_low(P, 0.0);
+    const bool compact_ok = getenv("SVMB200_NO_COMPACT") == nullptr;
+    const size_t cand_block = (size_t)2 * a.nct * 8;   // u64 keys per problem slot
     for (int64_t it = 0; it <= a.max_iter; ++it) {
         CK(launch_ovr_solve(a, st));
         TRY(timed_pass());
         if ((it % POLL) == POLL - 1) {   // host poll of the done flags
-            CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+            const int PA = a.P;
+            CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * PA, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             drain();
-            bool all = true;
-            for (int p = 0; p < P; ++p) all = all && dh[p];
-            if (all) break;
+            int active = 0;
+            for (int q = 0; q < PA; ++q) active += dh[q] ? 0 : 1;
+            if (active == 0) break;
+            if (compact_ok && active < PA) {
+                CK(cudaMemcpyAsync(ih.data(), a.iters, sizeof(int64_t) * PA, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(uh.data(), a.mup, sizeof(double) * PA, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(lh.data(), a.mlow, sizeof(double) * PA, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(inh.data(), a.inner_total, sizeof(int64_t) * PA, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                std::vector<int> norig;
+                std::vector<int64_t> ni, nin;
+                std::vector<double> nu, nl;
+                for (int q = 0; q < PA; ++q) {
+                    const int o = orig[q];
+                    if (dh[q]) {   // finished: keep its final counters
+                        fin_done[o] = 1; fin_iters[o] = ih[q]; fin_up[o] = uh[q]; fin_low[o] = lh[q];
+                        fin_inner[o] = inh[q];
+                        continue;
+                    }
+                    const int nq = (int)norig.size();
+                    if (nq != q)   // candidate lists of the last pass follow their problem
+                        CK(cudaMemcpyAsync(a.cand + (size_t)nq * cand_block, a.cand + (size_t)q * cand_block,
+                                           sizeof(uint64_t) * cand_block, cudaMemcpyDeviceToDevice, st));
+                    norig.push_back(o);
+                    ni.push_back(ih[q]); nin.push_back(inh[q]); nu.push_back(uh[q]); nl.push_back(lh[q]);
+                    a.alpha[nq] = probs[o].alpha.as<double>();
+                    a.G[nq] = probs[o].G.as<float>();
+                    a.status[nq] = probs[o].status.as<uint8_t>();
+                    a.Cp[nq] = probs[o].C;
+                    a.kpp[nq] = probs[o].kp;
+                }
+                std::vector<int32_t> zd(active, 0);
+                CK(cudaMemcpyAsync(a.done, zd.data(), sizeof(int32_t) * active, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(a.iters, ni.data(), sizeof(int64_t) * active, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(a.inner_total, nin.data(), sizeof(int64_t) * active, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(a.mup, nu.data(), sizeof(double) * active, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(a.mlow, nl.data(), sizeof(double) * active, cudaMemcpyHostToDevice, st));
+                CK(cudaStreamSynchronize(st));
+                orig = norig;
+                a.P = active;
+                a.NU = 16 * active;
+            }
         }
     }
     CK(launch_ovr_solve(a, st));   // stop tests of the final state
     CK(cudaEventRecord(e1, st));
-    std::vector<int64_t> ih(P);
-    std::vector<double> uh(P), lh(P);
-    CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(ih.data(), a.iters, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(uh.data(), a.mup, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(lh.data(), a.mlow, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    {
+        const int PA = a.P;
+        CK(cudaMemcpyAsync(dh.data(), a.done, sizeof(int32_t) * PA, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ih.data(), a.iters, sizeof(int64_t) * PA, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(uh.data(), a.mup, sizeof(double) * PA, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(lh.data(), a.mlow, sizeof(double) * PA, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int q = 0; q < PA; ++q) {
+            const int o = orig[q];
+            fin_done[o] = dh[q]; fin_iters[o] = ih[q]; fin_up[o] = uh[q]; fin_low[o] = lh[q];
+        }
+        dh = fin_done; ih = fin_iters; uh = fin_up; lh = fin_low;
+    }
     drain();
     for (int k = 0; k < NEV; ++k)
         for (int j = 0; j < 2; ++j) cudaEventDestroy(pev[k][j]);

@@ -2553,19 +2553,34 @@ void smo_l2_restore()
     cudaGetLastError();
 }
 
-cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
+static const void* smo_pick(const SmoArgs& a)
 {
-    void* args[] = {const_cast<SmoArgs*>(&a)};
-    const void* fn;
     const bool rbf = a.kp.kernel == 2;
 #define SMO_PICK(CSR_, RPT_, XS_) \
     (rbf ? (const void*)smo_persistent<CSR_, RPT_, XS_, true> : (const void*)smo_persistent<CSR_, RPT_, XS_, false>)
-    if (a.XT == nullptr) fn = SMO_PICK(true, 1, false);
-    else if (a.x_in_smem)
-        fn = a.rpt == 4 ? SMO_PICK(false, 4, true) : a.rpt == 2 ? SMO_PICK(false, 2, true) : SMO_PICK(false, 1, true);
-    else
-        fn = a.rpt == 4 ? SMO_PICK(false, 4, false) : a.rpt == 2 ? SMO_PICK(false, 2, false) : SMO_PICK(false, 1, false);
+    if (a.XT == nullptr) return SMO_PICK(true, 1, false);
+    if (a.x_in_smem)
+        return a.rpt == 4 ? SMO_PICK(false, 4, true) : a.rpt == 2 ? SMO_PICK(false, 2, true) : SMO_PICK(false, 1, true);
+    return a.rpt == 4 ? SMO_PICK(false, 4, false) : a.rpt == 2 ? SMO_PICK(false, 2, false) : SMO_PICK(false, 1, false);
 #undef SMO_PICK
+}
+
+// Dynamic shared memory available to the persistent kernel variant `a` selects: the device's
+// per-block opt-in maximum minus that variant's static shared memory (SmoShared) and 1 KB of slack.
+int smo_dyn_smem_cap(const SmoArgs& a)
+{
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, smo_pick(a)) != cudaSuccess) { cudaGetLastError(); return 200 * 1024; }
+    return optin - (int)fa.sharedSizeBytes - 1024;
+}
+
+cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st)
+{
+    void* args[] = {const_cast<SmoArgs*>(&a)};
+    const void* fn = smo_pick(a);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};

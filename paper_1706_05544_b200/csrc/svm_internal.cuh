@@ -283,6 +283,7 @@ inline int svm_device_sms()
 }
 
 cudaError_t launch_smo(const SmoArgs& a, int smem_bytes, cudaStream_t st);
+int smo_dyn_smem_cap(const SmoArgs& a);   // dynamic shared memory the selected variant may use
 void smo_l2_restore();   // after the launch's loop: the caller's persisting-L2 limit back
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
 int smo_ring_bytes(int rpt);
