@@ -833,15 +833,17 @@ __device__ __forceinline__ int solve_subproblem(SmoShared& sh, int nw, double C,
         const uint32_t lu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32) == hu ? (uint32_t)ku : 0u);
         const uint32_t ll = __reduce_max_sync(FULL, (uint32_t)(kl >> 32) == hl ? (uint32_t)kl : 0u);
         const uint64_t mu = ((uint64_t)hu << 32) | lu, ml = ((uint64_t)hl << 32) | ll;
-        const int i = __ffs(__ballot_sync(FULL, ku == mu)) - 1;
-        const int j = __ffs(__ballot_sync(FULL, kl == ml)) - 1;
-        const double si = unmono64(mu), sj = -unmono64(ml);
-        if (mu == 0 || ml == 0 || si - sj <= inner_tol) break;
+        const int i = (__ffs(__ballot_sync(FULL, ku == mu)) - 1) & 15;
+        const int j = (__ffs(__ballot_sync(FULL, kl == ml)) - 1) & 15;
+        // the step's operands are loaded before the stop test (in bounds for any i, j < 16), so
+        // the shared-memory latency overlaps the test instead of following it
         const double ie = lds_f64(a_ie + 8u * (uint32_t)(i * SVM_WS + j));
         const double kai = lds_f64(a_krow + 8u * (uint32_t)i);
         const double kaj = lds_f64(a_krow + 8u * (uint32_t)j);
         // lim_i = room of i to move up, lim_j = room of j to move down
         const double lim_i = __shfl_sync(FULL, up_room, i), lim_j = __shfl_sync(FULL, dn_room, j);
+        const double si = unmono64(mu), sj = -unmono64(ml);
+        if (mu == 0 || ml == 0 || si - sj <= inner_tol) break;
         double t = (si - sj) * ie;
         const bool ci = t >= lim_i;
         t = ci ? lim_i : t;
@@ -906,6 +908,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Bulk prefetch of [p, p + bytes) into L2 (16-byte aligned address and size).
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // 2D tensor copy (TMA) of one box of the map into shared memory, completing on an mbarrier.
@@ -1604,7 +1612,11 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             const int kp = max(1, min(4, SMO_THREADS / max(npairs, 1)));
             const int klen = ((d + kp - 1) / kp + 3) & ~3;
             if (tid < npairs * kp) {
-                const int p = tid / kp, part = tid - p * kp;
+                // part-major: the lanes of a warp share one k range and walk consecutive pairs
+                // (same row r, columns s = r..15): broadcast / distinct-bank loads instead of the
+                // 3-way conflicts of pair-major parts (k offsets 36 x 16 floats apart hit one
+                // bank); each pair's per-part sums are unchanged (bit-identical)
+                const int part = tid / npairs, p = tid - part * npairs;
                 int r = 0, rem = p;
                 while (rem >= nr - r) { rem -= nr - r; ++r; }
                 const int sidx = r + rem;
@@ -1617,7 +1629,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                     const float* xs = sXW + sidx;
                     auto ld = [&](const float* x, int k) { return k < d ? (double)x[k * WS] : 0.0; };
                     if (a.kp.kernel == 2) {
-#pragma unroll 1
+#pragma unroll 2
                         for (int k = k0; k < k1; k += 4) {
                             const double t0 = ld(xr, k) - ld(xs, k), t1 = ld(xr, k + 1) - ld(xs, k + 1);
                             const double t2 = ld(xr, k + 2) - ld(xs, k + 2), t3 = ld(xr, k + 3) - ld(xs, k + 3);
@@ -1627,7 +1639,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                             acc3 = fma(t3, t3, acc3);
                         }
                     } else {
-#pragma unroll 1
+#pragma unroll 2
                         for (int k = k0; k < k1; k += 4) {
                             acc0 = fma(ld(xr, k), ld(xs, k), acc0);
                             acc1 = fma(ld(xr, k + 1), ld(xs, k + 1), acc1);
