@@ -482,19 +482,20 @@ def test_tiny_problems(n):
                                atol=1e-4)
 
 
-@pytest.mark.parametrize("nslice", ["1", "auto"])
-def test_wide_rows_streamed_sliced(nslice):
-    """d = 784 (c3's MNIST shape): X streamed from HBM, features split into slices whose partial
-    dot products are summed in slice order; same solution as the oracle either way."""
+@pytest.mark.parametrize("mode", ["wide", "slices"])
+def test_wide_rows_streamed_sliced(mode):
+    """d = 784 (c3's MNIST shape): X streamed from HBM either through the wide-mode bulk-copy
+    pipeline (the default for <= 448 rows per CTA) or, with it disabled, through the feature-slice
+    fallback (partial dot products summed in slice order); same solution as the oracle either way."""
     import os
     ds = synth.make("c3", n=1500)
     y = np.where(ds.y == ds.y[0], 1.0, -1.0).astype(np.float32)
-    if nslice != "auto":
-        os.environ["SVMB200_NSLICE"] = nslice
+    if mode == "slices":
+        os.environ["SVMB200_NO_WIDE"] = "1"
     try:
         m = pkg.train(ds.X, y, gamma=1.0 / ds.d)
     finally:
-        os.environ.pop("SVMB200_NSLICE", None)
+        os.environ.pop("SVMB200_NO_WIDE", None)
     om = ora.train(ds.X, y, gamma=1.0 / ds.d)
     r = om.results[0]
     assert m.info.converged == 1
