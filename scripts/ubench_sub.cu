@@ -127,6 +127,114 @@ __device__ int solve_v1(Sh& sh, int nw, double C, double inner_tol, int inner_ma
     return step;
 }
 
+__device__ int solve_v2(Sh& sh, int nw, double C, double inner_tol, int inner_max, int lane)
+{
+    const int pa = lane & 15;
+    const bool valid = lane < nw;
+    const int y = valid ? sh.w_y[lane] : 1;
+    double al = valid ? sh.w_alpha[lane] : 0.0;
+    double s = valid ? -(double)y * sh.w_G[lane] : 0.0;
+    const uint32_t a_ie = (uint32_t)__cvta_generic_to_shared(sh.inv_eta);
+    const uint32_t a_krow = (uint32_t)__cvta_generic_to_shared(sh.kpos + pa * 16);
+    // room to move "up" (y a increases) and "down"
+    double up_room = valid ? (y > 0 ? C - al : al) : 0.0;    // > 0 <=> in I_up
+    double dn_room = valid ? (y > 0 ? al : C - al) : 0.0;    // > 0 <=> in I_low
+    int step = 0;
+    for (; step < inner_max; ++step) {
+        const uint64_t ku = up_room > 0.0 ? mono64(s) : 0ull;
+        const uint64_t kl = dn_room > 0.0 ? mono64(-s) : 0ull;
+        const uint32_t hu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32));
+        const uint32_t hl = __reduce_max_sync(FULL, (uint32_t)(kl >> 32));
+        const uint32_t lu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32) == hu ? (uint32_t)ku : 0u);
+        const uint32_t ll = __reduce_max_sync(FULL, (uint32_t)(kl >> 32) == hl ? (uint32_t)kl : 0u);
+        const uint64_t mu = ((uint64_t)hu << 32) | lu, ml = ((uint64_t)hl << 32) | ll;
+        const int i = (__ffs(__ballot_sync(FULL, ku == mu)) - 1) & 15;
+        const int j = (__ffs(__ballot_sync(FULL, kl == ml)) - 1) & 15;
+        const double ie = lds_f64(a_ie + 8u * (uint32_t)(i * 16 + j));
+        const double kai = lds_f64(a_krow + 8u * (uint32_t)i);
+        const double kaj = lds_f64(a_krow + 8u * (uint32_t)j);
+        const double lim_i = __shfl_sync(FULL, up_room, i), lim_j = __shfl_sync(FULL, dn_room, j);
+        const double si = unmono64(mu), sj = -unmono64(ml);
+        if (mu == 0 || ml == 0 || si - sj <= inner_tol) break;
+        double t = (si - sj) * ie;
+        const bool ci = t >= lim_i;
+        t = ci ? lim_i : t;
+        const bool cj = t >= lim_j;
+        t = cj ? lim_j : t;
+        const bool clip_i = ci && (!cj || lim_i == lim_j);
+        if (lane == i) {
+            up_room = clip_i ? 0.0 : up_room - t;
+            dn_room = clip_i ? C : dn_room + t;
+        }
+        if (lane == j) {
+            dn_room = cj ? 0.0 : dn_room - t;
+            up_room = cj ? C : up_room + t;
+        }
+        s = fma(t, kaj - kai, s);
+    }
+    if (valid) al = y > 0 ? C - up_room : up_room;
+    if (lane < 16) sh.w_anew[lane] = al;
+    return step;
+}
+
+__device__ int solve_v3(Sh& sh, int nw, double C, double inner_tol, int inner_max, int lane)
+{
+    const int pa = lane & 15;
+    const bool valid = lane < nw;
+    const int y = valid ? sh.w_y[lane] : 1;
+    double al = valid ? sh.w_alpha[lane] : 0.0;
+    double s = valid ? -(double)y * sh.w_G[lane] : 0.0;
+    const uint32_t a_ie = (uint32_t)__cvta_generic_to_shared(sh.inv_eta);
+    const uint32_t a_krow = (uint32_t)__cvta_generic_to_shared(sh.kpos + pa * 16);
+    // room to move "up" (y a increases) and "down"
+    double up_room = valid ? (y > 0 ? C - al : al) : 0.0;    // > 0 <=> in I_up
+    double dn_room = valid ? (y > 0 ? al : C - al) : 0.0;    // > 0 <=> in I_low
+    int step = 0;
+    for (; step < inner_max; ++step) {
+        const uint64_t ku = up_room > 0.0 ? mono64(s) : 0ull;
+        const uint64_t kl = dn_room > 0.0 ? mono64(-s) : 0ull;
+        const uint32_t hu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32));
+        const uint32_t hl = __reduce_max_sync(FULL, (uint32_t)(kl >> 32));
+        const uint32_t bu = __ballot_sync(FULL, (uint32_t)(ku >> 32) == hu);
+        const uint32_t bl = __ballot_sync(FULL, (uint32_t)(kl >> 32) == hl);
+        uint32_t lu, ll;
+        if ((bu & (bu - 1)) == 0 && (bl & (bl - 1)) == 0) {   // unique high words (warp-uniform)
+            lu = __shfl_sync(FULL, (uint32_t)ku, __ffs(bu) - 1);
+            ll = __shfl_sync(FULL, (uint32_t)kl, __ffs(bl) - 1);
+        } else {
+            lu = __reduce_max_sync(FULL, (uint32_t)(ku >> 32) == hu ? (uint32_t)ku : 0u);
+            ll = __reduce_max_sync(FULL, (uint32_t)(kl >> 32) == hl ? (uint32_t)kl : 0u);
+        }
+        const uint64_t mu = ((uint64_t)hu << 32) | lu, ml = ((uint64_t)hl << 32) | ll;
+        const int i = (__ffs(__ballot_sync(FULL, ku == mu)) - 1) & 15;
+        const int j = (__ffs(__ballot_sync(FULL, kl == ml)) - 1) & 15;
+        const double ie = lds_f64(a_ie + 8u * (uint32_t)(i * 16 + j));
+        const double kai = lds_f64(a_krow + 8u * (uint32_t)i);
+        const double kaj = lds_f64(a_krow + 8u * (uint32_t)j);
+        const double lim_i = __shfl_sync(FULL, up_room, i), lim_j = __shfl_sync(FULL, dn_room, j);
+        const double si = unmono64(mu), sj = -unmono64(ml);
+        if (mu == 0 || ml == 0 || si - sj <= inner_tol) break;
+        double t = (si - sj) * ie;
+        const bool ci = t >= lim_i;
+        t = ci ? lim_i : t;
+        const bool cj = t >= lim_j;
+        t = cj ? lim_j : t;
+        const bool clip_i = ci && (!cj || lim_i == lim_j);
+        if (lane == i) {
+            up_room = clip_i ? 0.0 : up_room - t;
+            dn_room = clip_i ? C : dn_room + t;
+        }
+        if (lane == j) {
+            dn_room = cj ? 0.0 : dn_room - t;
+            up_room = cj ? C : up_room + t;
+        }
+        s = fma(t, kaj - kai, s);
+    }
+    if (valid) al = y > 0 ? C - up_room : up_room;
+    if (lane < 16) sh.w_anew[lane] = al;
+    return step;
+}
+
 template <int V>
 __global__ void bench(Sh* shs, int nprob, int* steps_out, long long* cyc_out, double C, double tol)
 {
@@ -139,7 +247,7 @@ __global__ void bench(Sh* shs, int nprob, int* steps_out, long long* cyc_out, do
             reinterpret_cast<double*>(&sh)[i] = reinterpret_cast<const double*>(&shs[p])[i];
         __syncwarp();
         long long t0 = clock64();
-        int st = V == 0 ? solve_v0(sh, 16, C, tol, 1024, threadIdx.x) : solve_v1(sh, 16, C, tol, 1024, threadIdx.x);
+        int st = V == 0 ? solve_v0(sh, 16, C, tol, 1024, threadIdx.x) : V == 1 ? solve_v1(sh, 16, C, tol, 1024, threadIdx.x) : V == 2 ? solve_v2(sh, 16, C, tol, 1024, threadIdx.x) : solve_v3(sh, 16, C, tol, 1024, threadIdx.x);
         __syncwarp();
         long long t1 = clock64();
         tot += t1 - t0;
@@ -177,16 +285,19 @@ int main()
     long long* dc;
     cudaMalloc(&ds, 4);
     cudaMalloc(&dc, 8);
-    double res[2][16];
-    for (int v = 0; v < 2; ++v) {
+    double res[4][16];
+    for (int v = 0; v < 4; ++v) {
         cudaMemcpy(d, h, sizeof(Sh) * NP, cudaMemcpyHostToDevice);
-        if (v == 0) bench<0><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
-        else bench<1><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+        auto run = [&]() {
+            if (v == 0) bench<0><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+            else if (v == 1) bench<1><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+            else if (v == 2) bench<2><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+            else bench<3><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+        };
+        run();
         cudaDeviceSynchronize();
-        if (v == 0) bench<0><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
         cudaMemcpy(d, h, sizeof(Sh) * NP, cudaMemcpyHostToDevice);
-        if (v == 0) bench<0><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
-        else bench<1><<<1, 32>>>(d, NP, ds, dc, 1.0, 1e-4);
+        run();
         int st; long long cy;
         cudaMemcpy(&st, ds, 4, cudaMemcpyDeviceToHost);
         cudaMemcpy(&cy, dc, 8, cudaMemcpyDeviceToHost);
@@ -195,7 +306,10 @@ int main()
         for (int a = 0; a < 16; ++a) res[v][a] = last.w_anew[a];
         printf("v%d: %d steps over %d problems, %.1f cycles/step\n", v, st, NP, (double)cy / st);
     }
-    double md = 0; for (int a = 0; a < 16; ++a) md = fmax(md, fabs(res[0][a] - res[1][a]));
-    printf("max |alpha_v0 - alpha_v1| = %g  err=%s\n", md, cudaGetErrorString(cudaGetLastError()));
+    for (int v = 1; v < 4; ++v) {
+        double md = 0; for (int a = 0; a < 16; ++a) md = fmax(md, fabs(res[0][a] - res[v][a]));
+        printf("max |alpha_v0 - alpha_v%d| = %g\n", v, md);
+    }
+    printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
