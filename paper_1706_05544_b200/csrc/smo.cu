@@ -1606,8 +1606,69 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         }   // X_W staged (once in pass-only mode)
         mark(2);
         wmark(-1);
-        // ---- K between the distinct W rows in fp64 (all threads, k split in up to 4 parts) ----
-        if (!a.pass_only) {
+        // ---- K between the distinct W rows in fp64 ---------------------------------------------
+        if (!CSR && !a.pass_only && a.qww_mma) {
+            // Gram X_W X_W^T on the fp64 tensor cores (mma.sync m8n8k4, as the batched solve):
+            // warps 0-5 = 3 8x8 tiles x 2 k-parts, operands promoted exactly from the fp32 tile,
+            // parts summed in a fixed order; RBF distance G_aa + G_bb - 2 G_ab clamped at 0
+            // (exactly 0 on the diagonal)
+            double* gpart = sh.qpart;                 // [2 parts][3 tiles][64]
+            double* gram = sh.kpos;                   // [16][16] (kpos is rebuilt from kr below)
+            const int dp4 = (d + 3) & ~3, nsteps = dp4 >> 2;
+            if (warp < 6) {
+                const int tl = warp >> 1, part = warp & 1;
+                const int I = tl == 2 ? 1 : 0, J = tl == 0 ? 0 : 1;
+                const int ra = I * 8 + (lane >> 2), rb = J * 8 + (lane >> 2), kk = lane & 3;
+                double c0 = 0.0, c1 = 0.0;
+                for (int st = part; st < nsteps; st += 2) {
+                    const int k = 4 * st + kk;
+                    const double a0 = k < d ? (double)sXW[k * SVM_WS + ra] : 0.0;
+                    const double b0 = k < d ? (double)sXW[k * SVM_WS + rb] : 0.0;
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(c0), "+d"(c1) : "d"(a0), "d"(b0));
+                }
+                gpart[(part * 3 + tl) * 64 + (lane >> 2) * 8 + (lane & 3) * 2] = c0;
+                gpart[(part * 3 + tl) * 64 + (lane >> 2) * 8 + (lane & 3) * 2 + 1] = c1;
+            }
+            __syncthreads();
+            if (tid < SVM_WS * SVM_WS) {
+                const int ra = tid >> 4, rb = tid & 15;
+                const bool sw = (ra >> 3) > (rb >> 3);
+                const int I = sw ? rb >> 3 : ra >> 3, J = sw ? ra >> 3 : rb >> 3;
+                const int tl = I == 0 ? (J == 0 ? 0 : 1) : 2;
+                const int e = sw ? (rb & 7) * 8 + (ra & 7) : (ra & 7) * 8 + (rb & 7);
+                gram[tid] = gpart[tl * 64 + e] + gpart[(3 + tl) * 64 + e];
+            }
+            __syncthreads();
+            wmark(6);
+            if (tid < SVM_WS * SVM_WS) {
+                const int ra = tid >> 4, rb = tid & 15;
+                if (ra < nr && rb < nr) {
+                    double dv = gram[tid];
+                    if (a.kp.kernel == 2) {
+                        dv = ra == rb ? 0.0 : gram[ra * 17] + gram[rb * 17] - 2.0 * gram[tid];
+                        dv = dv > 0.0 ? dv : 0.0;
+                    }
+                    sh.kr[tid] = kernel_fp64_from(dv, a.kp);
+                }
+            }
+            __syncthreads();
+            wmark(7);
+            if (tid < SVM_WS * SVM_WS) {
+                const int pa = tid >> 4, pb = tid & 15;
+                double kab = 0.0, ie = 0.0;
+                if (pa < nw && pb < nw) {
+                    const int sa = sh.w_slot[pa], sb = sh.w_slot[pb];
+                    kab = sh.kr[sa * SVM_WS + sb];
+                    const double eta = sh.kr[sa * SVM_WS + sa] + sh.kr[sb * SVM_WS + sb] - 2.0 * kab;
+                    ie = 1.0 / (eta < 1e-12 ? 1e-12 : eta);
+                }
+                sh.kpos[tid] = kab;
+                sh.inv_eta[tid] = ie;
+            }
+            __syncthreads();
+        } else if (!a.pass_only) {
+            // k-split pair sums from the fp32 tile (all threads, up to 4 parts per pair)
             const int npairs = nr * (nr + 1) / 2;
             const int kp = max(1, min(4, SMO_THREADS / max(npairs, 1)));
             const int klen = ((d + kp - 1) / kp + 3) & ~3;

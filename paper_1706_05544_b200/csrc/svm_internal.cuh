@@ -209,6 +209,7 @@ struct SmoArgs {
     // (dim 0 = rows, contiguous), box {32 RPT, min(d, 256)}.
     int32_t x_tma, tma_ns;
     int32_t chunk_rows;       // rows per warp work item (multiple of 4, <= 32 rpt; 0 = 32 rpt)
+    int32_t qww_mma;          // 1: K_WW from the fp64 tensor-core Gram (dense X)
     // kernel-column cache (SPEC KernelRowCache S:105-110): cache_slots columns of
     // K(x_i, x_r) over the local rows ([slot][n_pad] fp32), per-CTA 4-way set-associative LRU tags
     // and stamps ([nblk][cache_slots]); 0 slots = off
