@@ -1025,22 +1025,7 @@ static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_para
 static int solve_problem(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
                          cudaStream_t st)
 {
-    // The loop runs in chunks of max(2 m, 200,000) iterations; a chunk that ends unconverged is
-    // followed by a G refresh from the support vectors (the certification pass).  fp32 G drifts
-    // by ~sqrt(iterations) ulps, and at large n the extremes of that noise can keep the measured
-    // violation above a tight tolerance forever (c4 at tol 1e-4 ran to max_iter = 5,000,000
-    // without one); after a refresh the stop test sees the accurate G again.  Problems that
-    // converge within the first chunk (every BASELINE config at tol 1e-3) are unaffected.
-    const int64_t chunk = std::max<int64_t>(2 * D.n * P.ncopy, 200000);
-    for (;;) {
-        const int64_t left = P.max_iter - P.iterations;
-        if (left <= 0) break;
-        TRY(run_loop(D, P, E, std::min(left, chunk), st, nullptr));
-        if (P.converged || P.iterations >= P.max_iter || prm->certify == 0) break;
-        double viol = 0;
-        TRY(certify(D, P, &viol, st));
-        if (viol <= SVM_CERT_MARGIN * P.tol) { P.converged = true; break; }
-    }
+    TRY(run_loop(D, P, E, P.max_iter, st, nullptr));
     return certify_resume(D, P, E, prm, st);
 }
 
