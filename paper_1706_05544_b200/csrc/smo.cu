@@ -486,7 +486,8 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
 {
     // kmode (kernel-column cache): 0 = K from the dot products; 1 = the same, and
     // the columns of the W rows newly cached this iteration (sh.c_ins[r] >= 0) are stored into
-    // kc[slot][row]; 2 = every W row is cached: K read from kc[sh.c_slot[r]][row] (no X, no dots).
+    // kc[slot][row]; 2 = every W row is cached: K read from kc[sh.c_slot[r]][row] (no X, no dots);
+    // 3 = acc already holds those cached K values (copied to shared memory during phase A).
     // The stored values are exactly the ones the computing path uses, and S sums over r in the
     // same order either way, so all three modes give bit-identical G.
     if constexpr (RPT == 4) {
@@ -511,7 +512,12 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
         }
         float S[4] = {0.f, 0.f, 0.f, 0.f};
         const bool full = li0 + 4 <= cta_end;
-        if (do_update && kmode == 2) {
+        if (do_update && kmode == 3) {   // acc holds the cached K values (phase A copy)
+#pragma unroll
+            for (int r = 0; r < SVM_WS; ++r)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) S[j] = fmaf(sh.c[r], acc[j][r], S[j]);
+        } else if (do_update && kmode == 2) {
 #pragma unroll
             for (int r = 0; r < SVM_WS; ++r) {
                 const int sl = sh.c_slot[r];
@@ -605,7 +611,10 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
         ku[2 * j] = ku[2 * j + 1] = kl[2 * j] = kl[2 * j + 1] = 0ull;
         if (li >= cta_end) continue;
         float S = 0.0f;
-        if (do_update && kmode == 2) {
+        if (do_update && kmode == 3) {
+#pragma unroll
+            for (int r = 0; r < SVM_WS; ++r) S = fmaf(sh.c[r], acc[j][r], S);
+        } else if (do_update && kmode == 2) {
 #pragma unroll
             for (int r = 0; r < SVM_WS; ++r) {
                 const int sl = sh.c_slot[r];
@@ -1748,7 +1757,9 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         const int ks = nsl > 1 ? (d + nsl - 1) / nsl : d;
         const int kmode = a.cache_slots > 0 ? sh.c_mode : 0;   // kernel-column cache mode
         float* kcache = a.cache_data ? a.cache_data + (a.virt ? v.row0 : 0) : nullptr;
-        const int nitems = kmode == 2 ? 0 : (nsl > 1 ? nchunks * nsl : nbuf);   // cache pass: no dots
+        // cache pass: phase A copies the buffered chunks' cached K values into the dot buffer
+        // while the subproblem runs (HBM is otherwise idle then); no dots anywhere
+        const int nitems = kmode == 2 ? (nsl > 1 ? 0 : nbuf) : (nsl > 1 ? nchunks * nsl : nbuf);
         // ---- phase A: dot products x_i . X_W of the buffered chunks into shared memory --------
         auto phase_a = [&]() {
             for (;;) {
@@ -1764,7 +1775,24 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                 const int64_t lrow = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
                 const int64_t li0 = lane_on ? lrow : cta_end;   // idle lanes: past the CTA's rows
                 float acc[RPT][SVM_WS];
-                if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                if (kmode == 2) {   // the cached K columns of the W rows (K values, not dots)
+#pragma unroll
+                    for (int r = 0; r < SVM_WS; ++r) {
+                        const int csl = sh.c_slot[r];
+                        const float* src = kcache + (int64_t)(csl >= 0 ? csl : 0) * a.n_pad + li0;
+                        const bool ok = csl >= 0 && li0 < cta_end;
+                        if constexpr (RPT == 4) {
+                            const float4 kv = ok ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+                            acc[0][r] = kv.x; acc[1][r] = kv.y; acc[2][r] = kv.z; acc[3][r] = kv.w;
+                        } else if constexpr (RPT == 2) {
+                            const float2 kv = ok ? *reinterpret_cast<const float2*>(src) : make_float2(0.f, 0.f);
+                            acc[0][r] = kv.x; acc[1][r] = kv.y;
+                        } else {
+                            acc[0][r] = ok ? *src : 0.0f;
+                        }
+                    }
+                }
+                else if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
                 else if (tma) {
                     const uint64_t T = (uint64_t)t * nchunks + ch;
                     dots_tile<RPT>(tma_acquire(T), d, lane, sXW, acc);
@@ -1874,7 +1902,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         // ---- phase B / a3: epilogue of every chunk (buffered dots, or computed now) ----------
         // chunks [0, nA) have buffered dots; the streamed ones [nA, nchunks) are handed out
         // first so that their X reads start together and no streamed chunk forms the tail
-        const int nA = kmode == 2 ? 0 : (nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf));
+        const int nA = nitems == 0 ? 0 : (nsl > 1 ? nchunks : (sh.next_chunk < nbuf ? sh.next_chunk : nbuf));
         const int nS = nchunks - nA;
         for (;;) {
             int tk = 0;
@@ -1885,9 +1913,12 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             const int64_t lrow = cta_begin + (int64_t)ch * rows_per_chunk + lane * RPT;
             const int64_t li0 = lane_on ? lrow : cta_end;   // idle lanes: past the CTA's rows
             float acc[RPT][SVM_WS];
-            if (kmode == 2) {
+            int ekmode = kmode;   // the epilogue's kernel-value source
+            if (kmode == 2 && ch >= nA) {
                 zero_acc<RPT>(acc);   // (unused: K comes from the cache)
             } else if (ch < nA) {
+                if (kmode == 2) ekmode = 3;   // the buffer holds cached K values
+
                 const int lr = lane_on ? (int)(lrow - cta_begin) : 0;
 #pragma unroll
                 for (int r = 0; r < SVM_WS; ++r) {
@@ -1922,7 +1953,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             }
             wmark(0);
             uint64_t ku[2 * RPT], kl[2 * RPT];
-            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, true, acc, ku, kl, kmode, kcache);
+            row_epilogue<RPT, RBFK>(a, v, sh, li0, cta_end, true, acc, ku, kl, ekmode, kcache);
             wmark(2);
             merge_chunk_rows<RPT>(ku, kl, wlu, wll, lane, a.ncopy);
             wmark(3);
