@@ -96,3 +96,37 @@ def test_cross_validate_errors():
         binding.cross_validate(ds.X, ds.y, 3, fold=np.full(ds.n, 5, np.int32))
     with pytest.raises(pkg.SvmError):
         binding.cross_validate(ds.X, ds.y, 3, costs=[-1.0])
+
+
+def test_cross_validate_failed_fold_and_linear():
+    """a fold whose training split holds a single class fails and leaves the mean
+    (reported in `failed`); the linear kernel ignores gamma."""
+    rng = np.random.default_rng(5)
+    n = 60
+    X = rng.standard_normal((n, 3)).astype(np.float32)
+    y = np.where(np.arange(n) < 50, 1.0, -1.0).astype(np.float32)   # class -1 only in rows 50..59
+    fold = np.where(np.arange(n) >= 50, 0, 1 + np.arange(n) % 2).astype(np.int32)
+    res, dec = binding.cross_validate(X, y, 3, fold=fold, kernel="linear", decision=True)
+    assert res[0]["failed"] == 1 and res[0]["nfold"] == 3     # fold 0's training split: one class
+    # the other two folds: held-out decisions against the oracle's fold models; the metric is the
+    # mean accuracy of those decisions over the two folds that did not fail
+    accs = []
+    for f in (1, 2):
+        tr, he = np.nonzero(fold != f)[0], np.nonzero(fold == f)[0]
+        m = ora.train(X[tr], y[tr], kernel="linear")
+        fo = m.decision_function(X[he])[:, 0]
+        assert np.abs(dec[0, he, 0] - fo).max() <= 1e-3
+        accs.append(np.mean(np.where(dec[0, he, 0] > 0, 1.0, -1.0) == y[he]))
+    assert abs(res[0]["metric"] - np.mean(accs)) <= 1e-9
+
+
+def test_batch_solver_errors():
+    ds = synth.mnist_like(n=300, d=16, k=3)
+    Y = np.stack([np.where(ds.y == c, 1.0, -1.0) for c in range(3)]).astype(np.float32)
+    with pytest.raises(pkg.SvmError):
+        binding.BatchSolver(ds.X, Y[:1])                       # nprob < 2
+    with pytest.raises(pkg.SvmError):
+        binding.BatchSolver(ds.X, Y * 2.0)                     # labels not +-1
+    b = binding.BatchSolver(ds.X, Y)
+    with pytest.raises(pkg.SvmError):
+        b.set_state(0, np.full(300, 2.0), np.zeros(300, np.float32))   # alpha outside [0, C]
