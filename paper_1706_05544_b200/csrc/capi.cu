@@ -256,6 +256,8 @@ struct Data {
     int nblk = 0;
     bool csr = false;
     DBuf XT, XR_own, norms, indptr_own, indices_own, vals_own;
+    DBuf sell_idx, sell_val, sell_gptr;   // CSR in slices of 32 rows for the pass (build_sell)
+    int sell_spc = 0;
     const float* XR = nullptr;            // row-major rows (owned or borrowed)
     const int64_t* indptr = nullptr;      // CSR (owned or borrowed)
     const int32_t* indices = nullptr;
@@ -330,6 +332,36 @@ static int build_dense(Data& D, const float* X, int64_t n, int64_t d, int layout
     return SVM_OK;
 }
 
+// The pass's copy of a CSR matrix (SmoArgs::sell_*, layout.cu k_sell_fill): the rows of every
+// 32-row warp chunk of every CTA interleaved lane by lane in groups of 4 nonzeros, so that a warp
+// streams its chunk with coalesced 8- and 16-byte loads and no shared-memory staging.  Built for
+// the CTA geometry of D (a virtual-rank launch partitions the rows identically).  Column indices
+// are stored as u16 (the pass stages X_W^T [d][20] in shared memory, so d is far below 65536).
+static int build_sell(Data& D, cudaStream_t st)
+{
+    D.sell_spc = 0;
+    if (D.d > 65535 || getenv("SVMB200_CSR_STAGED")) return SVM_OK;   // per-warp staging path
+    const int spc = (int)((D.rows_per_cta + 31) / 32);
+    const int64_t ns = (int64_t)D.nblk * spc;
+    DBuf len;
+    TRY(len.alloc(sizeof(int64_t) * ns));
+    CK(lay_sell_len(D.indptr, D.n, D.rows_per_cta, spc, ns, len.as<int64_t>(), st));
+    std::vector<int64_t> h(ns + 1, 0);
+    CK(cudaMemcpyAsync(h.data() + 1, len.p, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < ns; ++i) h[i + 1] += h[i];
+    TRY(D.sell_gptr.alloc(sizeof(int64_t) * (ns + 1)));
+    CK(cudaMemcpyAsync(D.sell_gptr.p, h.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
+    const int64_t groups = std::max<int64_t>(h[ns], 1);
+    TRY(D.sell_idx.alloc(sizeof(uint2) * groups * 32));
+    TRY(D.sell_val.alloc(sizeof(float4) * groups * 32));
+    CK(lay_sell_fill(D.indptr, D.indices, D.vals, D.n, D.rows_per_cta, spc, ns,
+                     D.sell_gptr.as<int64_t>(), D.sell_idx.as<uint2>(), D.sell_val.as<float4>(), st));
+    CK(cudaStreamSynchronize(st));   // h is freed on return
+    D.sell_spc = spc;
+    return SVM_OK;
+}
+
 static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, const float* data,
                      int64_t n, int64_t d, int nblk, cudaStream_t st)
 {
@@ -368,7 +400,7 @@ static int build_csr(Data& D, const int64_t* indptr, const int32_t* indices, con
     TRY(check_bad_flag(bad, st, SVM_ENONFINITE, "X contains a non-finite value"));
     TRY(D.norms.alloc(sizeof(float) * D.n_pad));
     CK(lay_norms_csr(D.indptr, D.vals, n, D.n_pad, D.norms.as<float>(), st));
-    return SVM_OK;
+    return build_sell(D, st);
 }
 
 // Handles that outlive the call (svm_solver, svm_batch) must not keep the caller's device arrays
@@ -528,6 +560,12 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.peer_indptr[0] = D.indptr;
     a.peer_indices[0] = D.indices;
     a.peer_vals[0] = D.vals;
+    if (D.csr && D.sell_spc > 0) {
+        a.sell_idx = D.sell_idx.as<uint2>();
+        a.sell_val = D.sell_val.as<float4>();
+        a.sell_gptr = D.sell_gptr.as<int64_t>();
+        a.sell_spc = D.sell_spc;
+    }
     a.rank_rpc[0] = D.rows_per_cta;
     a.peer_xw[0] = E.buf(0);
     a.timeout_ns = 30ull * 1000000000ull;
@@ -661,7 +699,8 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         a.x_ring = (!D.csr && (a.rpt >= 2 || D.d >= 256)) ? 1 : 0;
         if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
         smem = smo_smem_bytes(D.d, a.world, a.nblk, 0) +
-               (D.csr ? smo_csr_stage_bytes() + smo_csr_w_extra_bytes(D.d)
+               (D.csr ? (a.sell_spc > 0 ? smo_sell_bytes(a.sell_spc) : smo_csr_stage_bytes()) +
+                            smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
         // dense rows of <= 256 features: the TMA ring (one tensor copy per 32 rpt-row chunk)
         // (opt-in, SVMB200_TMA=1: measured slower than the per-lane ring on c4)

@@ -402,6 +402,50 @@ __global__ void k_gather_global_sv(SvPeers P, int64_t nsv, int64_t nsv_pad, int6
     if (grow) grow[s] = P.row0[r] + li;
 }
 
+// ---- CSR in slices of 32 rows for the persistent pass (SmoArgs::sell_*) ---------
+// Slice s = g * spc + c holds the rows g R + 32 c + l (l < 32) of CTA g that exist (32 c + l < R
+// and row < n).  Its length is the longest of those rows in groups of 4 nonzeros.
+__global__ void k_sell_len(const int64_t* __restrict__ indptr, int64_t n, int64_t R, int spc,
+                           int64_t ns, int64_t* __restrict__ len)
+{
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    const int64_t g = s / spc, c = s - g * spc;
+    const int64_t r0 = g * R + 32 * c;
+    const int64_t r1 = min(min(r0 + 32, g * R + R), n);
+    int64_t m = 0;
+    for (int64_t r = r0; r < r1; ++r) m = max(m, indptr[r + 1] - indptr[r]);
+    len[s] = (m + 3) / 4;
+}
+
+// One warp per slice: lane l writes the nonzeros of its row, 4 per group, at
+// [(gptr[s] + j) * 32 + l] (column indices as u16, zero padding past the row's end).
+__global__ void k_sell_fill(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                            const float* __restrict__ vals, int64_t n, int64_t R, int spc,
+                            int64_t ns, const int64_t* __restrict__ gptr, uint2* __restrict__ sidx,
+                            float4* __restrict__ sval)
+{
+    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int64_t g = s / spc, c = s - g * spc;
+    const int64_t row = g * R + 32 * c + lane;
+    const bool on = 32 * c + lane < R && row < n;
+    const int64_t b = on ? indptr[row] : 0, e = on ? indptr[row + 1] : 0;
+    const int64_t g0 = gptr[s], ng = gptr[s + 1] - g0;
+    for (int64_t j = 0; j < ng; ++j) {
+        uint32_t k[4];
+        float v[4];
+        for (int u = 0; u < 4; ++u) {
+            const int64_t p = b + 4 * j + u;
+            k[u] = p < e ? (uint32_t)idx[p] : 0u;
+            v[u] = p < e ? vals[p] : 0.0f;
+        }
+        sidx[(g0 + j) * 32 + lane] = make_uint2(k[0] | (k[1] << 16), k[2] | (k[3] << 16));
+        sval[(g0 + j) * 32 + lane] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 inline unsigned nblocks(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 }  // namespace
@@ -420,6 +464,23 @@ cudaError_t lay_check_csr(const int64_t* indptr, const int32_t* idx, int64_t n, 
 {
     svm_note_launches(1);
     k_check_csr<<<nblocks(n, 256), 256, 0, st>>>(indptr, idx, n, d, nnz, d_bad);
+    return cudaGetLastError();
+}
+cudaError_t lay_sell_len(const int64_t* indptr, int64_t n, int64_t R, int spc, int64_t ns,
+                         int64_t* len, cudaStream_t st)
+{
+    if (ns <= 0) return cudaSuccess;
+    svm_note_launches(1);
+    k_sell_len<<<nblocks(ns, 256), 256, 0, st>>>(indptr, n, R, spc, ns, len);
+    return cudaGetLastError();
+}
+cudaError_t lay_sell_fill(const int64_t* indptr, const int32_t* idx, const float* vals, int64_t n,
+                          int64_t R, int spc, int64_t ns, const int64_t* gptr, uint2* sidx,
+                          float4* sval, cudaStream_t st)
+{
+    if (ns <= 0) return cudaSuccess;
+    svm_note_launches(1);
+    k_sell_fill<<<nblocks(ns * 32, 256), 256, 0, st>>>(indptr, idx, vals, n, R, spc, ns, gptr, sidx, sval);
     return cudaGetLastError();
 }
 cudaError_t lay_rowmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, int64_t n_pad,

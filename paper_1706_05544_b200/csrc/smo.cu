@@ -404,6 +404,78 @@ __device__ __forceinline__ void dots_csr_staged(const int64_t* __restrict__ indp
     __syncwarp();
 }
 
+// CSR pass from the slice copy (SmoArgs::sell_*, built once per training by layout.cu
+// k_sell_fill): lane l walks the nonzeros of its row 4 at a time from [(g0 + j) * 32 + l] --
+// coalesced 256-B index and 512-B value loads straight into registers, SELL_PF groups in flight
+// per lane, no shared-memory staging and no bank conflicts on the stage -- with the same per-row
+// order and masked X_W updates as dots_csr, so the sums are bit-identical to the staged path.
+constexpr int SELL_PF = 4;
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void dots_sell(const uint2* __restrict__ gi, const float4* __restrict__ gv,
+                                          int ng, int cnt, const float* sXW, float (&acc)[1][SVM_WS])
+{
+    zero_acc<1>(acc);
+    const uint32_t wsm = (uint32_t)__cvta_generic_to_shared(sXW);   // X_W^T [d][WSTR_CSR] fp32
+    uint2 ri[SELL_PF];
+    float4 rv[SELL_PF];
+#pragma unroll
+    for (int p = 0; p < SELL_PF; ++p) {
+        ri[p] = make_uint2(0u, 0u);
+        rv[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (p < ng) { ri[p] = __ldcs(gi + p * 32); rv[p] = __ldcs(gv + p * 32); }
+    }
+    for (int j0 = 0; j0 < ng; j0 += SELL_PF) {
+#pragma unroll
+        for (int p = 0; p < SELL_PF; ++p) {
+            const int j = j0 + p;
+            if (j < ng) {
+                const uint2 ci = ri[p];
+                const float4 cv = rv[p];
+                if (j + SELL_PF < ng) {
+                    ri[p] = __ldcs(gi + (j + SELL_PF) * 32);
+                    rv[p] = __ldcs(gv + (j + SELL_PF) * 32);
+                }
+                const int kk[4] = {(int)(ci.x & 0xffffu), (int)(ci.x >> 16), (int)(ci.y & 0xffffu), (int)(ci.y >> 16)};
+                const float vv[4] = {cv.x, cv.y, cv.z, cv.w};
+                // the 4 group masks first (no branch between them: the loads issue together);
+                // a nonzero past the row's end gets mask 0, i.e. no update
+                uint32_t m[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    m[u] = lds_u32(wsm + 4u * (uint32_t)csr_mask_slot(kk[u])) & (4 * j + u < cnt ? 0xffffu : 0u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t wk = wsm + 4u * WSTR_CSR * (uint32_t)kk[u];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (m[u] & (0xFu << (4 * q))) {   // as fma_row16_masked
+                            const float4 w = lds_f4(wk + 16u * q);
+                            const float2 xx = make_float2(vv[u], vv[u]);
+                            const float2 lo = __ffma2_rn(xx, make_float2(w.x, w.y), make_float2(acc[0][4 * q], acc[0][4 * q + 1]));
+                            const float2 hi = __ffma2_rn(xx, make_float2(w.z, w.w), make_float2(acc[0][4 * q + 2], acc[0][4 * q + 3]));
+                            acc[0][4 * q] = lo.x;
+                            acc[0][4 * q + 1] = lo.y;
+                            acc[0][4 * q + 2] = hi.x;
+                            acc[0][4 * q + 3] = hi.y;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 // Shared state of one persistent CTA (static part; X_W, the staged keys, the score arrays and
 // the optional X slice are dynamic).
 struct SmoShared {
@@ -623,17 +695,24 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
         } else if (do_update) {
             const float xn = xnv[j];
             const float ng = -a.kp.gamma * 1.4426950408889634f;  // exp(z) = 2^(z log2 e)
-#pragma unroll
-            for (int r = 0; r < SVM_WS; ++r) {
-                float K;
+            auto kval = [&](int r) -> float {
                 if constexpr (RBFK) {  // exp(-gamma |x_i - x_r|^2) with the distance from the norms
                     const float d2 = fmaxf(fmaf(-2.0f, acc[j][r], xn + sh.xn[r]), 0.0f);
-                    K = exp2f_approx(ng * d2);
+                    return exp2f_approx(ng * d2);
                 } else {
-                    K = kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]);
+                    return kernel_from_dot(a.kp, acc[j][r], xn, sh.xn[r]);
                 }
-                S = fmaf(sh.c[r], K, S);
-                if (kmode == 1 && sh.c_ins[r] >= 0) kc[(int64_t)sh.c_ins[r] * a.n_pad + li] = K;
+            };
+            if (kmode == 1) {   // cache inserts of the new W columns (same S order as below)
+#pragma unroll
+                for (int r = 0; r < SVM_WS; ++r) {
+                    const float K = kval(r);
+                    S = fmaf(sh.c[r], K, S);
+                    if (sh.c_ins[r] >= 0) kc[(int64_t)sh.c_ins[r] * a.n_pad + li] = K;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < SVM_WS; ++r) S = fmaf(sh.c[r], kval(r), S);
             }
         }
 #pragma unroll
@@ -953,6 +1032,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     float* sX = reinterpret_cast<float*>(sKL + (size_t)L * 8);               // [d][R] (XS)
     // dot-product buffer: [16][dbuf_rows] fp32, column r holds x_i . x_{W_r} for the CTA's first
     // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
+    const bool sell = CSR && a.sell_idx != nullptr;   // CSR from the slice copy (no staging)
+    int32_t* sGp = reinterpret_cast<int32_t*>(sX);     // SELL: [spc + 1] group offsets of this CTA
     float* csr_val = sX + (size_t)warp * CSR_CAP;                                   // CSR only
     uint16_t* csr_idx = reinterpret_cast<uint16_t*>(sX + (size_t)SMO_WARPS * CSR_CAP) + (size_t)warp * CSR_CAP;
     // TMA ring (streamed dense X, a.x_tma): tma_ns slots of [d][32 RPT] fp32, 128-byte aligned
@@ -963,7 +1044,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     float* tring = reinterpret_cast<float*>(dyn_smem + ((smem_u32(sX) + 127u) & ~127u) - smem_u32(dyn_smem));
     const uint32_t stage_floats = (uint32_t)d * CH;
     float* sDot = tma ? tring + (size_t)NS * stage_floats
-                      : sX + (XS ? (size_t)d * R : (CSR ? (size_t)SMO_WARPS * CSR_CAP * 6 / 4 : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
+                      : sX + (XS ? (size_t)d * R : (CSR ? (sell ? (size_t)((a.sell_spc + 4) & ~3) : (size_t)SMO_WARPS * CSR_CAP * 6 / 4)
+                                                        : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
     const int64_t cta_begin = (int64_t)v.cta * a.rows_per_cta;
@@ -995,6 +1077,24 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
             for (int r = lane; r < R; r += 32)
                 sX[(size_t)k * R + r] = v.XT[(int64_t)k * a.n_pad + cta_begin + r];
     }
+    // SELL CSR: this CTA's slice offsets, relative to its first group (constant for the training)
+    int64_t sell_g0 = 0;
+    if (sell) {
+        const int64_t* gp = a.sell_gptr + ((a.virt ? (int64_t)v.rank * a.nblk : 0) + v.cta) * a.sell_spc;
+        sell_g0 = gp[0];
+        for (int c = tid; c <= a.sell_spc; c += SMO_THREADS) sGp[c] = (int32_t)(gp[c] - sell_g0);
+        __syncthreads();
+    }
+    auto csr_dots = [&](int ch, int64_t li0, float (&acc)[1][SVM_WS]) {
+        if (sell) {
+            const int64_t g0 = sell_g0 + sGp[ch];
+            const int cnt = li0 < cta_end ? (int)(v.indptr[li0 + 1] - v.indptr[li0]) : 0;
+            dots_sell(a.sell_idx + g0 * 32 + lane, a.sell_val + g0 * 32 + lane, sGp[ch + 1] - sGp[ch],
+                      cnt, sXW, acc);
+        } else {
+            dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+        }
+    };
     const float* xbase = XS ? sX : v.XT + cta_begin;
     const int64_t xld = XS ? R : a.n_pad;
     // per-lane cp.async ring for streamed X (in the place of the resident slice)
@@ -1792,7 +1892,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                         }
                     }
                 }
-                else if constexpr (CSR) dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                else if constexpr (CSR) csr_dots(ch, li0, acc);
                 else if (tma) {
                     const uint64_t T = (uint64_t)t * nchunks + ch;
                     dots_tile<RPT>(tma_acquire(T), d, lane, sXW, acc);
@@ -1941,7 +2041,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                             acc[j][r] += sDot[(size_t)(q * SVM_WS + r) * dbuf_rows + lr + j];
                 }
             } else if constexpr (CSR) {
-                dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
+                csr_dots(ch, li0, acc);
             } else if (tma) {
                 const uint64_t T = (uint64_t)t * nchunks + ch;
                 dots_tile<RPT>(tma_acquire(T), d, lane, sXW, acc);
@@ -2633,6 +2733,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
 
 int smo_ring_bytes(int rpt) { return SMO_THREADS * 4 * rpt * (rpt == 1 ? pf_x<1>() : rpt == 2 ? pf_x<2>() : pf_x<4>()); }
 int smo_csr_stage_bytes() { return SMO_WARPS * CSR_CAP * 6; }
+int smo_sell_bytes(int spc) { return 4 * ((spc + 4) & ~3); }
 int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS)); }
 
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)

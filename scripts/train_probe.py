@@ -12,7 +12,11 @@ from paper_1706_05544_b200 import synth  # noqa: E402
 cfg = os.environ.get("SWEEP_CFG", "c4")
 it = int(os.environ.get("ITERS", "3000"))
 ds = synth.make(cfg)
-m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), gamma=1.0 / ds.d,
-              svm_type="eps-regression" if ds.svm_type == 3 else "C-classification",
-              max_iter=it, certify=0)
+kw = dict(gamma=1.0 / ds.d, svm_type="eps-regression" if ds.svm_type == 3 else "C-classification",
+          max_iter=it, certify=0)
+if ds.is_csr:
+    m = pkg.train_csr(*(torch.from_numpy(v).cuda() for v in (ds.indptr, ds.indices, ds.data)),
+                      torch.from_numpy(ds.y).cuda(), ds.d, **kw)
+else:
+    m = pkg.train(torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda(), **kw)
 print(f"{cfg}: {m.info.iterations} iterations, loop {m.info.loop_ms:.1f} ms, cache passes {m.info.cache_passes}")

@@ -245,6 +245,30 @@ def test_column_cache_bit_identical(case):
         assert st1.cache_passes > 0
 
 
+@pytest.mark.parametrize("n,vr", [(20000, 1), (9000, 1), (30000, 2)])
+def test_csr_slice_copy_bit_identical(n, vr):
+    """The CSR pass streams each 32-row chunk from the library's slice copy (SmoArgs::sell_*,
+    DESIGN.md §4) instead of staging the chunk's nonzeros through shared memory: same per-row
+    order and masked updates, so alpha, G and the iteration count are bit-identical to the staged
+    path (SVMB200_CSR_STAGED=1), with one rank and with virtual ranks (global CTA slices)."""
+    ds = synth.make("c5", n=n)
+    sp = (ds.indptr, ds.indices, ds.data)
+
+    def run(staged):
+        ev = dict(SVMB200_CSR_STAGED=1) if staged else {}
+        with env(**ev):
+            s = pkg.Solver(csr=sp, y=ds.y, d=ds.d, gamma=1.0 / ds.d)
+        if vr > 1:
+            s.set_ranks(vr)
+        st = s.run(3000)
+        return st, s.get_state()
+    st0, (a0, g0) = run(True)
+    st1, (a1, g1) = run(False)
+    assert st1.iterations == st0.iterations > 0
+    np.testing.assert_array_equal(a1, a0)
+    np.testing.assert_array_equal(g1, g0)
+
+
 @pytest.mark.parametrize("n,d,P", [(1100, 40, 3), (700, 200, 4)])
 def test_batched_pass_one_step_vs_oracle(n, d, P):
     """one batched iteration (k_ovr_solve + the tcgen05 k_ovr_pass with 3 fp16-split
@@ -278,3 +302,27 @@ def test_batched_pass_one_step_vs_oracle(n, d, P):
         Gref = ora.gradient_update(ds.X, probs[p], ks, W, dA[W], G32.astype(np.float64))
         err = np.abs(Gg - Gref) / np.maximum(1.0, np.abs(Gref))
         assert err.max() <= 1e-5, (p, err.max())
+
+
+def test_process_state_restored_after_training():
+    """The library raises the persisting-L2 set-aside for its own launch only (DESIGN.md §4
+    "Process-wide state"): after training and predicting, the caller's limit is back, and a second
+    model trained in the same process on the same data gives the same result (no stale scratch)."""
+    import torch
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:
+        from cuda import cudart as rt
+    lim = rt.cudaLimit.cudaLimitPersistingL2CacheSize
+    err, before = rt.cudaDeviceGetLimit(lim)
+    assert int(err) == 0
+    ds = synth.make("c4", n=20000)
+    X, y = torch.from_numpy(ds.X).cuda(), torch.from_numpy(ds.y).cuda()
+    m1 = pkg.train(X, y, gamma=1.0 / ds.d)
+    f1 = m1.predict(ds.X[:500], decision=True)[1]
+    err, after = rt.cudaDeviceGetLimit(lim)
+    assert int(err) == 0 and after == before, (before, after)
+    m2 = pkg.train(X, y, gamma=1.0 / ds.d)
+    f2 = m2.predict(ds.X[:500], decision=True)[1]
+    assert m1.info.iterations == m2.info.iterations
+    np.testing.assert_array_equal(f1, f2)
