@@ -340,7 +340,7 @@ static int build_dense(Data& D, const float* X, int64_t n, int64_t d, int layout
 static int build_sell(Data& D, cudaStream_t st)
 {
     D.sell_spc = 0;
-    if (D.d > 65535 || getenv("SVMB200_CSR_STAGED")) return SVM_OK;   // per-warp staging path
+    if (D.d > 65534 || getenv("SVMB200_CSR_STAGED")) return SVM_OK;   // per-warp staging path
     const int spc = (int)((D.rows_per_cta + 31) / 32);
     const int64_t ns = (int64_t)D.nblk * spc;
     DBuf len;
@@ -355,7 +355,7 @@ static int build_sell(Data& D, cudaStream_t st)
     const int64_t groups = std::max<int64_t>(h[ns], 1);
     TRY(D.sell_idx.alloc(sizeof(uint2) * groups * 32));
     TRY(D.sell_val.alloc(sizeof(float4) * groups * 32));
-    CK(lay_sell_fill(D.indptr, D.indices, D.vals, D.n, D.rows_per_cta, spc, ns,
+    CK(lay_sell_fill(D.indptr, D.indices, D.vals, D.n, D.d, D.rows_per_cta, spc, ns,
                      D.sell_gptr.as<int64_t>(), D.sell_idx.as<uint2>(), D.sell_val.as<float4>(), st));
     CK(cudaStreamSynchronize(st));   // h is freed on return
     D.sell_spc = spc;
@@ -699,7 +699,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         a.x_ring = (!D.csr && (a.rpt >= 2 || D.d >= 256)) ? 1 : 0;
         if (const char* e = getenv("SVMB200_XRING")) a.x_ring = (!D.csr && atoi(e)) ? 1 : 0;
         smem = smo_smem_bytes(D.d, a.world, a.nblk, 0) +
-               (D.csr ? (a.sell_spc > 0 ? smo_sell_bytes(a.sell_spc) : smo_csr_stage_bytes()) +
+               (D.csr ? (a.sell_spc > 0 ? smo_sell_bytes(a.sell_spc, D.d) : smo_csr_stage_bytes()) +
                             smo_csr_w_extra_bytes(D.d)
                       : smo_ring_bytes(a.rpt));
         // dense rows of <= 256 features: the TMA ring (one tensor copy per 32 rpt-row chunk)

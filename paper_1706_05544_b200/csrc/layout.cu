@@ -419,9 +419,9 @@ __global__ void k_sell_len(const int64_t* __restrict__ indptr, int64_t n, int64_
 }
 
 // One warp per slice: lane l writes the nonzeros of its row, 4 per group, at
-// [(gptr[s] + j) * 32 + l] (column indices as u16, zero padding past the row's end).
+// [(gptr[s] + j) * 32 + l] (column indices as u16; past the row's end index d and value 0).
 __global__ void k_sell_fill(const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
-                            const float* __restrict__ vals, int64_t n, int64_t R, int spc,
+                            const float* __restrict__ vals, int64_t n, int64_t d, int64_t R, int spc,
                             int64_t ns, const int64_t* __restrict__ gptr, uint2* __restrict__ sidx,
                             float4* __restrict__ sval)
 {
@@ -438,7 +438,7 @@ __global__ void k_sell_fill(const int64_t* __restrict__ indptr, const int32_t* _
         float v[4];
         for (int u = 0; u < 4; ++u) {
             const int64_t p = b + 4 * j + u;
-            k[u] = p < e ? (uint32_t)idx[p] : 0u;
+            k[u] = p < e ? (uint32_t)idx[p] : (uint32_t)d;   // padding: feature d (mask 0)
             v[u] = p < e ? vals[p] : 0.0f;
         }
         sidx[(g0 + j) * 32 + lane] = make_uint2(k[0] | (k[1] << 16), k[2] | (k[3] << 16));
@@ -475,12 +475,12 @@ cudaError_t lay_sell_len(const int64_t* indptr, int64_t n, int64_t R, int spc, i
     return cudaGetLastError();
 }
 cudaError_t lay_sell_fill(const int64_t* indptr, const int32_t* idx, const float* vals, int64_t n,
-                          int64_t R, int spc, int64_t ns, const int64_t* gptr, uint2* sidx,
+                          int64_t d, int64_t R, int spc, int64_t ns, const int64_t* gptr, uint2* sidx,
                           float4* sval, cudaStream_t st)
 {
     if (ns <= 0) return cudaSuccess;
     svm_note_launches(1);
-    k_sell_fill<<<nblocks(ns * 32, 256), 256, 0, st>>>(indptr, idx, vals, n, R, spc, ns, gptr, sidx, sval);
+    k_sell_fill<<<nblocks(ns * 32, 256), 256, 0, st>>>(indptr, idx, vals, n, d, R, spc, ns, gptr, sidx, sval);
     return cudaGetLastError();
 }
 cudaError_t lay_rowmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, int64_t n_pad,

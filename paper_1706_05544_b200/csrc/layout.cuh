@@ -12,7 +12,7 @@ cudaError_t lay_check_csr(const int64_t* indptr, const int32_t* idx, int64_t n, 
 cudaError_t lay_sell_len(const int64_t* indptr, int64_t n, int64_t R, int spc, int64_t ns,
                          int64_t* len, cudaStream_t st);
 cudaError_t lay_sell_fill(const int64_t* indptr, const int32_t* idx, const float* vals, int64_t n,
-                          int64_t R, int spc, int64_t ns, const int64_t* gptr, uint2* sidx,
+                          int64_t d, int64_t R, int spc, int64_t ns, const int64_t* gptr, uint2* sidx,
                           float4* sval, cudaStream_t st);
 cudaError_t lay_rowmajor_to_XT(const float* X, int64_t n, int64_t d, float* XT, int64_t n_pad,
                                cudaStream_t st);

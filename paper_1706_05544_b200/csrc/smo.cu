@@ -423,10 +423,13 @@ __device__ __forceinline__ float4 lds_f4(uint32_t a)
     return v;
 }
 __device__ __forceinline__ void dots_sell(const uint2* __restrict__ gi, const float4* __restrict__ gv,
-                                          int ng, int cnt, const float* sXW, float (&acc)[1][SVM_WS])
+                                          int ng, const float* sXW, const uint32_t* sMask,
+                                          float (&acc)[1][SVM_WS])
 {
     zero_acc<1>(acc);
-    const uint32_t wsm = (uint32_t)__cvta_generic_to_shared(sXW);   // X_W^T [d][WSTR_CSR] fp32
+    uint32_t wsm = (uint32_t)__cvta_generic_to_shared(sXW);   // X_W^T [d][WSTR_CSR] fp32
+    uint32_t msm = (uint32_t)__cvta_generic_to_shared(sMask); // group masks [d + 1] (d: padding, 0)
+    asm volatile("" : "+r"(wsm), "+r"(msm));   // keep the bases in registers (no S2R rematerialisation)
     uint2 ri[SELL_PF];
     float4 rv[SELL_PF];
 #pragma unroll
@@ -449,11 +452,10 @@ __device__ __forceinline__ void dots_sell(const uint2* __restrict__ gi, const fl
                 const int kk[4] = {(int)(ci.x & 0xffffu), (int)(ci.x >> 16), (int)(ci.y & 0xffffu), (int)(ci.y >> 16)};
                 const float vv[4] = {cv.x, cv.y, cv.z, cv.w};
                 // the 4 group masks first (no branch between them: the loads issue together);
-                // a nonzero past the row's end gets mask 0, i.e. no update
+                // padding past a row's end has feature index d, whose mask is 0: no update
                 uint32_t m[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    m[u] = lds_u32(wsm + 4u * (uint32_t)csr_mask_slot(kk[u])) & (4 * j + u < cnt ? 0xffffu : 0u);
+                for (int u = 0; u < 4; ++u) m[u] = lds_u32(msm + 4u * (uint32_t)kk[u]);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t wk = wsm + 4u * WSTR_CSR * (uint32_t)kk[u];
@@ -1034,6 +1036,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     // dbuf_rows rows (filled while the subproblem runs, read by the epilogue afterwards)
     const bool sell = CSR && a.sell_idx != nullptr;   // CSR from the slice copy (no staging)
     int32_t* sGp = reinterpret_cast<int32_t*>(sX);     // SELL: [spc + 1] group offsets of this CTA
+    uint32_t* sMask = reinterpret_cast<uint32_t*>(sX) + ((a.sell_spc + 4) & ~3);   // SELL: [d + 1] masks
     float* csr_val = sX + (size_t)warp * CSR_CAP;                                   // CSR only
     uint16_t* csr_idx = reinterpret_cast<uint16_t*>(sX + (size_t)SMO_WARPS * CSR_CAP) + (size_t)warp * CSR_CAP;
     // TMA ring (streamed dense X, a.x_tma): tma_ns slots of [d][32 RPT] fp32, 128-byte aligned
@@ -1044,7 +1047,7 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     float* tring = reinterpret_cast<float*>(dyn_smem + ((smem_u32(sX) + 127u) & ~127u) - smem_u32(dyn_smem));
     const uint32_t stage_floats = (uint32_t)d * CH;
     float* sDot = tma ? tring + (size_t)NS * stage_floats
-                      : sX + (XS ? (size_t)d * R : (CSR ? (sell ? (size_t)((a.sell_spc + 4) & ~3) : (size_t)SMO_WARPS * CSR_CAP * 6 / 4)
+                      : sX + (XS ? (size_t)d * R : (CSR ? (sell ? (size_t)((a.sell_spc + 4) & ~3) + (size_t)((d + 4) & ~3) : (size_t)SMO_WARPS * CSR_CAP * 6 / 4)
                                                         : (size_t)SMO_THREADS * pf_x<RPT>() * RPT));
     const int dbuf_rows = a.dbuf_rows;
 
@@ -1088,9 +1091,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
     auto csr_dots = [&](int ch, int64_t li0, float (&acc)[1][SVM_WS]) {
         if (sell) {
             const int64_t g0 = sell_g0 + sGp[ch];
-            const int cnt = li0 < cta_end ? (int)(v.indptr[li0 + 1] - v.indptr[li0]) : 0;
             dots_sell(a.sell_idx + g0 * 32 + lane, a.sell_val + g0 * 32 + lane, sGp[ch + 1] - sGp[ch],
-                      cnt, sXW, acc);
+                      sXW, sMask, acc);
         } else {
             dots_csr_staged(v.indptr, a.indices, a.vals, li0 - lane, cta_end, lane, csr_idx, csr_val, sXW, acc);
         }
@@ -1657,6 +1659,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
         if (!a.pass_only || t == 0) {
         if constexpr (CSR) {
             for (int i = tid; i < d * WS; i += SMO_THREADS) sXW[i] = 0.0f;
+            if (sell)
+                for (int i = tid; i <= d; i += SMO_THREADS) sMask[i] = 0u;
         } else {
             for (int i = tid; i < d * SVM_WS; i += SMO_THREADS)
                 if ((i & 15) >= nr) sXW[i] = 0.0f;
@@ -1705,7 +1709,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                     const int k = a.peer_indices[o][p];
                     const float xv = a.peer_vals[o][p];
                     sXW[k * WS + r] = xv;
-                    if (xv != 0.0f) atomicOr(reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);   // group mask
+                    if (xv != 0.0f)   // group mask
+                        atomicOr(sell ? sMask + k : reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);
                 }
             }
             if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];
@@ -2733,7 +2738,7 @@ __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
 
 int smo_ring_bytes(int rpt) { return SMO_THREADS * 4 * rpt * (rpt == 1 ? pf_x<1>() : rpt == 2 ? pf_x<2>() : pf_x<4>()); }
 int smo_csr_stage_bytes() { return SMO_WARPS * CSR_CAP * 6; }
-int smo_sell_bytes(int spc) { return 4 * ((spc + 4) & ~3); }
+int smo_sell_bytes(int spc, int64_t d) { return (int)(4 * (((spc + 4) & ~3) + ((d + 4) & ~3))); }
 int smo_csr_w_extra_bytes(int64_t d) { return (int)(d * 4 * (WSTR_CSR - SVM_WS)); }
 
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows)

@@ -220,7 +220,8 @@ struct SmoArgs {
     // CSR rows in slices of 32 for the pass (layout.cu k_sell_fill): slice
     // s = g * sell_spc + c holds rows g R + 32 c + l of global CTA g (l = lane); group j of slice s
     // (4 consecutive nonzeros of every lane's row) at [(sell_gptr[s] + j) * 32 + l]: 4 u16 column
-    // indices packed in a uint2, the 4 values in a float4.  NULL: per-warp shared-memory staging.
+    // indices packed in a uint2 (padding past a row's end: index d, value 0), the 4 values in a
+    // float4.  NULL: per-warp shared-memory staging.
     const uint2* sell_idx;
     const float4* sell_val;
     const int64_t* sell_gptr;  // [slices + 1] group offsets
@@ -297,7 +298,7 @@ void smo_l2_restore();   // after the launch's loop: the caller's persisting-L2 
 int smo_smem_bytes(int64_t d, int world, int nblk, int64_t x_rows);
 int smo_ring_bytes(int rpt);
 int smo_csr_stage_bytes();
-int smo_sell_bytes(int spc);   // the slice offsets of one CTA (SELL CSR pass)
+int smo_sell_bytes(int spc, int64_t d);   // slice offsets + group masks of one CTA (SELL CSR pass)
 int smo_csr_w_extra_bytes(int64_t d);
 cudaError_t launch_kernel_rows(const SmoArgs& a, const int64_t* rows, int nr, float* K,
                                cudaStream_t st);
