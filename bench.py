@@ -48,8 +48,9 @@ ROOF_NOTES = {
     "c3": "batched one-vs-rest: X (188 MB > L2) read once per batched iteration for all 10 "
           "problems; see DESIGN.md",
     "c4": "X (108 MB) streamed from HBM/L2 through per-lane cp.async rings; see DESIGN.md",
-    "c5": "CSR pass: per-warp staged nonzeros, masked X_W groups in shared memory (L1/shared-pipe "
-          "bound, not HBM); algorithmic bytes 8 nnz + 17 n per iteration; see DESIGN.md",
+    "c5": "CSR pass: 32-row slices streamed from the lane-interleaved copy (SELL), masked X_W groups "
+          "in shared memory (issue / shared-pipe bound, not HBM); algorithmic bytes 8 nnz + 17 n "
+          "per iteration; see DESIGN.md",
 }
 WORKLOADS = {
     "c1": "binary C-SVC, RBF, two Gaussian blobs, n=2,000 d=20 dense",
