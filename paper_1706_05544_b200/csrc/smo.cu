@@ -428,7 +428,7 @@ __device__ __forceinline__ void dots_sell(const uint2* __restrict__ gi, const fl
 {
     zero_acc<1>(acc);
     uint32_t wsm = (uint32_t)__cvta_generic_to_shared(sXW);   // X_W^T [d][WSTR_CSR] fp32
-    uint32_t msm = (uint32_t)__cvta_generic_to_shared(sMask); // group masks [d + 1] (d: padding, 0)
+    uint32_t msm = (uint32_t)__cvta_generic_to_shared(sMask); // 4-bit group masks [d + 1] (d: padding, 0)
     asm volatile("" : "+r"(wsm), "+r"(msm));   // keep the bases in registers (no S2R rematerialisation)
     uint2 ri[SELL_PF];
     float4 rv[SELL_PF];
@@ -461,7 +461,7 @@ __device__ __forceinline__ void dots_sell(const uint2* __restrict__ gi, const fl
                     const uint32_t wk = wsm + 4u * WSTR_CSR * (uint32_t)kk[u];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        if (m[u] & (0xFu << (4 * q))) {   // as fma_row16_masked
+                        if (m[u] & (1u << q)) {   // group q of X_W has a nonzero (as fma_row16_masked)
                             const float4 w = lds_f4(wk + 16u * q);
                             const float2 xx = make_float2(vv[u], vv[u]);
                             const float2 lo = __ffma2_rn(xx, make_float2(w.x, w.y), make_float2(acc[0][4 * q], acc[0][4 * q + 1]));
@@ -1710,7 +1710,8 @@ __global__ void __launch_bounds__(SMO_THREADS, 1) smo_persistent(const __grid_co
                     const float xv = a.peer_vals[o][p];
                     sXW[k * WS + r] = xv;
                     if (xv != 0.0f)   // group mask
-                        atomicOr(sell ? sMask + k : reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)), 1u << r);
+                        atomicOr(sell ? sMask + k : reinterpret_cast<unsigned int*>(sXW + csr_mask_slot(k)),
+                                 sell ? 1u << (r >> 2) : 1u << r);   // SELL: 4-row group bits
                 }
             }
             if (lane == 0) sh.xn[r] = a.peer_xnorm[o][lr];

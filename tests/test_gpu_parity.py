@@ -181,6 +181,41 @@ def test_one_step_from_identical_state(kname, svm_type, csr):
             assert abs(obj(dg2) - obj(dAt)) <= 1e-9 * max(1.0, abs(obj(dAt)))
 
 
+def test_csr_ragged_rows_one_step():
+    """The CSR pass's slice copy (32-row slices padded to their longest row with feature d) on
+    ragged rows: empty rows, fully dense rows and every length in between inside the same 32-row
+    slices.  One step from identical state: W identical, G equal to the oracle's step 6 applied to
+    the GPU's dalpha within 1e-5 max(1, |G|); then training to tol matches the dense path's dual."""
+    ds = synth.make("c1", n=900)
+    rng = np.random.default_rng(5)
+    X = ds.X.copy()
+    keep = rng.random(X.shape) < rng.random((X.shape[0], 1))   # per-row density U(0, 1)
+    X[~keep] = 0.0
+    X[::37] = 0.0                                                # empty rows
+    X[5::41] = ds.X[5::41]                                       # fully dense rows
+    ip = np.concatenate([[0], np.cumsum((X != 0).sum(1))]).astype(np.int64)
+    csr = (ip, np.nonzero(X)[1].astype(np.int32), X[X != 0])
+    lens = np.diff(ip)
+    assert lens.min() == 0 and lens.max() == ds.d
+    gamma = 1.0 / ds.d
+    ks = ora.kspec("rbf", gamma, d=ds.d)
+    prob = ora.Problem(ora.C_CLASSIFICATION, ds.y, ds.n)
+    for steps in (0, 9):
+        alpha, G = _state_after(X, prob, ks, 1.0, steps)
+        W, _, _, _ = ora.step(X, prob, ks, alpha, G, 1.0, q=16, tol=1e-3)
+        s = pkg.Solver(csr=csr, y=ds.y, d=ds.d, gamma=gamma)
+        s.set_state(alpha, G.astype(np.float32))
+        st = s.run(1)
+        np.testing.assert_array_equal(np.array(st.last_w[:st.last_nw]), W)
+        dg = np.array(st.last_dalpha[:st.last_nw])
+        _, Gg = s.get_state()
+        Gref = ora.gradient_update(X, prob, ks, W, dg, G)
+        assert (np.abs(Gg - Gref) <= 1e-5 * np.maximum(1.0, np.abs(Gref))).all(), np.abs(Gg - Gref).max()
+    mc = pkg.train_csr(*csr, ds.y, ds.d, gamma=gamma)
+    md = pkg.train(X, ds.y, gamma=gamma)
+    assert abs(mc.info.dual_objective - md.info.dual_objective) <= 1e-5 * abs(md.info.dual_objective)
+
+
 # ----------------------------------------------------------------------------- end to end
 def _labels_agree(out, f_ref, pred_ref, tol=1e-3):
     """Labels must agree wherever the oracle's decision is unique at the decision tolerance:
