@@ -119,6 +119,8 @@ typedef struct svm_model_info {
     double exchange_p99_us; /* (histogram of 512-cycle bins, converted at the loop's clock)       */
     int64_t cache_passes;   /* iterations whose W rows were all in the kernel-column cache (SURVEY */
                             /* 8(f) #3): their pass read K columns instead of X                  */
+    int32_t certifications; /* certification passes run over all problems (a resumed loop is     */
+                            /* certified again, from the rows whose coefficient changed only)    */
 } svm_model_info;
 
 /*

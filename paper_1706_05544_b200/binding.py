@@ -56,7 +56,7 @@ class svm_model_info(ctypes.Structure):
                 ("passes", ctypes.c_int64), ("pass_ms", ctypes.c_double),
                 ("batched", ctypes.c_int32), ("exchange_ms", ctypes.c_double),
                 ("exchange_p50_us", ctypes.c_double), ("exchange_p99_us", ctypes.c_double),
-                ("cache_passes", ctypes.c_int64)]
+                ("cache_passes", ctypes.c_int64), ("certifications", ctypes.c_int32)]
 
 
 class svm_solver_stats(ctypes.Structure):

@@ -457,7 +457,15 @@ struct Exchange {
 // SURVEY 8(c) "Proposals"): the certified violation is computed with fp32-accurate kernel values
 // (fp64 sums), and at full size it sat up to 1.8e-5 below the fp64-recomputed one (c3, tol 1e-3);
 // aiming at 0.95 tol keeps the fp64 violation <= tol.
-#define SVM_CERT_MARGIN 0.95
+#define SVM_CERT_MARGIN_DEFAULT 0.95
+// (SVMB200_CERT_MARGIN overrides the certification target only, not the loop's first stop: a
+// test knob that forces resumptions)
+static double cert_margin()
+{
+    const char* e = getenv("SVMB200_CERT_MARGIN");
+    return (e && atof(e) > 0 && atof(e) <= 1) ? atof(e) : SVM_CERT_MARGIN_DEFAULT;
+}
+#define SVM_CERT_MARGIN cert_margin()
 
 struct Problem {
     int ncopy = 1;
@@ -472,6 +480,7 @@ struct Problem {
     double tol_loop = 0;   // the loop's stop threshold: SVM_CERT_MARGIN tol, lowered after a failed
                            // certification (R16)
     double loop_ms = 0, cert_ms = 0;
+    int32_t n_cert = 0;     // certifications run (1 + resumptions when every loop was certified)
     double exch_ms = 0;    // share of loop_ms CTA 0 spent in the candidate exchange
     double exch_hist[SMO_EXCH_BINS] = {};   // per-iteration exchange latency histogram (us units
                                             // after scaling: see exch_percentile)
@@ -489,7 +498,7 @@ static int problem_init(Problem& P, const Data& D, const float* yv_host, const s
     P.C = prm->cost;
     P.eps = prm->epsilon;
     P.tol = prm->tolerance;
-    P.tol_loop = SVM_CERT_MARGIN * prm->tolerance;   // DESIGN.md reading R16
+    P.tol_loop = SVM_CERT_MARGIN_DEFAULT * prm->tolerance;   // DESIGN.md reading R16
     P.q = prm->working_set;
     int64_t m = D.n * P.ncopy;
     P.max_iter = prm->max_iter > 0 ? prm->max_iter : std::max<int64_t>(10 * m, 10000);
@@ -1022,15 +1031,36 @@ static bool want_certify(const svm_params* prm, int64_t n, int64_t nsv, int64_t 
     return (double)n * (double)nsv * (double)d <= 2e15;
 }
 
+// What a certification leaves for the next one of the same solve: the fp64 decision sums F it
+// computed and the coefficients they were computed from.
+struct CertState {
+    DBuf F, coef;
+    bool valid = false;
+};
+
 // Certification (a4): recompute G = Q a + p from the support vectors with fp64 accumulation and
-// re-measure the violation; returns it in *viol.
-static int certify(const Data& D, Problem& P, double* viol, cudaStream_t st)
+// re-measure the violation; returns it in *viol.  With a valid CertState (a resumed loop after an
+// earlier certification of the same problem) only the rows whose coefficient changed since then
+// enter: F += sum_{s changed} (coef_s - coef'_s) K(x_s, .) -- the same fp64 sums of fp32 kernel
+// values as a full recomputation, over the ~16 x (resumed iterations) changed rows instead of
+// every SV (c5: 13 k instead of 940 k rows).
+static int certify(const Data& D, Problem& P, double* viol, cudaStream_t st, CertState* cs = nullptr)
 {
     double t0 = now_ms();
     DBuf coef, flag, idx, SVT, svn, coef_sv, F;
     TRY(flag.alloc(D.n));
     CK(cudaMemsetAsync(flag.p, 0, D.n, st));
     TRY(problem_coef(D, P, coef, flag, st));
+    const bool delta = cs && cs->valid && !getenv("SVMB200_FULL_RECERT");
+    DBuf dcoef;
+    if (delta) {   // coef <- coef - coef', flag <- changed, coef' <- coef
+        TRY(dcoef.alloc(sizeof(double) * D.n));
+        CK(lay_coef_delta(coef.as<double>(), cs->coef.as<double>(), D.n, dcoef.as<double>(),
+                          flag.as<uint8_t>(), st));
+        std::swap(coef.p, dcoef.p);
+        std::swap(coef.bytes, dcoef.bytes);
+        std::swap(coef.plain, dcoef.plain);
+    }
     int64_t nsv = 0;
     TRY(compact(flag, D.n, idx, &nsv, st));
     const bool prof = getenv("SVMB200_PROFILE") != nullptr;
@@ -1040,21 +1070,35 @@ static int certify(const Data& D, Problem& P, double* viol, cudaStream_t st)
     TRY(coef_sv.alloc(sizeof(double) * nsv_pad));
     CK(lay_gather_coef(coef.as<double>(), idx.as<int64_t>(), nsv, nsv_pad, coef_sv.as<double>(), st));
     double tb = prof ? (cudaStreamSynchronize(st), now_ms()) : 0;
-    TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef_sv, P.kp, F, st));
+    if (nsv > 0 || !delta) TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef_sv, P.kp, F, st));
     double tc = prof ? (cudaStreamSynchronize(st), now_ms()) : 0;
-    CK(pred_refresh_G(F.as<double>(), P.yv.as<float>(), P.status.as<uint8_t>(), D.n, D.n_pad,
+    if (delta) {
+        if (nsv > 0) CK(lay_add_f64(cs->F.as<double>(), F.as<double>(), D.n, st));
+    } else if (cs) {   // keep F and the coefficients for an incremental re-certification
+        std::swap(cs->F.p, F.p);
+        std::swap(cs->F.bytes, F.bytes);
+        std::swap(cs->F.plain, F.plain);
+        std::swap(cs->coef.p, coef.p);
+        std::swap(cs->coef.bytes, coef.bytes);
+        std::swap(cs->coef.plain, coef.plain);
+        cs->valid = true;
+    }
+    const double* Fall = cs ? cs->F.as<double>() : F.as<double>();
+    CK(pred_refresh_G(Fall, P.yv.as<float>(), P.status.as<uint8_t>(), D.n, D.n_pad,
                       P.ncopy, P.eps, P.G.as<float>(), st));
     Reduced r;
     TRY(reduce_state(D, P, &r, st));
     if (prof)
-        fprintf(stderr, "[svmb200] certify: nsv %lld, coef+compact %.1f ms, SV gather %.1f ms, decision %.1f ms, "
-                "refresh+reduce %.1f ms, violation %.3g\n", (long long)nsv, ta - t0, tb - ta, tc - tb,
+        fprintf(stderr, "[svmb200] certify%s: nsv %lld, coef+compact %.1f ms, SV gather %.1f ms, decision %.1f ms, "
+                "refresh+reduce %.1f ms, violation %.3g\n", delta ? " (changed rows only)" : "",
+                (long long)nsv, ta - t0, tb - ta, tc - tb,
                 (cudaStreamSynchronize(st), now_ms()) - tc, r.m_up - r.M_low);
     P.m_up = r.m_up;
     P.M_low = r.M_low;
     *viol = r.m_up - r.M_low;
     P.certified = true;
     P.cert_ms += now_ms() - t0;
+    ++P.n_cert;
     return SVM_OK;
 }
 
@@ -1089,9 +1133,10 @@ static double resume_factor()
 static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_params* prm,
                           cudaStream_t st)
 {
+    CertState cs;
     for (int round = 0;; ++round) {
         if (!P.converged || prm->certify == 0) break;
-        if (prm->certify < 0) {  // auto: only when one pass over n x n_SV is affordable
+        if (prm->certify < 0 && round == 0) {  // auto: only when one pass over n x n_SV is affordable
             DBuf coef, flag, idx;
             TRY(flag.alloc(D.n));
             CK(cudaMemsetAsync(flag.p, 0, D.n, st));
@@ -1101,7 +1146,7 @@ static int certify_resume(const Data& D, Problem& P, Exchange& E, const svm_para
             if (!want_certify(prm, D.n, nsv, D.d)) break;
         }
         double viol = 0;
-        TRY(certify(D, P, &viol, st));
+        TRY(certify(D, P, &viol, st, &cs));
         const double target = SVM_CERT_MARGIN * P.tol;
         if (viol <= target) { P.converged = true; break; }
         P.converged = viol <= P.tol;   // (reported if the resumptions run out)
@@ -1467,6 +1512,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     double xh[SMO_EXCH_BINS] = {}, upc = 0;
     int64_t cache_passes = 0;
     int64_t iters = 0, passes = 0;
+    int32_t n_cert = 0;
     bool conv = true, cert = true;
     for (size_t p = 0; p < ys.size(); ++p) TRY(problem_init(probs[p], D, ys[p].data(), prm, st));
     bool batched = false;
@@ -1491,6 +1537,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
         for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
         if (P.us_per_cycle > 0) upc = P.us_per_cycle;
         cert_ms += P.cert_ms;
+        n_cert += P.n_cert;
         if (!batched) { passes += P.iterations; pass_ms += P.loop_ms; }
     }
     if (batched) { passes = probs[0].passes; pass_ms = probs[0].pass_ms; }
@@ -1530,6 +1577,7 @@ static int train_common(Data& D, const float* y, const svm_params* prm, svm_mode
     I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
     I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
     I.cache_passes = cache_passes;
+    I.certifications = n_cert;
     I.certify_ms = cert_ms;
     I.setup_ms = t_setup;
     I.passes = passes;
@@ -2515,6 +2563,7 @@ static int shard_certify(svm_shard* S, Problem& P, double* viol)
     *viol = g.m_up - g.M_low;
     P.certified = true;
     P.cert_ms += now_ms() - t0;
+    ++P.n_cert;
     return SVM_OK;
 }
 
@@ -2531,6 +2580,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     TRY(shard_xchg(S, {0.0}, none, 300.0));        // start barrier
     std::vector<Problem> probs(S->nprob);
     std::vector<double> bs(S->nprob);
+    int32_t n_cert = 0;
     double dual = 0, worst = -INFINITY, loop_ms = 0, cert_ms = 0, exch_ms = 0;
     double xh[SMO_EXCH_BINS] = {}, upc = 0;
     int64_t cache_passes = 0;
@@ -2581,6 +2631,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         cache_passes += P.cache_allhit;
         for (int b = 0; b < SMO_EXCH_BINS; ++b) xh[b] += P.exch_hist[b];
         if (P.us_per_cycle > 0) upc = P.us_per_cycle;
+        n_cert += P.n_cert;
         cert_ms += P.cert_ms;
     }
     // model: union of SVs over problems, coefficients of every problem, rows gathered
@@ -2646,6 +2697,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
     I.exchange_ms = exch_ms;
     I.exchange_p50_us = exch_percentile(xh, 0.50) * upc;
     I.exchange_p99_us = exch_percentile(xh, 0.99) * upc;
+    I.certifications = n_cert;
     I.cache_passes = cache_passes;
     I.certify_ms = cert_ms;
     I.passes = iters;

@@ -272,6 +272,23 @@ __global__ void k_coef(const double* __restrict__ alpha, const uint8_t* __restri
     if (c != 0.0) svflag[i] = 1;
 }
 
+// Incremental re-certification: delta = coef - coef_prev (flag where nonzero), and F += dF.
+__global__ void k_coef_delta(const double* __restrict__ coef, double* __restrict__ coef_prev,
+                             int64_t n, double* __restrict__ delta, uint8_t* __restrict__ flag)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double dc = coef[i] - coef_prev[i];
+    delta[i] = dc;
+    flag[i] = dc != 0.0 ? 1 : 0;
+    coef_prev[i] = coef[i];
+}
+__global__ void k_add_f64(double* __restrict__ a, const double* __restrict__ b, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] += b[i];
+}
+
 // block-level counts of flagged rows, then scatter with host-scanned offsets
 __global__ void k_count_flags(const uint8_t* __restrict__ flag, int64_t n, int32_t* __restrict__ cnt)
 {
@@ -572,6 +589,21 @@ cudaError_t lay_coef(const double* alpha, const uint8_t* status, int64_t n, int6
 {
     svm_note_launches(1);
     k_coef<<<nblocks(n, 256), 256, 0, st>>>(alpha, status, n, n_pad, ncopy, C, coef, 0, svflag);
+    return cudaGetLastError();
+}
+cudaError_t lay_coef_delta(const double* coef, double* coef_prev, int64_t n, double* delta,
+                           uint8_t* flag, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    svm_note_launches(1);
+    k_coef_delta<<<nblocks(n, 256), 256, 0, st>>>(coef, coef_prev, n, delta, flag);
+    return cudaGetLastError();
+}
+cudaError_t lay_add_f64(double* a, const double* b, int64_t n, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    svm_note_launches(1);
+    k_add_f64<<<nblocks(n, 256), 256, 0, st>>>(a, b, n);
     return cudaGetLastError();
 }
 cudaError_t lay_count_flags(const uint8_t* flag, int64_t n, int32_t* cnt, int* nblk_out,

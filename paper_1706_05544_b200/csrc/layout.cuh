@@ -39,6 +39,11 @@ cudaError_t lay_reduce_state(const double* alpha, const float* G, const uint8_t*
                              double C, double* d_out5, cudaStream_t st);
 cudaError_t lay_coef(const double* alpha, const uint8_t* status, int64_t n, int64_t n_pad,
                      int ncopy, double C, double* coef, uint8_t* svflag, cudaStream_t st);
+// incremental re-certification: delta = coef - coef_prev, flag = delta != 0, coef_prev = coef;
+// a += b (fp64)
+cudaError_t lay_coef_delta(const double* coef, double* coef_prev, int64_t n, double* delta,
+                           uint8_t* flag, cudaStream_t st);
+cudaError_t lay_add_f64(double* a, const double* b, int64_t n, cudaStream_t st);
 cudaError_t lay_count_flags(const uint8_t* flag, int64_t n, int32_t* cnt, int* nblk_out,
                             cudaStream_t st);
 cudaError_t lay_scatter_flags(const uint8_t* flag, int64_t n, const int64_t* offs, int64_t* out,

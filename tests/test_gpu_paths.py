@@ -326,3 +326,46 @@ def test_process_state_restored_after_training():
     f2 = m2.predict(ds.X[:500], decision=True)[1]
     assert m1.info.iterations == m2.info.iterations
     np.testing.assert_array_equal(f1, f2)
+
+
+def _kkt_fp64_svc(X, ybin, sv_idx, coef, rows, gamma, C=1.0):
+    """fp64 m_up - M_low over the duals of `rows`, G_i = -1 + y_i sum_s coef_s K(x_s, x_i) from
+    the model's SVs (oracle kernels)."""
+    ks = ora.kspec("rbf", gamma, d=X.shape[1])
+    f = ora.decision(X[sv_idx], coef, 0.0, ks, X[rows])
+    c = np.zeros(X.shape[0])
+    c[sv_idx] = coef
+    a = np.abs(c[rows])
+    y = ybin[rows].astype(np.float64)
+    s = -y * (-1.0 + y * f)
+    up = np.where(y > 0, a < C, a > 0)
+    lo = np.where(y > 0, a > 0, a < C)
+    return s[up].max() - s[lo].min()
+
+
+def test_incremental_recertification():
+    """A resumed loop is certified again from the rows whose coefficient changed since the previous
+    certification (F += sum_s (coef_s - coef'_s) K(x_s, .), fp64 sums): with resumptions forced
+    (SVMB200_CERT_MARGIN = 0.6: the certification target drops to 0.6 tol) the result agrees with
+    full re-certifications (SVMB200_FULL_RECERT=1), and the certified violation holds against the
+    oracle's fp64 recomputation from the model's support vectors."""
+    ds = synth.make("c4", n=20000)
+    gamma = 1.0 / ds.d
+
+    def run(full):
+        ev = dict(SVMB200_CERT_MARGIN=0.6)
+        if full:
+            ev["SVMB200_FULL_RECERT"] = 1
+        with env(**ev):
+            return pkg.train(ds.X, ds.y, gamma=gamma)
+    mi, mf = run(False), run(True)
+    assert mi.info.certifications >= 2 and mf.info.certifications >= 2
+    assert mi.info.converged == 1 and mf.info.converged == 1
+    assert abs(mi.info.dual_objective - mf.info.dual_objective) <= 1e-7 * abs(mf.info.dual_objective)
+    idx, coef = mi.support()
+    ybin = ora.binary_labels(ds.y)[0]
+    rows = np.arange(0, ds.n, 4)
+    viol = _kkt_fp64_svc(ds.X, ybin, idx, coef[0], rows, gamma)
+    assert viol <= 0.6e-3 + 2e-5, viol
+    m0 = pkg.train(ds.X, ds.y, gamma=gamma)   # default margin: the counter is at least 1
+    assert m0.info.certifications >= 1
