@@ -181,6 +181,30 @@ def test_one_step_from_identical_state(kname, svm_type, csr):
             assert abs(obj(dg2) - obj(dAt)) <= 1e-9 * max(1.0, abs(obj(dAt)))
 
 
+@pytest.mark.parametrize("codes", [(7.0, 3.0), (0.0, 1.0), (1.0, 0.0), (-1.0, 1.0)])
+def test_binary_label_map_vs_oracle(codes):
+    """The binary label map (reading R15) on the GPU against the oracle's:
+    exactly {-1, +1} is used as-is, any other pair maps its first-appearing label to +1; the
+    decision value's sign and the predicted labels follow.  y[0] takes codes[0], so the
+    first-appearing label is codes[0]; (1, 0) and (0, 1) flip the map of the same data."""
+    ds = synth.make("c1", n=600)
+    y = np.where(ds.y > 0, codes[0], codes[1]).astype(np.float32)
+    if y[0] != codes[0]:
+        y = np.where(ds.y > 0, codes[1], codes[0]).astype(np.float32)
+    assert y[0] == codes[0]
+    m = pkg.train(ds.X, y, gamma=1.0 / ds.d)
+    om = ora.train(ds.X, y, gamma=1.0 / ds.d)
+    Xq = np.concatenate([ds.X[:300], synth.make("c1", n=300, heldout=True).X])
+    out, dec = m.predict(Xq, decision=True)
+    f_ora = om.decision_function(Xq)[:, 0]
+    assert np.abs(dec[:, 0] - f_ora).max() <= 1e-3
+    lab_ora = om.predict(Xq)
+    assert set(np.unique(out).tolist()) <= set(codes)
+    assert _labels_agree(out, f_ora, lab_ora) >= 0.999
+    pos = 1.0 if set(codes) == {-1.0, 1.0} else codes[0]
+    assert (out[f_ora > 2e-3] == pos).all()
+
+
 def test_csr_ragged_rows_one_step():
     """The CSR pass's slice copy (32-row slices padded to their longest row with feature d) on
     ragged rows: empty rows, fully dense rows and every length in between inside the same 32-row
