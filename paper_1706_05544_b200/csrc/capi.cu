@@ -2542,20 +2542,41 @@ static int shard_reduce(svm_shard* S, const Problem& P, Reduced* g)
     return SVM_OK;
 }
 
-static int shard_certify(svm_shard* S, Problem& P, double* viol)
+// As certify(): the global SVs (every rank's, over NVLink) against this rank's rows; with a valid
+// CertState only the rows (of every rank) whose coefficient changed since the previous
+// certification enter, with their coefficient change.
+static int shard_certify(svm_shard* S, Problem& P, double* viol, CertState* cs = nullptr)
 {
     double t0 = now_ms();
     const Data& D = S->D;
-    DBuf flag, coefrow, SVT, svn, coef, F;
+    DBuf flag, coefrow, SVT, svn, coef, F, dcoef;
     TRY(flag.alloc(D.n));
     CK(cudaMemsetAsync(flag.p, 0, D.n, S->st));
     TRY(problem_coef(D, P, coefrow, flag, S->st));
-    CK(cudaMemcpyAsync(S->coefx.p, coefrow.p, sizeof(double) * D.n, cudaMemcpyDeviceToDevice, S->st));
-    int64_t nsv = 0, nsv_pad = 0;
+    const bool delta = cs && cs->valid && !getenv("SVMB200_FULL_RECERT");
+    if (delta) {
+        TRY(dcoef.alloc(sizeof(double) * D.n));
+        CK(lay_coef_delta(coefrow.as<double>(), cs->coef.as<double>(), D.n, dcoef.as<double>(),
+                          flag.as<uint8_t>(), S->st));
+    }
+    CK(cudaMemcpyAsync(S->coefx.p, delta ? dcoef.p : coefrow.p, sizeof(double) * D.n,
+                       cudaMemcpyDeviceToDevice, S->st));
+    int64_t nsv = 0, nsv_pad = 0;   // global count: the same decision on every rank
     TRY(shard_global_sv(S, 1, flag, SVT, svn, coef, &nsv, &nsv_pad, nullptr));
-    TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef, P.kp, F, S->st));
-    CK(pred_refresh_G(F.as<double>(), P.yv.as<float>(), P.status.as<uint8_t>(), D.n, D.n_pad,
-                      P.ncopy, P.eps, P.G.as<float>(), S->st));
+    if (nsv > 0 || !delta) TRY(training_decision(D, SVT, svn, nsv, nsv_pad, coef, P.kp, F, S->st));
+    if (delta) {
+        if (nsv > 0) CK(lay_add_f64(cs->F.as<double>(), F.as<double>(), D.n, S->st));
+    } else if (cs) {
+        std::swap(cs->F.p, F.p);
+        std::swap(cs->F.bytes, F.bytes);
+        std::swap(cs->F.plain, F.plain);
+        std::swap(cs->coef.p, coefrow.p);
+        std::swap(cs->coef.bytes, coefrow.bytes);
+        std::swap(cs->coef.plain, coefrow.plain);
+        cs->valid = true;
+    }
+    CK(pred_refresh_G(cs ? cs->F.as<double>() : F.as<double>(), P.yv.as<float>(),
+                      P.status.as<uint8_t>(), D.n, D.n_pad, P.ncopy, P.eps, P.G.as<float>(), S->st));
     Reduced g;
     TRY(shard_reduce(S, P, &g));
     P.m_up = g.m_up;
@@ -2592,8 +2613,9 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
         P.max_iter = prm->max_iter > 0 ? prm->max_iter
                                        : std::max<int64_t>(10 * S->n_global * P.ncopy, 10000);
         TRY(run_loop(D, P, S->E, P.max_iter, S->st, nullptr, &S->sc));
+        CertState cs;
         for (int round = 0; P.converged && prm->certify != 0; ++round) {
-            if (prm->certify < 0) {   // auto rule of svm_train, on the global SV count
+            if (prm->certify < 0 && round == 0) {   // auto rule of svm_train, on the global SV count
                 DBuf cf, fl, ix;
                 TRY(fl.alloc(D.n));
                 CK(cudaMemsetAsync(fl.p, 0, D.n, S->st));
@@ -2607,7 +2629,7 @@ extern "C" int svm_shard_train(svm_shard* S, svm_model** out)
                 if (!want_certify(prm, S->n_global, (int64_t)nsv_g, D.d)) break;
             }
             double viol = 0;
-            TRY(shard_certify(S, P, &viol));
+            TRY(shard_certify(S, P, &viol, &cs));
             const double target = SVM_CERT_MARGIN * P.tol;
             if (viol <= target) { P.converged = true; break; }
             P.converged = viol <= P.tol;

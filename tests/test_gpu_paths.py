@@ -369,3 +369,10 @@ def test_incremental_recertification():
     assert viol <= 0.6e-3 + 2e-5, viol
     m0 = pkg.train(ds.X, ds.y, gamma=gamma)   # default margin: the counter is at least 1
     assert m0.info.certifications >= 1
+    # the sharded path (one rank) re-certifies the same way: the same model bit for bit
+    from paper_1706_05544_b200 import binding
+    with env(SVMB200_CERT_MARGIN=0.6):
+        ms = binding.train_sharded_nccl(ds.X, 0, ds.y, 0, 1, binding.nccl_unique_id(), gamma=gamma)
+    assert ms.info.certifications == mi.info.certifications
+    assert ms.info.iterations == mi.info.iterations
+    np.testing.assert_array_equal(ms.support()[1], mi.support()[1])
