@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(PT, 2)
                int64_t nsv_pad, int64_t d, const double* __restrict__ coef, int n_out, KParams kp,
                int tiles_per_split, double* __restrict__ Fpart)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     auto sQ = reinterpret_cast<float (*)[BK][BQ]>(smem_raw);                         // [2][BK][BQ]
     auto sS = reinterpret_cast<float (*)[BK][BS]>(smem_raw + 2 * BK * BQ * 4);       // [2][BK][BS]
     auto sK = reinterpret_cast<float (*)[BS + 1]>(smem_raw + 2 * BK * (BQ + BS) * 4); // [BQ][BS+1]

@@ -60,10 +60,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-__device__ __forceinline__ void named_bar_arrive(int id, int nthreads)
-{
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // 64-bit warp max from two 32-bit REDUX reductions (all lanes participate).
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t k)
@@ -660,7 +656,7 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
             }
         }
         return;
-    }
+    } else {
     // RPT 1 / 2: every row's status, G and norm loaded before the first G store (as above)
     uint32_t stv[RPT][2];
     float gv[RPT][2], xnv[RPT];
@@ -735,6 +731,7 @@ __device__ __forceinline__ void row_epilogue(const SmoArgs& a, const RankView& v
             if (st_in_low(st)) kl[2 * j + c] = ((uint64_t)ord_f32(-sc) << 32) | lo;
         }
     }
+}   // RPT 1 / 2
 }
 
 // Descending sort of a lane's NK keys (odd-even transposition network, fully unrolled).
@@ -998,12 +995,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
-// Bulk prefetch of [p, p + bytes) into L2 (16-byte aligned address and size).
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // 2D tensor copy (TMA) of one box of the map into shared memory, completing on an mbarrier.
@@ -2479,11 +2470,10 @@ __global__ void __launch_bounds__(OVR_PASS_THREADS, 1) k_ovr_pass(const OvrArgs 
 
 __global__ void __launch_bounds__(OVR_THREADS, 1) k_ovr_solve(const OvrArgs a)
 {
-    extern __shared__ __align__(16) unsigned char ovr_smem[];
+    extern __shared__ __align__(1024) unsigned char ovr_smem[];
     float* sXW = reinterpret_cast<float*>(ovr_smem);   // dynamic shared memory: the fp64 X_W below
     __shared__ SmoShared sh;
     __shared__ uint64_t gm[16][8];
-    __shared__ int32_t gms[16][8];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int p = blockIdx.x;
     const int d = (int)a.d;
