@@ -213,6 +213,9 @@ __host__ __device__ constexpr int pf_x() { return RPT == 1 ? 16 : (RPT == 4 ? SM
 template <int RPT>
 __device__ __forceinline__ void cp_async_x(uint32_t dst, const float* src)
 {
+#ifdef SMO_EXP_NOX   // diagnostic build (bound experiments): no X loads, FMAs on stale ring data
+    return;
+#endif
     if constexpr (RPT == 4)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     else if constexpr (RPT == 2)
@@ -241,7 +244,11 @@ __device__ __forceinline__ void x_fma_slot(uint32_t sa, const float4* w4k, float
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[0]) : "r"(sa) : "memory");
     }
     if constexpr (RPT == 4) {
+#ifdef SMO_EXP_NOFMA   // diagnostic build (bound experiments): stream X, no dot FMAs
+        for (int j = 0; j < 4; ++j) acc[j][0] += x[j];
+#else
         fma_rows4_x16(x, w4k, acc);
+#endif
     } else {
         float4 wv[4] = {w4k[0], w4k[1], w4k[2], w4k[3]};
 #pragma unroll
