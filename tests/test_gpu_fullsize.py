@@ -1,4 +1,4 @@
-"""GPU parity for C5 (CSR), whose full-size oracle run does not finish on the host.
+"""GPU parity for C5 (CSR) at its full size, whose full-size oracle run does not finish on the host.
 
 C1-C4 are compared at full size against the oracle's own solutions (tests/test_gpu_golden.py).
 For the CSR config the GPU model is checked on SAMPLED outputs the oracle computes one by one in
@@ -30,6 +30,18 @@ def _cuda():
     pkg.lib()
 
 
+def _csr_rows(ds, rows):
+    """Dense fp32 copies of the given CSR rows (the full 2,000,000 x 400 matrix is 3.2 GB)."""
+    rows = np.asarray(rows, np.int64)
+    out = np.zeros((len(rows), ds.d), np.float32)
+    ip = ds.indptr
+    lens = ip[rows + 1] - ip[rows]
+    owner = np.repeat(np.arange(len(rows)), lens)
+    pos = np.concatenate([np.arange(ip[r], ip[r + 1]) for r in rows]) if len(rows) else np.zeros(0, np.int64)
+    out[owner, ds.indices[pos]] = ds.data[pos]
+    return out
+
+
 def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=200,
                    held_rows=None):
     """prob: which binary problem of the model (one-vs-rest: class index); ybin: its +-1 labels
@@ -48,11 +60,11 @@ def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=
         assert abs(coef.sum()) <= 1e-9 * max(1.0, np.abs(coef).sum())   # sum(a*) = sum(a)
     else:
         assert abs(coef.sum()) <= 1e-9 * max(1.0, np.abs(coef).sum())   # sum y a = 0
-    X = ds.dense() if ds.is_csr else ds.X
-    SV = X[idx]
+    dense_rows = (lambda r: _csr_rows(ds, r)) if ds.is_csr else (lambda r: ds.X[r])
+    SV = dense_rows(idx)
     # sampled fp64 G from the GPU model (decision without b == sum coef K)
     rows = rng.choice(ds.n, size=min(n_sample, ds.n), replace=False)
-    f = ora.decision(SV, coef, 0.0, ks, X[rows])
+    f = ora.decision(SV, coef, 0.0, ks, dense_rows(rows))
     c_row = np.zeros(ds.n)
     c_row[idx] = coef
     up, low = [], []
@@ -98,12 +110,15 @@ def _sample_checks(ds, model, reg, rng, n_sample=300, prob=0, ybin=None, n_held=
     return dec, fo
 
 
-def test_c5_csr_sample_size():
-    """configs[4] recipe (CSR, ~10% density) at 200,000 rows: the full 2M-row problem needs
-    ~3 minutes on one GPU, beyond a test budget; the per-CTA CSR staging path is the same."""
-    ds = synth.make("c5", n=200000)
+def test_c5_full_size_sampled():
+    """BASELINE configs[4] at its full size (2,000,000 x 400 CSR, ~10% density) in the launch
+    configuration bench.py times (one training, ~1 minute): certified, and checked on sampled
+    outputs the oracle computes one by one in fp64 -- KKT over 100 training duals, 100 held-out
+    decision values (940 k support vectors each)."""
+    ds = synth.make("c5")
     import torch
     m = pkg.train_csr(torch.from_numpy(ds.indptr).cuda(), torch.from_numpy(ds.indices).cuda(),
                       torch.from_numpy(ds.data).cuda(), torch.from_numpy(ds.y).cuda(), ds.d,
                       gamma=1.0 / ds.d)
-    _sample_checks(ds, m, False, np.random.default_rng(2), n_sample=200)
+    assert m.info.certifications >= 1
+    _sample_checks(ds, m, False, np.random.default_rng(2), n_sample=100, n_held=100)
