@@ -353,6 +353,9 @@ static int build_sell(Data& D, cudaStream_t st)
     TRY(D.sell_gptr.alloc(sizeof(int64_t) * (ns + 1)));
     CK(cudaMemcpyAsync(D.sell_gptr.p, h.data(), sizeof(int64_t) * (ns + 1), cudaMemcpyHostToDevice, st));
     const int64_t groups = std::max<int64_t>(h[ns], 1);
+    // skewed row lengths pad every slice to its longest row: beyond 4x the CSR bytes (+64 MB) the
+    // per-warp staging path, which reads only the real nonzeros, is kept instead
+    if ((double)groups * 32 * 24 > 4.0 * 8.0 * (double)D.nnz + 64.0 * (1 << 20)) return SVM_OK;
     TRY(D.sell_idx.alloc(sizeof(uint2) * groups * 32));
     TRY(D.sell_val.alloc(sizeof(float4) * groups * 32));
     CK(lay_sell_fill(D.indptr, D.indices, D.vals, D.n, D.d, D.rows_per_cta, spc, ns,
