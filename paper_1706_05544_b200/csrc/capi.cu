@@ -581,7 +581,7 @@ static SmoArgs make_args(const Data& D, Problem& P, Exchange& E, const ShardCtx*
     a.rank_rpc[0] = D.rows_per_cta;
     a.peer_xw[0] = E.buf(0);
     a.timeout_ns = 30ull * 1000000000ull;
-    a.overlap = 2;   // measured: c2 -5%, c4 -2% per iteration vs 1 (all warps in phase A)
+    a.overlap = 2;   // (run_loop: 2 for X resident in shared memory, 1 for streamed X)
     a.qww_mma = (!D.csr && getenv("SVMB200_QWW_MMA") && atoi(getenv("SVMB200_QWW_MMA"))) ? 1 : 0;
     if (const char* e = getenv("SVMB200_OVERLAP")) a.overlap = atoi(e);
     a.info = E.info.as<SmoInfo>();
@@ -746,6 +746,10 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
             smem = base + (int)(8 * 4 * kc * Rs);
         }
     }
+    // phase-A warps while the subproblem runs: X resident in shared memory (c2, chain-bound) keeps
+    // the solver's sub-partition free (2: c2 419 vs 451 ms); streamed X gives it to phase A too
+    // (1: c4 3184 vs 3215 ms, c5 857 vs 860 ms per 3,000 iterations; round-2 measurements)
+    if (!getenv("SVMB200_OVERLAP")) a.overlap = a.x_in_smem ? 2 : 1;
     const int dyn_cap = smo_dyn_smem_cap(a);   // (opt-in maximum - this variant's static SmoShared)
     if (smem > dyn_cap)
         return fail(SVM_EINVAL, "shared-memory need %d B exceeds the SM (d = %lld, %d + %d lists)",
