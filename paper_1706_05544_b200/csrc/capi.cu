@@ -765,17 +765,18 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
         }
     }
     // kernel-column cache: streamed X only (X resident in shared memory costs no
-    // HBM; the wide and TMA pipelines consume every chunk of every iteration); up to 4096 columns
+    // HBM; the wide and TMA pipelines consume every chunk of every iteration); up to 8192 columns
     // within min(12 GiB, 20% of the free device memory) -- inside the pool's retained bound, so
-    // repeated trainings do not re-map it (c4, 16384 columns = 33 GB: +1.2-3 s of mapping per
-    // training, measured).  SVMB200_CACHE = slots (0 = off).
+    // repeated trainings do not re-map it (c4: 6144 columns, bench 3.21 s vs 3.29 s at 4096;
+    // 10240 columns = 20 GB: 3.36 s, re-mapped every training; 16384 = 33 GB: +1.2-3 s).
+    // SVMB200_CACHE = slots (0 = off).
     DBuf cdata, ctag, cstamp;
     if (!a.x_in_smem && !a.wide && !a.x_tma && !a.pass_only) {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const int64_t col = D.n_pad * (int64_t)sizeof(float);
         const double budget = std::min(12.0 * (1ull << 30), 0.2 * (double)fr);
-        int64_t slots = std::min<int64_t>(4096, (int64_t)budget / std::max<int64_t>(col, 1));
+        int64_t slots = std::min<int64_t>(8192, (int64_t)budget / std::max<int64_t>(col, 1));
         if (const char* e = getenv("SVMB200_CACHE")) slots = std::min<int64_t>(atoll(e), 65536);
         slots = slots / 4 * 4;
         const int nctas = a.virt ? a.nblk * a.world : a.nblk;
