@@ -402,6 +402,46 @@ def test_errors_and_edge_cases():
     assert e.value.code == -1
 
 
+@pytest.mark.parametrize("case", ["duplicate_rows_opposite_labels", "svr_eps_covers_all", "tiny_C",
+                                  "constant_and_zero_features"])
+def test_degenerate_cases_vs_oracle(case):
+    """Degenerate instances of Eq. 2 against the oracle (same readings R1-R6): identical rows with
+    opposite labels (tied scores, non-separable), eps-SVR with eps above every |z| (no support
+    vector: f = b only, R6's no-free-dual bias), C so small that every dual ends at a bound, and
+    columns / rows that are entirely zero."""
+    rng = np.random.default_rng(11)
+    n, d = 400, 6
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    y = np.where(X[:, 0] + 0.5 * X[:, 1] > 0, 1.0, -1.0).astype(np.float32)
+    kw, okw = dict(gamma=0.3, tolerance=1e-5), dict(gamma=0.3, tol=1e-5)
+    svm_type = "C-classification"
+    if case == "duplicate_rows_opposite_labels":
+        X[200:260] = X[:60]
+        y[200:260] = -y[:60]
+    elif case == "svr_eps_covers_all":
+        svm_type = "eps-regression"
+        y = (0.1 * X[:, 0]).astype(np.float32)
+        kw["epsilon"] = okw["epsilon"] = float(np.abs(y).max()) + 0.05
+    elif case == "tiny_C":
+        kw["cost"] = okw["C"] = 1e-3
+    else:
+        X[:, 2] = 0.0
+        X[:, 4] = 1.5
+        X[7] = 0.0
+    otype = ora.EPS_REGRESSION if svm_type == "eps-regression" else ora.C_CLASSIFICATION
+    m = pkg.train(X, y, svm_type=svm_type, **kw)
+    r = ora.train(X, y, svm_type=otype, **okw)
+    assert m.info.converged == 1
+    d_ora = r.results[0]["dual"]
+    assert abs(m.info.dual_objective - d_ora) <= 1e-5 * max(1.0, abs(d_ora)), (m.info.dual_objective, d_ora)
+    f_gpu = m.predict(X, decision=True)[1][:, 0]
+    f_ora = r.decision_function(X)[:, 0]
+    np.testing.assert_allclose(f_gpu, f_ora, atol=1e-4)
+    if case == "svr_eps_covers_all":
+        assert m.info.n_sv == 0
+        assert np.ptp(f_gpu) == 0.0   # f = b everywhere
+
+
 def test_partition_invariance_bit_identical():
     """Virtual shards (SURVEY 8(e) invariant): the per-row arithmetic does not depend on which CTA
     owns a row and the candidate merge is exact, so alpha, G and the iteration count are
