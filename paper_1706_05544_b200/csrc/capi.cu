@@ -767,7 +767,7 @@ static int run_loop(const Data& D, Problem& P, Exchange& E, int64_t max_iter, cu
     // kernel-column cache: streamed X only (X resident in shared memory costs no
     // HBM; the wide and TMA pipelines consume every chunk of every iteration); up to 8192 columns
     // within min(12 GiB, 20% of the free device memory) -- inside the pool's retained bound, so
-    // repeated trainings do not re-map it (c4: 6144 columns, bench 3.21 s vs 3.29 s at 4096;
+    // repeated trainings do not re-map it (c4: 6436 columns = the budget, bench 3.20 s; 3.29 s at 4096;
     // 10240 columns = 20 GB: 3.36 s, re-mapped every training; 16384 = 33 GB: +1.2-3 s).
     // SVMB200_CACHE = slots (0 = off).
     DBuf cdata, ctag, cstamp;
